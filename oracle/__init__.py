@@ -1,0 +1,194 @@
+"""TEST INFRASTRUCTURE ONLY — the fp64 CPU oracle for the hot path of arxiv 2504.03651.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg
+and ``--impl reference``) may import this package.  It shares no code with the CUDA
+product in ``paper_2504_03651_b200/``; the only module both sides use is ``workloads``
+(seeded input generators, no method arithmetic).
+
+The arithmetic lives in ``oracle.cpp`` (plain C++17, fp64, no -ffast-math); this file
+only compiles it with g++ and marshals numpy arrays through ctypes.  Every function
+cites the passage it follows (P:n = PAPER.md line n, S:n = SPEC.md line n); readings
+of silent passages are listed in DESIGN.md §3.
+
+Parity pins (tests/test_oracle_*.py): dense unpaged numpy attention, torch SDPA fp64,
+closed forms (ctx=1, constant V, equal keys), block-permutation / sharing / chunking /
+GQA-repeat invariants, brute-force allocation, SPEC eviction examples and a heap free
+table with lazy re-insertion.  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, INVALID, NEEDS_EVICTION, CAPACITY, EVICTION_SHORT, GROUP = 0, 1, 3, 4, 5, 6
+
+# block states for orc_evict_keys (reading #17)
+FREE, RUNNING_ONLINE, PINNED, ACTIVE_OFFLINE, FINISHED_ONLINE, FINISHED_OFFLINE = range(6)
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.cpp -> liboracle.so with g++ (no CUDA, no fast-math)."""
+    if (not force and os.path.exists(_LIB_PATH)
+            and os.path.getmtime(_LIB_PATH) >= os.path.getmtime(_SRC)):
+        return _LIB_PATH
+    tmp = _LIB_PATH + f".tmp{os.getpid()}"
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread",
+                           "-fno-fast-math", "-o", tmp, _SRC])
+    os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            _lib = ctypes.CDLL(build())
+            P = ctypes.c_void_p
+            i32, i64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+            _lib.orc_attention.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32,
+                                           dbl, P, P, P, P, P, ctypes.c_int]
+            _lib.orc_attention_rows.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32,
+                                                dbl, P, P, P, P, P, i64, P, P, ctypes.c_int]
+            _lib.orc_kv_append.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, i32,
+                                           P, P, P, P, P, P]
+            _lib.orc_evict_keys.argtypes = [P, P, P, P, i64, P]
+            _lib.orc_evict_select.argtypes = [P, i64, i64, P, P]
+            _lib.orc_validate.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32]
+            for f in ("orc_attention", "orc_attention_rows", "orc_kv_append",
+                      "orc_evict_keys", "orc_evict_select", "orc_validate"):
+                getattr(_lib, f).restype = ctypes.c_int
+    return _lib
+
+
+def _p(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def _c(a, dtype):
+    return None if a is None else np.ascontiguousarray(a, dtype=dtype)
+
+
+def _bits16(t):
+    """bf16 tensor/array -> contiguous uint16 numpy array of its bit patterns."""
+    try:
+        import torch
+        if isinstance(t, torch.Tensor):
+            t = t.detach().cpu().contiguous()
+            if t.dtype == torch.bfloat16:
+                t = t.view(torch.int16)
+            return t.numpy().view(np.uint16)
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.ascontiguousarray(t)
+    return a.view(np.uint16)
+
+
+def _nthreads(n):
+    return int(n) if n else (os.cpu_count() or 1)
+
+
+def _batch_args(b):
+    return (np.int32(b["num_reqs"]), _c(b["q_indptr"], np.int32), _c(b["ctx_len"], np.int32),
+            _c(b["block_table"], np.int32), _c(b.get("group_of"), np.int32),
+            _c(b.get("group_prefix_blocks"), np.int32))
+
+
+def attention(b: dict, k_pool, v_pool, q, nthreads: int = 0):
+    """Paged causal attention by definition.
+
+    ``b`` keys: num_reqs, num_q_heads, num_kv_heads, head_dim, q_indptr, ctx_len,
+    block_table [R][max_blocks], group_of, group_prefix_blocks, num_blocks, sm_scale.
+    k_pool/v_pool bf16 [num_blocks][Hkv][16][d]; q bf16 [total_q][Hq][d].
+    Returns (status, out fp64 [total_q][Hq][d], lse fp64 [total_q][Hq]).
+    """
+    lib = _load()
+    R, qi, ctx, bt, gof, gpb = _batch_args(b)
+    Hq, Hkv, d = b["num_q_heads"], b["num_kv_heads"], b["head_dim"]
+    kp, vp, qq = _bits16(k_pool), _bits16(v_pool), _bits16(q)
+    total_q = int(qi[-1])
+    out = np.zeros((total_q, Hq, d), np.float64)
+    lse = np.zeros((total_q, Hq), np.float64)
+    st = lib.orc_attention(R, Hq, Hkv, d, _p(qi), _p(ctx), _p(bt), bt.shape[1], _p(gof),
+                           len(gpb) if gpb is not None else 0, _p(gpb), b["num_blocks"],
+                           float(b.get("sm_scale", 0.0) or 0.0), _p(kp), _p(vp), _p(qq),
+                           _p(out), _p(lse), _nthreads(nthreads))
+    return st, out, lse
+
+
+def attention_rows(b: dict, k_pool, v_pool, q, rows, heads, nthreads: int = 0):
+    """Sampled (q_row, head) outputs, each exact by definition (rows are independent)."""
+    lib = _load()
+    R, qi, ctx, bt, gof, gpb = _batch_args(b)
+    Hq, Hkv, d = b["num_q_heads"], b["num_kv_heads"], b["head_dim"]
+    kp, vp, qq = _bits16(k_pool), _bits16(v_pool), _bits16(q)
+    rows = _c(rows, np.int32)
+    heads = _c(heads, np.int32)
+    n = len(rows)
+    out = np.zeros((n, d), np.float64)
+    lse = np.zeros((n,), np.float64)
+    st = lib.orc_attention_rows(R, Hq, Hkv, d, _p(qi), _p(ctx), _p(bt), bt.shape[1], _p(gof),
+                                len(gpb) if gpb is not None else 0, _p(gpb), b["num_blocks"],
+                                float(b.get("sm_scale", 0.0) or 0.0), _p(kp), _p(vp), _p(qq),
+                                _p(rows), _p(heads), n, _p(out), _p(lse), _nthreads(nthreads))
+    return st, out, lse
+
+
+def kv_append(b: dict, k_pool, v_pool, free_bits, k_new, v_new):
+    """KV append + smallest-free-id allocation (Eq.(5)).
+
+    Works on copies; returns (status, deficit, k_pool', v_pool', block_table', free_bits')
+    with the pools as uint16 bit arrays.
+    """
+    lib = _load()
+    R, qi, ctx, bt, gof, gpb = _batch_args(b)
+    bt = bt.copy()
+    Hkv, d = b["num_kv_heads"], b["head_dim"]
+    kp, vp = _bits16(k_pool).copy(), _bits16(v_pool).copy()
+    fb = _c(free_bits, np.uint32).copy()
+    kn, vn = _bits16(k_new), _bits16(v_new)
+    deficit = np.zeros(1, np.int32)
+    st = lib.orc_kv_append(R, Hkv, d, _p(qi), _p(ctx), _p(bt), bt.shape[1], _p(gof),
+                           len(gpb) if gpb is not None else 0, _p(gpb), b["num_blocks"],
+                           _p(kp), _p(vp), _p(fb), _p(kn), _p(vn), _p(deficit))
+    return st, int(deficit[0]), kp, vp, bt, fb
+
+
+def evict_keys(state, rc, lat, depth=None):
+    """priority_of as order-preserving u64 keys (readings #15-#20)."""
+    lib = _load()
+    st_ = _c(state, np.uint8)
+    rc_ = _c(rc, np.uint32)
+    lat_ = _c(lat, np.uint32)
+    dep = _c(depth, np.uint16)
+    n = len(st_)
+    keys = np.zeros(n, np.uint64)
+    s = lib.orc_evict_keys(_p(st_), _p(rc_), _p(lat_), _p(dep), n, _p(keys))
+    return s, keys
+
+
+def evict_select(keys, k: int):
+    """Eviction order: (key, id) ascending, first k."""
+    lib = _load()
+    kk = _c(keys, np.uint64)
+    out = np.full(max(int(k), 0), -1, np.int32)
+    nsel = np.zeros(1, np.int64)
+    s = lib.orc_evict_select(_p(kk), len(kk), int(k), _p(out), _p(nsel))
+    return s, out[: int(nsel[0])]
+
+
+def validate(b: dict):
+    lib = _load()
+    R, qi, ctx, bt, gof, gpb = _batch_args(b)
+    return lib.orc_validate(R, b["num_q_heads"], b["num_kv_heads"], b["head_dim"], _p(qi),
+                            _p(ctx), _p(bt), bt.shape[1], _p(gof),
+                            len(gpb) if gpb is not None else 0, _p(gpb), b["num_blocks"])
