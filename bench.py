@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py — one iteration of the co-scheduled serving loop's device hot path per step
+(SURVEY §8(a) rows a1-a8): kv_append (+ block allocation) -> hybrid_attention (plan + tile /
+decode split-KV / LSE-merge kernels) -> [G>1: NCCL all-gather of O over NVLink] ->
+evict_keys + evict_select (1M-block pool, top-64k) -> release of this step's blocks.
+
+Contract: `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on rank 0.
+`--impl reference` times the fp64 CPU oracle (the reference arm of this tier) instead.
+The default workload is BASELINE.json configs[1] (Llama-2-7B-shaped mixed batch with a shared
+offline prefix, "llama7b"); inputs are seeded synthetic (workloads/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "mixed-batch attention tokens/s and HBM GB/s (% of B200 roofline) at 1/2/4/8 GPUs"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama7b")
+    ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region (200 ms)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6448.1), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel="decode_kernel"):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import paper_2504_03651_b200 as K
+    import workloads as W
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    cfg = W.get_config(args.config)
+    wl = W.make_workload(cfg, device=dev, rank=rank, world=world)
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    pool = K.Pool(wl.k_pool, wl.v_pool, K.free_bits_tensor(wl.free_bits, dev))
+    batch = K.Batch(wl.batch, dev)
+    pristine_dev = batch.table_dev.clone()
+    pristine_host = batch.table_host.copy()
+    new_mask = pristine_host == -1
+    ws_app = torch.empty(K.kv_append_workspace_size(batch), dtype=torch.uint8, device=dev)
+    ws_att = torch.empty(K.hybrid_attention_workspace_size(batch), dtype=torch.uint8, device=dev)
+    q, k_new, v_new = wl.q, wl.k_new, wl.v_new
+    T, Hl, d = q.shape
+    out = torch.empty((T, Hl, d), dtype=out_dtype, device=dev)
+    lse = torch.empty((T, Hl), dtype=torch.float32, device=dev)
+    gbuf = torch.empty((world, T, Hl, d), dtype=out_dtype, device=dev) if world > 1 else None
+
+    ev = None
+    if not args.no_evict:
+        evw = W.make_evict()
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)
+        ev = dict(state=t(evw.state, np.uint8), rc=t(evw.rc, np.int32), lat=t(evw.lat, np.int32),
+                  depth=t(evw.depth, np.int16), k=evw.k, n=len(evw.state))
+        ev["keys"] = torch.empty(ev["n"], dtype=torch.int64, device=dev)
+        ev["ids"] = torch.empty(ev["k"], dtype=torch.int32, device=dev)
+        ev["ws"] = torch.empty(K.evict_select_workspace_size(ev["n"], ev["k"]), dtype=torch.uint8, device=dev)
+
+    # e2e host buffers (pinned): inputs in, output out, every step
+    h_q = q.cpu().pin_memory()
+    h_k = k_new.cpu().pin_memory()
+    h_v = v_new.cpu().pin_memory()
+    h_out = torch.empty((gbuf if world > 1 else out).shape, dtype=out.dtype).pin_memory()
+
+    launches = {"n": 0}
+    dec_ev = []
+
+    def step(e2e=False, time_decode=False):
+        batch.table_dev.copy_(pristine_dev, non_blocking=True)
+        batch.table_host[...] = pristine_host
+        if e2e:
+            q.copy_(h_q, non_blocking=True)
+            k_new.copy_(h_k, non_blocking=True)
+            v_new.copy_(h_v, non_blocking=True)
+        K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
+        plan = K.Plan(pool, batch, ws_att, stream=stream)
+        n = 2 + plan.launch_count()
+        if time_decode:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            plan.run(q, out, lse, stream=stream, phases=K.PHASE_TILE)
+            a.record(stream)
+            plan.run(q, out, lse, stream=stream, phases=K.PHASE_DECODE)
+            b.record(stream)
+            plan.run(q, out, lse, stream=stream, phases=K.PHASE_MERGE)
+            dec_ev.append((a, b))
+        else:
+            plan.run(q, out, lse, stream=stream)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gbuf, out)
+        if ev is not None:
+            K.evict_keys(ev["state"], ev["rc"], ev["lat"], ev["depth"], keys=ev["keys"], stream=stream)
+            K.evict_select(ev["keys"], ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=stream,
+                           sync=False)
+            n += 2
+        if e2e:
+            h_out.copy_(gbuf if world > 1 else out, non_blocking=True)
+        allocated = batch.table_host[new_mask]
+        K.kv_release_blocks(pool, allocated, stream=stream)
+        n += 1
+        launches["n"] += n
+        plan.close()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def timed(nsteps, e2e=False, time_decode=False):
+        barrier()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(nsteps):
+            step(e2e=e2e, time_decode=time_decode)
+        e.record(stream)
+        barrier()
+        ms = s.elapsed_time(e) / nsteps
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    plan0 = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
+    stats = plan0.stats()
+    plan0.close()
+
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+    launches["n"] = 0
+    ms = timed(args.steps, time_decode=True)
+    gpu_launches = launches["n"]
+    ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+    dec_ms = [a.elapsed_time(b) for a, b in dec_ev]
+    ms_e2e = None
+    if not args.no_e2e and not args.profile:
+        for _ in range(2):
+            step(e2e=True)
+        ms_e2e = timed(args.steps, e2e=True)
+
+    tokens = T  # query tokens of the batch (every rank holds all tokens for its heads)
+    g = Hl // wl.batch["num_kv_heads"]
+    dec_rows_tok = sum(int(wl.batch["q_indptr"][i + 1] - wl.batch["q_indptr"][i])
+                       for i in range(wl.batch["num_reqs"])
+                       if (wl.batch["q_indptr"][i + 1] - wl.batch["q_indptr"][i]) * g <= 16)
+    dec_bytes = stats["decode_kv_bytes"] + dec_rows_tok * Hl * d * 2
+    dec_avg = statistics.mean(dec_ms) if dec_ms else float("nan")
+    peak, peak_src = measured_peaks()
+    achieved = dec_bytes / (dec_avg * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[1])" if args.config == "llama7b" else args.config,
+                   "q_tokens": tokens, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "head_dim": cfg.d,
+                   "requests": len(cfg.reqs), "parallelism": f"kv-head shard x{world}",
+                   "kv_bytes_algorithmic_per_rank": stats["kv_bytes_algorithmic"],
+                   "flops_per_rank": stats["flops"],
+                   "step": "kv_append+hybrid_attention(plan,tile,decode,merge)" +
+                           ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+evict_keys+evict_select(1M,k=64k)") +
+                           "+release",
+                   "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
+                   "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype},
+        "roofline": {"bound": "hbm", "kernel": "decode_kernel (split-KV)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(), "bytes_per_launch": dec_bytes, "peak_source": peak_src},
+        "clocks": ck, "gpu_launches": gpu_launches,
+    }
+    if ms_e2e is not None:
+        res["e2e"] = {"value": tokens / (ms_e2e * 1e-3), "unit": UNIT,
+                      "h2d_bytes_per_step": int(h_q.numel() * 2 + h_k.numel() * 2 + h_v.numel() * 2),
+                      "d2h_bytes_per_step": int(h_out.numel() * h_out.element_size()),
+                      "ms_per_step": ms_e2e}
+    return res, wl
+
+
+def _post_append_batch(K, wl, dev):
+    """Descriptor with every block allocated (for plan statistics only)."""
+    b = dict(wl.batch)
+    bt = b["block_table"].copy()
+    nxt = 0
+    free = [i for i in range(b["num_blocks"]) if (int(wl.free_bits[i // 32]) >> (i % 32)) & 1]
+    for i in range(b["num_reqs"]):
+        for k in range((int(b["ctx_len"][i]) + 15) // 16):
+            if bt[i, k] == -1:
+                bt[i, k] = free[nxt]
+                nxt += 1
+    b["block_table"] = bt
+    return K.Batch(b, dev)
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_sample(wl, seconds, seed=0):
+    """Time the fp64 oracle on a bounded random sample of (row, head) pairs of the batch."""
+    import oracle
+    import workloads as W  # noqa: F401
+    cpu = W_cpu(wl)
+    st, _, kp, vp, bt, fb = oracle.kv_append(cpu.batch, cpu.k_pool, cpu.v_pool, cpu.free_bits,
+                                             cpu.k_new, cpu.v_new)
+    b = dict(cpu.batch, block_table=bt)
+    Hq = b["num_q_heads"]
+    rng = np.random.default_rng(seed)
+    nthreads = os.cpu_count() or 1
+    n = max(nthreads, 16)
+    while True:
+        rows = rng.integers(0, cpu.total_q, n).astype(np.int32)
+        heads = rng.integers(0, Hq, n).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.attention_rows(b, kp, vp, cpu.q, rows, heads, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        if dt >= seconds * 0.5 or n >= 1 << 22:
+            break
+        n = int(n * min(16.0, max(2.0, seconds / max(dt, 1e-3))))
+    return {"value": (n / Hq) / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": f"{n} random (query row, q-head) pairs of the {wl.cfg.name} batch, fp64 C++ "
+                      f"oracle attention only ({dt:.1f} s; tokens = pairs / Hq)", "seconds": dt}
+
+
+def W_cpu(wl):
+    import workloads as W
+    if wl.k_pool.device.type == "cpu":
+        return wl
+    return W.Workload(wl.cfg, wl.batch, wl.k_pool.cpu(), wl.v_pool.cpu(), wl.free_bits,
+                      wl.k_new.cpu(), wl.v_new.cpu(), wl.q.cpu(), wl.head_range, wl.kv_head_range)
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the fp64 CPU oracle (this tier has no reference implementation)."""
+    import workloads as W
+    if rank != 0:
+        return None
+    wl = W.make_workload(args.config, device="cpu")
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(wl, per_step * 0.2, seed=1)
+    vals, secs = [], 0.0
+    last = None
+    for s in range(args.steps):
+        last = oracle_sample(wl, per_step, seed=100 + s)
+        vals.append(last["value"])
+        secs += last["seconds"]
+    v = statistics.mean(vals)
+    cfg = W.get_config(args.config)
+    return {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": args.config, "q_tokens": wl.total_q, "Hq": cfg.Hq, "Hkv": cfg.Hkv,
+                   "head_dim": cfg.d},
+        "cpu_baseline": dict(last, value=v),
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    rank, world, local = dist_setup(args)
+    res, wl = run_ours(args, rank, world, local)
+    if rank == 0:
+        if not args.no_cpu_baseline and not args.profile and world == 1:
+            res["cpu_baseline"] = oracle_sample(wl, args.cpu_seconds)
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,232 @@
+/*
+ * kvattn.h — C ABI of the B200-native hybrid paged-attention library (libkvattn.so).
+ *
+ * The library implements the device hot path of one iteration of the co-scheduled
+ * online/offline serving loop of arxiv 2504.03651 (citation keys: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n; "reading #n" = DESIGN.md §3):
+ *   1. kv_append        — append this iteration's K/V into the paged pool, allocating
+ *                          blocks deterministically ("appending the corresponding KV
+ *                          state to the cache"; P:328 fixed-size blocks; Eq.(5)).
+ *   2. hybrid_attention — one attention step for a MIXED batch of online decodes and
+ *                          offline chunked prefills in which
+ *                          offline tasks share resident prefix blocks.
+ *   3. evict_keys/evict_select — the task-aware eviction order: priority then
+ *                          last access time, as kept by the free table.
+ *
+ * Conventions (all calls):
+ *   - Every call returns kva_status; nothing throws or exits across the ABI.  On error a
+ *     thread-local message is available from kva_last_error().
+ *   - All descriptor validation runs on the host, synchronously, BEFORE anything is
+ *     enqueued; an error status means no device work was enqueued and no state changed.
+ *   - Device work is enqueued on the caller's stream (NULL = legacy default stream) and
+ *     the call returns after enqueue, except where a host output needs a device result
+ *     (documented per call: evict_select's n_selected, kv_pool_create's free count).
+ *   - Pointers marked "device" must be device memory of the pool's device; "host" are host
+ *     memory.  All device buffers are caller-owned (PyTorch allocates them); the library
+ *     owns only its opaque handles, host planning scratch and pinned staging buffers.
+ *   - bf16 = IEEE bfloat16 bit pattern (uint16).  Block size is fixed at 16 tokens
+ *     (reading #5).  head_dim must be 64 or 128 (else KVA_ERR_UNSUPPORTED).
+ *   - Single writer per pool: calls on one pool must not run concurrently.
+ */
+#ifndef KVATTN_H_
+#define KVATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *kva_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  KVA_OK = 0,
+  KVA_ERR_INVALID = 1,      /* shape / pointer / descriptor error ("domain error") */
+  KVA_ERR_UNSUPPORTED = 2,  /* head_dim not in {64,128}, block_size != 16, ...            */
+  KVA_NEEDS_EVICTION = 3,   /* kv_append: free blocks < needed; *deficit_blocks set;
+                               NO state change                                 */
+  KVA_ERR_CAPACITY = 4,     /* one request needs more blocks than the pool has      */
+  KVA_EVICTION_SHORT = 5,   /* evict_select: fewer than k evictable blocks; the first
+                               n_selected ids are valid (S:147 EvictionImpossible)         */
+  KVA_ERR_GROUP = 6,        /* shared-prefix precondition violated (reading #8)             */
+  KVA_ERR_CUDA = 7          /* CUDA runtime / launch error                                  */
+} kva_status;
+
+/* Thread-local text of the last error (never NULL). */
+const char *kva_last_error(void);
+/* Library build string (compile target, version). */
+const char *kva_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * Pool.  The paged KV cache of P:328 ("the KV cache is divided into fixed-sized blocks
+ * ... enabling efficient and non-contiguous memory allocation").
+ *   k_pool, v_pool : device bf16 [num_blocks][num_kv_heads][16][head_dim]  (caller-owned)
+ *                    num_kv_heads is the LOCAL count (heads sharded over G ranks, §8(e)).
+ *   free_bits      : device uint32 [ceil(num_blocks/32)], bit b%32 of word b/32 set = block
+ *                    b free (caller-owned).  The library keeps a host mirror of it (it is
+ *                    the single writer after create) and uses it to allocate blocks.
+ * kv_pool_create reads free_bits once (synchronous device->host copy).
+ * ------------------------------------------------------------------------------------ */
+typedef struct kva_pool kva_pool;
+typedef struct {
+  int32_t num_blocks;
+  int32_t block_size;   /* must be 16 */
+  int32_t num_kv_heads; /* local */
+  int32_t head_dim;     /* 64 | 128 */
+  void *k_pool;
+  void *v_pool;
+  uint32_t *free_bits;
+  int32_t device;       /* CUDA ordinal the buffers live on */
+} kva_pool_desc;
+
+kva_status kv_pool_create(const kva_pool_desc *desc, kva_pool **out);
+/* Frees library-owned host state only; never frees caller memory. */
+kva_status kv_pool_destroy(kva_pool *pool);
+/* Number of free blocks according to the library's mirror (host, no sync). */
+kva_status kv_pool_free_count(const kva_pool *pool, int64_t *n_free);
+/* Re-read free_bits from the device (synchronous) after the caller edited it. */
+kva_status kv_pool_resync(kva_pool *pool);
+
+/* ------------------------------------------------------------------------------------
+ * Batch descriptor: the iteration's batch T_i of prefill chunks + decode tokens (P:172,
+ * P:226-228).  R = num_reqs.  Request i owns query rows [q_indptr[i], q_indptr[i+1])
+ * (q_len_i = q_indptr[i+1]-q_indptr[i] >= 1) at absolute positions [ctx_i - q_len_i, ctx_i);
+ * ctx_len[i] is its KV length AFTER this step's append (readings #2-#4).  A query at
+ * position p attends to keys [0, p] (causal).
+ * Shared-prefix groups: group_of[i] = -1 or a group index;
+ * group g covers the first group_prefix_blocks[g] blocks; every member's first
+ * group_prefix_blocks[g] table entries must equal the group's blocks (those of its first
+ * member) and every member's queries must lie after the prefix, else KVA_ERR_GROUP.
+ * Grouping never changes results (reading #7); it changes how blocks are read.
+ * ------------------------------------------------------------------------------------ */
+enum { KVA_ONLINE_DECODE = 0, KVA_OFFLINE_PREFILL = 1, KVA_OFFLINE_DECODE = 2,
+       KVA_ONLINE_PREFILL = 3 };
+enum { KVA_OUT_BF16 = 0, KVA_OUT_F32 = 1 };
+
+typedef struct {
+  int32_t num_reqs;
+  int32_t num_q_heads;              /* local; num_q_heads % num_kv_heads == 0 */
+  int32_t num_kv_heads;             /* local; must equal the pool's */
+  int32_t head_dim;
+  const int32_t *req_type;          /* host [R]; planning/metrics only (nullable) */
+  const int32_t *q_indptr;          /* host [R+1], q_indptr[0] = 0, non-decreasing */
+  const int32_t *ctx_len;           /* host [R] */
+  int32_t *block_table;             /* device [R][max_blocks] int32, -1 = unallocated */
+  int32_t *block_table_host;        /* host mirror [R][max_blocks]; kv_append writes the
+                                       ids it allocates into BOTH tables */
+  int32_t max_blocks;
+  const int32_t *group_of;          /* host [R] (nullable = no groups) */
+  int32_t num_groups;
+  const int32_t *group_prefix_blocks; /* host [num_groups] */
+  float sm_scale;                   /* <= 0 -> 1/sqrt(head_dim) (reading #1) */
+} kva_batch_desc;
+
+/* Host-only descriptor check (no device work): mode 0 = as hybrid_attention validates it
+ * (every block of [0, ctx) allocated), mode 1 = as kv_append does (resident part only).
+ * Returns the status the corresponding call would return for descriptor errors. */
+kva_status kva_validate_batch(const kva_batch_desc *desc, int32_t num_blocks, int32_t mode);
+
+/* ------------------------------------------------------------------------------------
+ * kv_append (a2).  For each request in descriptor order and each new position t in
+ * [ctx-q_len, ctx) ascending: if table[i][t/16] == -1 the smallest free block id is taken
+ * (reading #13; a partially filled last block is filled first, reading #14), then the K/V
+ * row of every local kv-head is written to slot (table[i][t/16], t % 16).
+ *   k_new, v_new : device bf16 [total_q][num_kv_heads][head_dim]; token stride
+ *                  new_stride_tok elements (>= num_kv_heads*head_dim), heads contiguous.
+ *   workspace    : device scratch of kv_append_workspace_size() bytes (16-B aligned).
+ * Errors: KVA_NEEDS_EVICTION (needed > free, *deficit_blocks = needed - free, nothing
+ * enqueued); KVA_ERR_CAPACITY (ceil(ctx/16) > num_blocks for some request);
+ * KVA_ERR_GROUP (an appended position inside a group prefix); KVA_ERR_INVALID.
+ * ------------------------------------------------------------------------------------ */
+kva_status kv_append_workspace_size(const kva_batch_desc *desc, size_t *bytes);
+kva_status kv_append(kva_pool *pool, kva_batch_desc *desc, const void *k_new,
+                     const void *v_new, int64_t new_stride_tok, int32_t *deficit_blocks,
+                     void *workspace, size_t workspace_bytes, kva_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * hybrid_attention (a1 plan + a3..a6).  out[row][h][:] = softmax over keys [0, p] of
+ * (q . k) * sm_scale, times V, for every query row and local q-head h (kv-head
+ * h / (Hq/Hkv), reading #9); lse[row][h] = natural-log log-sum-exp of the scaled scores.
+ *   q   : device bf16, element (row, h, c) at q[row*q_stride_tok + h*q_stride_head + c]
+ *   out : device, bf16 (KVA_OUT_BF16) or fp32 (KVA_OUT_F32), same indexing with o_stride_*
+ *   lse : device fp32 [total_q][num_q_heads] (nullable)
+ *   workspace : device scratch of hybrid_attention_workspace_size() bytes.
+ * hybrid_attention = hybrid_attention_plan + hybrid_attention_run.  The plan (host work
+ * lists uploaded into the workspace on `stream`) can be reused by several runs — e.g.
+ * every layer of a model — while the descriptor is unchanged; runs enqueue kernels only
+ * (CUDA-graph capturable).  Errors: KVA_ERR_GROUP, KVA_ERR_INVALID, KVA_ERR_UNSUPPORTED.
+ * ------------------------------------------------------------------------------------ */
+typedef struct kva_plan kva_plan;
+kva_status hybrid_attention_workspace_size(const kva_batch_desc *desc, size_t *bytes);
+kva_status hybrid_attention_plan(kva_pool *pool, const kva_batch_desc *desc, void *workspace,
+                                 size_t workspace_bytes, kva_stream_t stream, kva_plan **plan);
+kva_status hybrid_attention_run(const kva_plan *plan, const void *q, int64_t q_stride_tok,
+                                int64_t q_stride_head, void *out, int64_t o_stride_tok,
+                                int64_t o_stride_head, int32_t out_dtype, float *lse,
+                                kva_stream_t stream);
+/* Run only some phases of a plan (profiling / per-kernel timing inside a step); phases is a
+ * mask of KVA_PHASE_*.  Running TILE|DECODE then MERGE in order equals hybrid_attention_run. */
+enum { KVA_PHASE_TILE = 1, KVA_PHASE_DECODE = 2, KVA_PHASE_MERGE = 4, KVA_PHASE_ALL = 7 };
+kva_status hybrid_attention_run_phases(const kva_plan *plan, const void *q, int64_t q_stride_tok,
+                                       int64_t q_stride_head, void *out, int64_t o_stride_tok,
+                                       int64_t o_stride_head, int32_t out_dtype, float *lse,
+                                       int32_t phases, kva_stream_t stream);
+/* Number of kernel launches hybrid_attention_run_phases(plan, phases) enqueues. */
+kva_status kva_plan_launch_count(const kva_plan *plan, int32_t phases, int32_t *n_launches);
+kva_status kva_plan_destroy(kva_plan *plan);
+/* Plan statistics: counts of work items per kernel and algorithmic bytes/flops. */
+typedef struct {
+  int64_t n_decode_items, n_tile_items, n_cascade_items, n_merge_rows;
+  int64_t kv_bytes_algorithmic;     /* distinct KV bytes (prefix once per group/kv-head) */
+  int64_t q_bytes, o_bytes;         /* bf16 Q read + O written */
+  int64_t decode_kv_bytes;          /* KV bytes read by the split-KV (decode) kernel */
+  int64_t flops;                    /* 4*d per (q-head, query, visible key) */
+} kva_plan_stats;
+kva_status kva_plan_get_stats(const kva_plan *plan, kva_plan_stats *stats);
+kva_status hybrid_attention(kva_pool *pool, const kva_batch_desc *desc, const void *q,
+                            int64_t q_stride_tok, int64_t q_stride_head, void *out,
+                            int64_t o_stride_tok, int64_t o_stride_head, int32_t out_dtype,
+                            float *lse, void *workspace, size_t workspace_bytes,
+                            kva_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Eviction (a8).  Block states (S:103 BlockMeta.task_class + reading #17):
+ *   0 free, 1 running-online, 2 pinned (referenced by this iteration's batch),
+ *   3 active-offline, 4 finished-online, 5 finished-offline.
+ * evict_keys: priority_of as an order-preserving u64 key:
+ *   free / running-online / pinned -> UINT64_MAX (never selected)
+ *   rc > 0 -> priority rc ; finished-online (rc 0) -> 0.5 ; other offline (rc 0) -> 0
+ *   code16 = min(2*priority, 0xFFFE);
+ *   key = code16 << 48 | lat32 << 16 | (0xFFFF - min(depth, 0xFFFF))      (readings #18-#20)
+ *   state, rc, lat, depth: device arrays [n] (uint8, uint32, uint32, uint16; depth nullable
+ *   => 0).  Unknown state -> UINT64_MAX and KVA_ERR_INVALID is NOT detected on device.
+ * evict_select: the k blocks with the smallest (key, block id), in that order (P:338
+ *   "first consider the priority ... then the last access time").
+ *   out_ids: device int32 [k].  *n_selected (host) = min(k, #evictable) — this implies one
+ *   stream synchronisation; n_selected = NULL enqueues only (no sync, no SHORT status; the
+ *   unused tail of out_ids is left untouched), which apply != 0 does not allow.  apply != 0 marks the selected blocks free in free_bits and in
+ *   the pool's host mirror (pool required then).  KVA_EVICTION_SHORT if fewer than k.
+ *   workspace: evict_select_workspace_size(n, k) bytes of device scratch.
+ * ------------------------------------------------------------------------------------ */
+/* kv_release_blocks: return blocks to the free pool (recompute-mode preemption or a
+ * finished request whose KV is dropped, "preempts and release the KV cache of the
+ * victim request").  ids: HOST int32 [n], each allocated (not free) and distinct, else
+ * KVA_ERR_INVALID with no change.  Sets the device free bits on `stream` and the mirror. */
+kva_status kv_release_blocks(kva_pool *pool, const int32_t *ids, int64_t n, kva_stream_t stream);
+
+enum { KVA_BLK_FREE = 0, KVA_BLK_RUNNING_ONLINE = 1, KVA_BLK_PINNED = 2,
+       KVA_BLK_ACTIVE_OFFLINE = 3, KVA_BLK_FINISHED_ONLINE = 4, KVA_BLK_FINISHED_OFFLINE = 5 };
+
+kva_status evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
+                      const uint16_t *depth, int64_t n, uint64_t *keys_out,
+                      kva_stream_t stream);
+kva_status evict_select_workspace_size(int64_t n, int64_t k, size_t *bytes);
+kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
+                        int64_t *n_selected, int32_t apply, kva_pool *pool, void *workspace,
+                        size_t workspace_bytes, kva_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVATTN_H_ */

@@ -1,0 +1,272 @@
+// kernels_decode.cu — split-KV paged decode attention.
+//
+// The decode stage "uses the KV cache to generate a single token at a time ... memory-bound
+// due to the high frequency of KV cache access"; Eq.(7) P:389-391 models its time
+// as gamma*max(L) + delta*mean(L) — the max(L) term is load imbalance that fixed-length
+// splits (kSplitKeys, depending only on ctx) remove.
+//
+// Design (B200): one WARP per work item = (request, kv-head, split of <= 512 keys), rows =
+// q_len x g <= 16 packed along the MMA M dimension (GQA heads share the K/V bytes).  Each
+// warp streams its split's 16-token blocks (K and V, 2*16*d*2 bytes) through its own
+// NST-stage ring in shared memory with 2-D TMA (cp.async.bulk.tensor, 128-B swizzle) and
+// one mbarrier per stage; lane 0 is the producer.  QK^T and PV run on mma.sync bf16 with fp32
+// accumulation (legacy tensor path: ~10x headroom over what the HBM stream needs, H2);
+// softmax is online in fp32 with quad shuffles.  Blocks of the split are looked up once
+// (lane j holds block j's id).  Output: normalised partial (O, lse) per split, or the final
+// output when the item is the row's only contribution.
+#include <cuda.h>
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace kva {
+using namespace dev;
+
+template <int D, int NST>
+__global__ void __launch_bounds__(128, 2)
+    decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
+                  const __grid_constant__ CUtensorMap tmv, const DecodeItem *__restrict__ items,
+                  int n_items) {
+  constexpr int HALVES = D / 64;
+  constexpr int KBYTES = 16 * D * 2;  // K (or V) of one block for one head
+  constexpr int STAGE = 2 * KBYTES;
+  constexpr int KT = D / 16;          // k-steps of the QK^T contraction
+  constexpr int NT = D / 8;           // n-tiles of the PV output
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[4][NST];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item_idx = blockIdx.x * 4 + warp;
+  if (item_idx >= n_items) return;  // no CTA-wide barrier below
+  const DecodeItem it = items[item_idx];
+  uint8_t *sbase = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  uint8_t *ws = sbase + warp * NST * STAGE;
+  uint64_t *bar = bars[warp];
+  const int g = p.g;
+  const int n_rows = it.n_tok * g;
+
+  if (lane == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int b0 = it.k0 / kBlock;
+  const int nblk = (it.k1 + kBlock - 1) / kBlock - b0;  // <= 32
+  const int32_t *trow = p.block_table + (int64_t)it.table_row * p.max_blocks + b0;
+  const int my_id = lane < nblk ? __ldg(trow + lane) : 0;
+  const int row_base = it.kv_head * kBlock;  // + id*Hkv*16
+
+  auto issue = [&](int st, int id) {  // lane 0 only
+    uint64_t *b = &bar[st];
+    mbar_arrive_expect_tx(b, STAGE);
+    const int row = id * p.Hkv * kBlock + row_base;
+    uint8_t *dst = ws + st * STAGE;
+#pragma unroll
+    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
+#pragma unroll
+    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
+  };
+
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int id = __shfl_sync(0xffffffffu, my_id, s);
+    if (lane == 0 && s < nblk) issue(s, id);
+  }
+
+  // Q fragments (A operand, rows = tok*g + hh)
+  const int r_lo = lane >> 2, r_hi = r_lo + 8;
+  const int cq = (lane & 3) * 2;
+  uint32_t qa[KT][4];
+  {
+    const uint32_t *qlo = nullptr, *qhi = nullptr;
+    if (r_lo < n_rows)
+      qlo = reinterpret_cast<const uint32_t *>(
+          p.q + (int64_t)(it.q_row0 + r_lo / g) * p.q_stride_tok +
+          (int64_t)(it.kv_head * g + r_lo % g) * p.q_stride_head);
+    if (r_hi < n_rows)
+      qhi = reinterpret_cast<const uint32_t *>(
+          p.q + (int64_t)(it.q_row0 + r_hi / g) * p.q_stride_tok +
+          (int64_t)(it.kv_head * g + r_hi % g) * p.q_stride_head);
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      const int c = kk * 16 + cq;
+      qa[kk][0] = qlo ? __ldg(qlo + c / 2) : 0u;
+      qa[kk][1] = qhi ? __ldg(qhi + c / 2) : 0u;
+      qa[kk][2] = qlo ? __ldg(qlo + (c + 8) / 2) : 0u;
+      qa[kk][3] = qhi ? __ldg(qhi + (c + 8) / 2) : 0u;
+    }
+  }
+  const int pos_lo = it.pos0 + r_lo / g, pos_hi = it.pos0 + r_hi / g;
+
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_lo = -CUDART_INF_F, m_hi = -CUDART_INF_F, l_lo = 0.f, l_hi = 0.f;
+  const float sl2 = p.scale_log2;
+
+  for (int j = 0; j < nblk; ++j) {
+    const int st = j % NST;
+    const int next_id = __shfl_sync(0xffffffffu, my_id, (j + NST) & 31);
+    mbar_wait(&bar[st], (j / NST) & 1);
+    const uint32_t kb = smem_u32(ws + st * STAGE), vb = kb + KBYTES;
+    const int key0 = (b0 + j) * kBlock;
+    if (key0 + kBlock > it.k1) {
+      // never-written slots of the last block are NaN-poisoned: zero those V rows
+      const int vr = it.k1 - key0;  // valid rows
+      uint8_t *vp = ws + st * STAGE + KBYTES;
+      for (int c = lane; c < (16 - vr) * HALVES * 8; c += 32) {
+        const int h = c / ((16 - vr) * 8), rem = c % ((16 - vr) * 8);
+        const int row = vr + rem / 8, ch = rem % 8;
+        *reinterpret_cast<uint4 *>(vp + h * 2048 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    // S = Q K^T  (16 rows x 16 keys)
+    float s[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+    {
+      const int key = (lane >> 4) * 8 + (lane & 7);
+      const int csub = ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk) {
+        const int col = kk * 16 + csub;
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4(kb + (col >> 6) * 2048 + sw128(key, col & 63), r0, r1, r2, r3);
+        mma_bf16(s[0], qa[kk], r0, r1);
+        mma_bf16(s[1], qa[kk], r2, r3);
+      }
+    }
+    // mask + scale (log2 domain)
+    float mx_lo = -CUDART_INF_F, mx_hi = -CUDART_INF_F;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = key0 + n * 8 + cq + (e & 1);
+        const int pos = (e >> 1) ? pos_hi : pos_lo;
+        const bool ok = key >= it.k0 && key < it.k1 && key <= pos;
+        s[n][e] = ok ? s[n][e] * sl2 : -CUDART_INF_F;
+      }
+      mx_lo = fmaxf(mx_lo, fmaxf(s[n][0], s[n][1]));
+      mx_hi = fmaxf(mx_hi, fmaxf(s[n][2], s[n][3]));
+    }
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+    const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
+    const float base_lo = mn_lo == -CUDART_INF_F ? 0.f : mn_lo;
+    const float base_hi = mn_hi == -CUDART_INF_F ? 0.f : mn_hi;
+    const float a_lo = fast_exp2(m_lo - base_lo), a_hi = fast_exp2(m_hi - base_hi);
+    m_lo = mn_lo;
+    m_hi = mn_hi;
+    float ps_lo = 0.f, ps_hi = 0.f;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      s[n][0] = fast_exp2(s[n][0] - base_lo);
+      s[n][1] = fast_exp2(s[n][1] - base_lo);
+      s[n][2] = fast_exp2(s[n][2] - base_hi);
+      s[n][3] = fast_exp2(s[n][3] - base_hi);
+      ps_lo += s[n][0] + s[n][1];
+      ps_hi += s[n][2] + s[n][3];
+    }
+    l_lo = l_lo * a_lo + ps_lo;
+    l_hi = l_hi * a_hi + ps_hi;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      o[n][0] *= a_lo;
+      o[n][1] *= a_lo;
+      o[n][2] *= a_hi;
+      o[n][3] *= a_hi;
+    }
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[0][0], s[0][1]);
+    pa[1] = pack_bf16(s[0][2], s[0][3]);
+    pa[2] = pack_bf16(s[1][0], s[1][1]);
+    pa[3] = pack_bf16(s[1][2], s[1][3]);
+    // O += P V
+    {
+      const int key = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int csub = (lane >> 4) * 8;
+#pragma unroll
+      for (int c16 = 0; c16 < D / 16; ++c16) {
+        const int col = c16 * 16 + csub;
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4_t(vb + (col >> 6) * 2048 + sw128(key, col & 63), r0, r1, r2, r3);
+        mma_bf16(o[2 * c16], pa, r0, r1);
+        mma_bf16(o[2 * c16 + 1], pa, r2, r3);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && j + NST < nblk) {
+      fence_proxy_async();
+      issue(st, next_id);
+    }
+  }
+  // row sums across the quad
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+
+  constexpr float kLn2 = 0.6931471805599453f;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int r = half ? r_hi : r_lo;
+    if (r >= n_rows) continue;
+    const float l = half ? l_hi : l_lo, m = half ? m_hi : m_lo;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const float lse = l > 0.f ? (m + __log2f(l)) * kLn2 : -CUDART_INF_F;
+    const int tok = r / g, hq = it.kv_head * g + r % g;
+    if (it.slot < 0) {
+      const int64_t qrow = it.q_row0 + tok;
+      if (p.out_f32) {
+        float *dst = reinterpret_cast<float *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<float2 *>(dst + n * 8 + cq) =
+              make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+      } else {
+        uint16_t *dst =
+            reinterpret_cast<uint16_t *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<uint32_t *>(dst + n * 8 + cq) =
+              pack_bf16(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+      }
+      if (p.lse && (lane & 3) == 0) p.lse[qrow * p.Hq + hq] = lse;
+    } else {
+      float *dst = p.part_o + (int64_t)(it.slot + r) * D;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<float2 *>(dst + n * 8 + cq) =
+            make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+      if ((lane & 3) == 0) p.part_lse[it.slot + r] = lse;
+    }
+  }
+}
+
+template <int D, int NST>
+static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const void *tmv,
+                                   const DecodeItem *items, int n, cudaStream_t s) {
+  const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;  // + alignment slack
+  auto kern = decode_kernel<D, NST>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
+  const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
+  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, items, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
+                          const DecodeItem *items, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (p.d == 128) return launch_decode_t<128, 3>(p, tmk, tmv, items, n, s);
+  return launch_decode_t<64, 4>(p, tmk, tmv, items, n, s);
+}
+
+}  // namespace kva

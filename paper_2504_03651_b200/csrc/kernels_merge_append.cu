@@ -1,0 +1,137 @@
+// kernels_merge_append.cu — LSE merge of partial softmax states and the
+// coalesced KV-append block scatter (a2).
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace kva {
+using namespace dev;
+
+// ---------------------------------------------------------------------------------------
+// a6: for each output (row, q-head) with partials {(O_j, lse_j)}:
+//   lse = ln sum_j e^{lse_j},  O = sum_j e^{lse_j - lse} O_j.
+// One warp per output row; each lane owns D/32 contiguous channels (16-B / 8-B vectors).
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
+                                                    const MergeRow *__restrict__ rows,
+                                                    const int32_t *__restrict__ slots, int n_rows) {
+  constexpr int V = D / 32;  // 4 (d=128) or 2 (d=64)
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= n_rows) return;
+  const MergeRow mr = rows[w];
+  float L = -CUDART_INF_F;
+  for (int i = lane; i < mr.s_count; i += 32) L = fmaxf(L, p.part_lse[slots[mr.s_begin + i]]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xffffffffu, L, o));
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  float sum = 0.f;
+  for (int i = 0; i < mr.s_count; ++i) {
+    const int sl = __ldg(slots + mr.s_begin + i);
+    const float lj = __ldg(p.part_lse + sl);
+    const float wgt = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
+    sum += wgt;
+    const float *src = p.part_o + (int64_t)sl * D + lane * V;
+    if constexpr (V == 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4 *>(src));
+      acc[0] += wgt * x.x; acc[1] += wgt * x.y; acc[2] += wgt * x.z; acc[3] += wgt * x.w;
+    } else {
+      const float2 x = __ldg(reinterpret_cast<const float2 *>(src));
+      acc[0] += wgt * x.x; acc[1] += wgt * x.y;
+    }
+  }
+  const float inv = 1.f / sum;
+  const int64_t off = (int64_t)mr.q_row * p.o_stride_tok + (int64_t)mr.q_head * p.o_stride_head + lane * V;
+  if (p.out_f32) {
+    float *dst = reinterpret_cast<float *>(p.out) + off;
+    if constexpr (V == 4)
+      *reinterpret_cast<float4 *>(dst) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    else
+      *reinterpret_cast<float2 *>(dst) = make_float2(acc[0] * inv, acc[1] * inv);
+  } else {
+    uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + off;
+    if constexpr (V == 4)
+      *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
+                                                   pack_bf16(acc[2] * inv, acc[3] * inv));
+    else
+      *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
+  }
+  if (p.lse && lane == 0) p.lse[(int64_t)mr.q_row * p.Hq + mr.q_head] = L + __logf(sum);
+}
+
+cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
+                         int n_rows, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int grid = (n_rows + 7) / 8;
+  if (p.d == 128)
+    merge_kernel<128><<<grid, 256, 0, s>>>(p, rows, slots, n_rows);
+  else
+    merge_kernel<64><<<grid, 256, 0, s>>>(p, rows, slots, n_rows);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// a2: KV append.  (1) alloc_write publishes the ids the host allocator chose (smallest free
+// first, reading #13) in the device block table and clears their free bits; (2) the scatter
+// copies every (new token, local kv-head) row to slot (table[i][t/16], t % 16): one warp per
+// unit, lanes 0-15 move K and 16-31 move V in 16-byte vectors (one d=128 bf16 row each).
+// ---------------------------------------------------------------------------------------
+__global__ void alloc_write_kernel(int32_t *__restrict__ block_table, uint32_t *__restrict__ free_bits,
+                                   const int32_t *__restrict__ tbl_idx, const int32_t *__restrict__ ids,
+                                   int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t id = ids[i];
+  block_table[tbl_idx[i]] = id;
+  atomicAnd(free_bits + (id >> 5), ~(1u << (id & 31)));
+}
+
+cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,
+                               const int32_t *ids, int32_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  alloc_write_kernel<<<(n + 255) / 256, 256, 0, s>>>(block_table, free_bits, tbl_idx, ids, n);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) append_kernel(
+    const uint16_t *__restrict__ k_new, const uint16_t *__restrict__ v_new, int64_t stride_tok,
+    uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
+    const int32_t *__restrict__ block_table, int32_t max_blocks, const AppendReq *__restrict__ reqs,
+    const int32_t *__restrict__ q_indptr, int32_t num_reqs, int32_t total_new_tok) {
+  const int64_t unit = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // (token, head)
+  const int lane = threadIdx.x & 31;
+  if (unit >= (int64_t)total_new_tok * Hkv) return;
+  const int row = (int)(unit / Hkv), h = (int)(unit % Hkv);
+  int lo = 0, hi = num_reqs - 1;  // request of this token: last i with q_indptr[i] <= row
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(q_indptr + mid) <= row) lo = mid; else hi = mid - 1;
+  }
+  const AppendReq rq = reqs[lo];
+  const int t = rq.pos0 + (row - rq.q_row0);
+  const int32_t id = block_table[(int64_t)rq.table_row * max_blocks + t / kBlock];
+  const int chunks = d / 8;  // 16-B chunks per row
+  const int tensor = lane >> 4, c = lane & 15;
+  if (c >= chunks) return;
+  const uint16_t *src = (tensor ? v_new : k_new) + (int64_t)row * stride_tok + (int64_t)h * d + c * 8;
+  uint16_t *dst = (tensor ? v_pool : k_pool) + (((int64_t)id * Hkv + h) * kBlock + t % kBlock) * d + c * 8;
+  *reinterpret_cast<uint4 *>(dst) = __ldg(reinterpret_cast<const uint4 *>(src));
+}
+
+cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
+                          uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
+                          const int32_t *block_table, int32_t max_blocks, const AppendReq *reqs,
+                          const int32_t *q_indptr, int32_t num_reqs, int32_t total_new_tok,
+                          cudaStream_t s) {
+  const int64_t units = (int64_t)total_new_tok * Hkv;
+  if (units <= 0) return cudaSuccess;
+  append_kernel<<<(unsigned)((units + 7) / 8), 256, 0, s>>>(k_new, v_new, stride_tok, k_pool, v_pool,
+                                                             Hkv, d, block_table, max_blocks, reqs,
+                                                             q_indptr, num_reqs, total_new_tok);
+  return cudaGetLastError();
+}
+
+}  // namespace kva

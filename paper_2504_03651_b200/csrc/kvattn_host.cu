@@ -1,0 +1,802 @@
+// kvattn_host.cu — the C ABI of include/kvattn.h: pool handle, host validation, the block
+// allocator, the hybrid-attention planner, plan upload and launches.
+// Product code; shares nothing with oracle/.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/kvattn.h"
+#include "internal.h"
+
+using namespace kva;
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err = "";
+
+static kva_status fail(kva_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(KVA_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                             \
+  } while (0)
+
+extern "C" const char *kva_last_error(void) { return g_err.c_str(); }
+extern "C" const char *kva_version(void) {
+  return "kvattn 0.1 (sm_100a; decode split-KV TMA+mma.sync, tile attention, radix top-k)";
+}
+
+namespace {
+
+struct DeviceGuard {  // switch to the pool's device for the call, restore afterwards
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Pinned host staging ring for plan uploads (host -> workspace copies on the stream).
+struct Staging {
+  struct Slot {
+    void *host = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  };
+  Slot slot[4];
+  int next = 0;
+  cudaError_t get(size_t bytes, Slot **out) {
+    Slot &s = slot[next];
+    next = (next + 1) % 4;
+    if (s.pending) {
+      cudaError_t e = cudaEventSynchronize(s.ev);
+      if (e != cudaSuccess) return e;
+      s.pending = false;
+    }
+    if (!s.ev) {
+      cudaError_t e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    if (s.cap < bytes) {
+      if (s.host) cudaFreeHost(s.host);
+      s.cap = std::max<size_t>(bytes, 1 << 16);
+      cudaError_t e = cudaMallocHost(&s.host, s.cap);
+      if (e != cudaSuccess) {
+        s.host = nullptr;
+        s.cap = 0;
+        return e;
+      }
+    }
+    *out = &s;
+    return cudaSuccess;
+  }
+  cudaError_t upload(Slot *s, void *dev_dst, size_t bytes, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyAsync(dev_dst, s->host, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(s->ev, st);
+    s->pending = (e == cudaSuccess);
+    return e;
+  }
+  void release() {
+    for (auto &s : slot) {
+      if (s.pending) cudaEventSynchronize(s.ev);
+      if (s.host) cudaFreeHost(s.host);
+      if (s.ev) cudaEventDestroy(s.ev);
+      s = Slot{};
+    }
+  }
+};
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D view of a pool tensor: dim0 = head_dim (contiguous), dim1 = num_blocks*Hkv*16 rows;
+// box = 64 channels x 16 rows (one block-head half), 128-byte swizzle.
+kva_status make_pool_map(CUtensorMap *m, void *base, int64_t rows, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (rows >= (1ll << 32)) return fail(KVA_ERR_UNSUPPORTED, "pool has >= 2^32 rows");
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return KVA_OK;
+}
+
+}  // namespace
+
+struct kva_pool {
+  kva_pool_desc desc;
+  std::vector<uint32_t> free_host;  // mirror of free_bits (library is the single writer)
+  int64_t n_free = 0;
+  CUtensorMap tmk, tmv;
+  Staging staging;
+};
+
+static int64_t count_free(const std::vector<uint32_t> &w, int nb) {
+  int64_t n = 0;
+  for (int b = 0; b < nb; ++b) n += (w[b >> 5] >> (b & 31)) & 1u;
+  return n;
+}
+
+extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
+  if (!d || !out) return fail(KVA_ERR_INVALID, "kv_pool_create: null argument");
+  *out = nullptr;
+  if (d->block_size != kBlock) return fail(KVA_ERR_UNSUPPORTED, "block_size must be 16");
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return fail(KVA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", d->head_dim);
+  if (d->num_blocks <= 0 || d->num_kv_heads <= 0)
+    return fail(KVA_ERR_INVALID, "num_blocks and num_kv_heads must be positive");
+  if (!d->k_pool || !d->v_pool || !d->free_bits)
+    return fail(KVA_ERR_INVALID, "k_pool, v_pool and free_bits are required");
+  if ((reinterpret_cast<uintptr_t>(d->k_pool) | reinterpret_cast<uintptr_t>(d->v_pool)) & 127)
+    return fail(KVA_ERR_INVALID, "pool tensors must be 128-byte aligned");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) return fail(KVA_ERR_INVALID, "bad device %d", d->device);
+  DeviceGuard dg(d->device);
+  kva_pool *p = new kva_pool();
+  p->desc = *d;
+  const int words = (d->num_blocks + 31) / 32;
+  p->free_host.assign(words, 0);
+  cudaError_t e = cudaMemcpy(p->free_host.data(), d->free_bits, words * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(KVA_ERR_CUDA, "reading free_bits: %s", cudaGetErrorString(e));
+  }
+  p->n_free = count_free(p->free_host, d->num_blocks);
+  const int64_t rows = (int64_t)d->num_blocks * d->num_kv_heads * kBlock;
+  kva_status st = make_pool_map(&p->tmk, d->k_pool, rows, d->head_dim);
+  if (st == KVA_OK) st = make_pool_map(&p->tmv, d->v_pool, rows, d->head_dim);
+  if (st != KVA_OK) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_pool_destroy(kva_pool *p) {
+  if (!p) return KVA_OK;
+  {
+    DeviceGuard dg(p->desc.device);
+    p->staging.release();
+  }
+  delete p;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_pool_free_count(const kva_pool *p, int64_t *n) {
+  if (!p || !n) return fail(KVA_ERR_INVALID, "null argument");
+  *n = p->n_free;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_pool_resync(kva_pool *p) {
+  if (!p) return fail(KVA_ERR_INVALID, "null pool");
+  DeviceGuard dg(p->desc.device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(p->free_host.data(), p->desc.free_bits, p->free_host.size() * 4,
+                      cudaMemcpyDeviceToHost));
+  p->n_free = count_free(p->free_host, p->desc.num_blocks);
+  return KVA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// descriptor validation (host, synchronous, before anything is enqueued)
+// ------------------------------------------------------------------------------------------
+static inline int qlen(const kva_batch_desc *b, int i) { return b->q_indptr[i + 1] - b->q_indptr[i]; }
+static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// mode 0: attention (every block of [0, ctx) allocated); mode 1: append (resident part only)
+static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
+  if (!b) return fail(KVA_ERR_INVALID, "null descriptor");
+  if (b->num_reqs < 0) return fail(KVA_ERR_INVALID, "num_reqs < 0");
+  if (b->head_dim != 64 && b->head_dim != 128)
+    return fail(KVA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", b->head_dim);
+  if (b->num_kv_heads <= 0) return fail(KVA_ERR_INVALID, "num_kv_heads <= 0");
+  if (b->num_q_heads <= 0 || b->num_q_heads % b->num_kv_heads)
+    return fail(KVA_ERR_INVALID, "num_q_heads %d not a positive multiple of num_kv_heads %d",
+                b->num_q_heads, b->num_kv_heads);
+  if (b->num_reqs == 0) return KVA_OK;
+  if (!b->q_indptr || !b->ctx_len || !b->block_table || !b->block_table_host)
+    return fail(KVA_ERR_INVALID, "q_indptr, ctx_len, block_table and block_table_host are required");
+  if (b->max_blocks <= 0) return fail(KVA_ERR_INVALID, "max_blocks <= 0");
+  if (b->q_indptr[0] != 0) return fail(KVA_ERR_INVALID, "q_indptr[0] != 0");
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int ql = qlen(b, i), ctx = b->ctx_len[i];
+    if (ql < 1 || ql > ctx) return fail(KVA_ERR_INVALID, "request %d: q_len %d not in [1, ctx=%d]", i, ql, ctx);
+    if (ctx > b->max_blocks * kBlock)
+      return fail(KVA_ERR_INVALID, "request %d: ctx %d > max_blocks*16", i, ctx);
+    const int need_blocks = mode == 0 ? cdiv(ctx, kBlock) : cdiv(ctx - ql, kBlock);
+    const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+    for (int k = 0; k < need_blocks; ++k)
+      if (row[k] < 0 || row[k] >= nb)
+        return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid (num_blocks %d)", i, k,
+                    row[k], nb);
+  }
+  if (b->group_of) {
+    if (b->num_groups > 0 && !b->group_prefix_blocks)
+      return fail(KVA_ERR_INVALID, "group_prefix_blocks required");
+    std::vector<int> first(std::max(b->num_groups, 0), -1);
+    for (int i = 0; i < b->num_reqs; ++i) {
+      const int gi = b->group_of[i];
+      if (gi < 0) continue;
+      if (gi >= b->num_groups) return fail(KVA_ERR_GROUP, "request %d: group %d out of range", i, gi);
+      const int np = b->group_prefix_blocks[gi];
+      if (np < 0) return fail(KVA_ERR_GROUP, "group %d: negative prefix", gi);
+      if (b->ctx_len[i] - qlen(b, i) < np * kBlock)
+        return fail(KVA_ERR_GROUP, "request %d: queries/appends inside group %d's prefix", i, gi);
+      if (first[gi] < 0) first[gi] = i;
+      const int32_t *a = b->block_table_host + (int64_t)i * b->max_blocks;
+      const int32_t *c = b->block_table_host + (int64_t)first[gi] * b->max_blocks;
+      for (int k = 0; k < np; ++k)
+        if (a[k] != c[k] || a[k] < 0 || a[k] >= nb)
+          return fail(KVA_ERR_GROUP, "request %d: prefix block %d differs from group %d's", i, k, gi);
+    }
+  }
+  return KVA_OK;
+}
+
+static kva_status validate_desc(const kva_pool *p, const kva_batch_desc *b, int mode) {
+  if (!p || !b) return fail(KVA_ERR_INVALID, "null pool or descriptor");
+  if (b->num_kv_heads != p->desc.num_kv_heads)
+    return fail(KVA_ERR_INVALID, "num_kv_heads %d != pool's %d", b->num_kv_heads, p->desc.num_kv_heads);
+  if (b->head_dim != p->desc.head_dim)
+    return fail(KVA_ERR_INVALID, "head_dim %d != pool's %d", b->head_dim, p->desc.head_dim);
+  return validate_batch(b, p->desc.num_blocks, mode);
+}
+
+extern "C" kva_status kva_validate_batch(const kva_batch_desc *b, int32_t num_blocks, int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(KVA_ERR_INVALID, "mode must be 0 or 1");
+  return validate_batch(b, num_blocks, mode);
+}
+
+// ------------------------------------------------------------------------------------------
+// kv_append (a2)
+// ------------------------------------------------------------------------------------------
+struct AppendPlan {
+  std::vector<AppendReq> reqs;
+  std::vector<int32_t> tbl_idx, ids;
+  int64_t need = 0;
+  int total_q = 0;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t append_upload_bytes(int R, int64_t nalloc) {
+  return align256(sizeof(AppendReq) * std::max(R, 1)) + align256(4 * (R + 1)) +
+         2 * align256(4 * std::max<int64_t>(nalloc, 1));
+}
+
+extern "C" kva_status kv_append_workspace_size(const kva_batch_desc *b, size_t *bytes) {
+  if (!b || !bytes) return fail(KVA_ERR_INVALID, "null argument");
+  // upper bound on allocations: every new position's block
+  int64_t nalloc = 0;
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int ql = qlen(b, i), ctx = b->ctx_len[i];
+    nalloc += cdiv(ctx, kBlock) - (ctx - ql) / kBlock;
+  }
+  *bytes = append_upload_bytes(b->num_reqs, nalloc);
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_new,
+                                const void *v_new, int64_t stride_tok, int32_t *deficit,
+                                void *workspace, size_t ws_bytes, kva_stream_t stream) {
+  if (deficit) *deficit = 0;
+  kva_status st = validate_desc(p, b, 1);
+  if (st != KVA_OK) return st;
+  if (b->num_reqs == 0) return KVA_OK;
+  const int Hkv = b->num_kv_heads, d = b->head_dim, nb = p->desc.num_blocks;
+  if (!k_new || !v_new) return fail(KVA_ERR_INVALID, "k_new/v_new required");
+  if (stride_tok < (int64_t)Hkv * d) return fail(KVA_ERR_INVALID, "new_stride_tok too small");
+  if (((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15) ||
+      (stride_tok % 8))
+    return fail(KVA_ERR_INVALID, "k_new/v_new must be 16-byte aligned with stride %% 8 == 0");
+  AppendPlan ap;
+  ap.reqs.resize(b->num_reqs);
+  // count needed blocks (entries == -1 among new positions' blocks), validate the rest
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int ql = qlen(b, i), ctx = b->ctx_len[i], start = ctx - ql;
+    if (cdiv(ctx, kBlock) > nb)
+      return fail(KVA_ERR_CAPACITY, "request %d needs %d blocks > pool's %d", i, cdiv(ctx, kBlock), nb);
+    const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+    for (int k = start / kBlock; k < cdiv(ctx, kBlock); ++k) {
+      if (row[k] == -1) ++ap.need;
+      else if (row[k] < 0 || row[k] >= nb)
+        return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid", i, k, row[k]);
+    }
+    ap.reqs[i] = AppendReq{b->q_indptr[i], ql, start, i};
+  }
+  if (ap.need > p->n_free) {
+    if (deficit) *deficit = (int32_t)(ap.need - p->n_free);
+    return fail(KVA_NEEDS_EVICTION, "kv_append needs %lld blocks, %lld free", (long long)ap.need,
+                (long long)p->n_free);
+  }
+  const size_t up = append_upload_bytes(b->num_reqs, ap.need);
+  if (!workspace || ws_bytes < up)
+    return fail(KVA_ERR_INVALID, "kv_append workspace too small (%zu < %zu)", ws_bytes, up);
+  // allocate: descriptor order, positions ascending, smallest free id first (reading #13)
+  std::vector<uint32_t> fh = p->free_host;  // commit only after everything is enqueued
+  int scan = 0;
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int ql = qlen(b, i), ctx = b->ctx_len[i], start = ctx - ql;
+    const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+    for (int k = start / kBlock; k < cdiv(ctx, kBlock); ++k) {
+      if (row[k] != -1) continue;
+      while (!((fh[scan >> 5] >> (scan & 31)) & 1u)) ++scan;
+      fh[scan >> 5] &= ~(1u << (scan & 31));
+      ap.tbl_idx.push_back(i * b->max_blocks + k);
+      ap.ids.push_back(scan);
+    }
+  }
+  ap.total_q = b->q_indptr[b->num_reqs];
+  DeviceGuard dg(p->desc.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Staging::Slot *slot = nullptr;
+  CUDA_TRY(p->staging.get(up, &slot));
+  uint8_t *h = static_cast<uint8_t *>(slot->host);
+  uint8_t *dws = static_cast<uint8_t *>(workspace);
+  size_t off = 0;
+  auto put = [&](const void *src, size_t n) {
+    std::memcpy(h + off, src, n);
+    const size_t o = off;
+    off += align256(std::max<size_t>(n, 4));
+    return dws + o;
+  };
+  auto *d_reqs = reinterpret_cast<AppendReq *>(put(ap.reqs.data(), sizeof(AppendReq) * ap.reqs.size()));
+  auto *d_qi = reinterpret_cast<int32_t *>(put(b->q_indptr, 4 * (b->num_reqs + 1)));
+  auto *d_tbl = reinterpret_cast<int32_t *>(put(ap.tbl_idx.data(), 4 * ap.tbl_idx.size()));
+  auto *d_ids = reinterpret_cast<int32_t *>(put(ap.ids.data(), 4 * ap.ids.size()));
+  CUDA_TRY(p->staging.upload(slot, workspace, off, s));
+  CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, d_tbl, d_ids, (int)ap.ids.size(), s));
+  CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
+                         stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
+                         static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
+                         b->max_blocks, d_reqs, d_qi, b->num_reqs, ap.total_q, s));
+  // commit host state: free mirror + caller's host table mirror
+  p->free_host.swap(fh);
+  p->n_free -= ap.need;
+  for (size_t j = 0; j < ap.ids.size(); ++j) b->block_table_host[ap.tbl_idx[j]] = ap.ids[j];
+  return KVA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// hybrid attention planner (a1)
+// ------------------------------------------------------------------------------------------
+struct kva_plan {
+  AttnParams p;
+  CUtensorMap tmk, tmv;
+  const DecodeItem *d_dec = nullptr;
+  const TileItem *d_tile = nullptr;
+  const MergeRow *d_mrows = nullptr;
+  const int32_t *d_mslots = nullptr;
+  int n_dec = 0, n_tile = 0, n_mrows = 0;
+  int device = 0;
+  kva_plan_stats stats{};
+};
+
+struct PlanBuild {
+  std::vector<DecodeItem> dec;
+  std::vector<TileItem> tile;
+  std::vector<MergeRow> mrows;
+  std::vector<int32_t> mslots, row_list;
+  int64_t n_slots = 0;
+  kva_plan_stats stats{};
+};
+
+static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
+  const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
+  const int d = b->head_dim;
+  const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
+  auto grp = [&](int i) { return b->group_of ? b->group_of[i] : -1; };
+  auto dec_class = [&](int i) { return qlen(b, i) * g <= kDecodeRows; };
+  // --- cascade tiles: decode-class members of each group, stacked along M ---
+  std::vector<int> member_idx(R, -1), first_member(G, -1);
+  std::vector<std::vector<int64_t>> casc_base(G);
+  std::vector<int> group_rows(G, 0), list_off(G, 0);
+  for (int i = 0; i < R; ++i) {
+    const int gi = grp(i);
+    if (gi < 0) continue;
+    if (first_member[gi] < 0) first_member[gi] = i;
+  }
+  for (int gi = 0; gi < G; ++gi) {
+    list_off[gi] = (int)pb.row_list.size();
+    for (int i = 0; i < R; ++i) {
+      if (grp(i) != gi || !dec_class(i)) continue;
+      member_idx[i] = (int)pb.row_list.size() - list_off[gi];
+      for (int j = 0; j < qlen(b, i); ++j) pb.row_list.push_back(b->q_indptr[i] + j);
+    }
+    const int ntok = (int)pb.row_list.size() - list_off[gi];
+    group_rows[gi] = ntok * g;
+    if (ntok == 0) continue;
+    const int np = b->group_prefix_blocks[gi];
+    casc_base[gi].resize(Hkv);
+    for (int h = 0; h < Hkv; ++h) {
+      casc_base[gi][h] = pb.n_slots;
+      for (int m0 = 0; m0 < group_rows[gi]; m0 += kTileM) {
+        TileItem t{};
+        t.row_src = list_off[gi];
+        t.r0 = m0;
+        t.n_rows = std::min(kTileM, group_rows[gi] - m0);
+        t.kv_head = h;
+        t.table_row = first_member[gi];
+        t.k0 = 0;
+        t.k1 = np * kBlock;
+        t.pos0 = 0;
+        t.slot = (int32_t)(pb.n_slots + m0);
+        t.flags = kTileList;
+        pb.tile.push_back(t);
+        pb.stats.n_cascade_items++;
+      }
+      pb.n_slots += group_rows[gi];
+    }
+  }
+  // --- per request ---
+  int64_t kv_tokens = 0, dec_keys = 0, dec_rows = 0;
+  for (int gi = 0; gi < G; ++gi) kv_tokens += (int64_t)b->group_prefix_blocks[gi] * kBlock;
+  for (int i = 0; i < R; ++i) {
+    const int ql = qlen(b, i), ctx = b->ctx_len[i], gi = grp(i), q0 = b->q_indptr[i];
+    const int np = gi >= 0 ? b->group_prefix_blocks[gi] : 0;
+    kv_tokens += ctx - np * kBlock;
+    for (int j = 0; j < ql; ++j) pb.stats.flops += (int64_t)(ctx - ql + j + 1) * Hq * 4 * d;
+    if (dec_class(i)) {
+      const bool cascaded = gi >= 0 && member_idx[i] >= 0;
+      const int kb = cascaded ? np * kBlock : 0;
+      const int nsplit = cdiv(ctx - kb, kSplitKeys);
+      const bool direct = !cascaded && nsplit == 1;
+      const int rows = ql * g;
+      dec_rows += rows * Hkv;
+      for (int h = 0; h < Hkv; ++h) {
+        const int64_t base = direct ? -1 : pb.n_slots;
+        if (!direct) pb.n_slots += (int64_t)nsplit * rows;
+        for (int s = 0; s < nsplit; ++s) {
+          DecodeItem it{};
+          it.q_row0 = q0;
+          it.n_tok = ql;
+          it.kv_head = h;
+          it.table_row = i;
+          it.k0 = kb + s * kSplitKeys;
+          it.k1 = std::min(ctx, kb + (s + 1) * kSplitKeys);
+          it.pos0 = ctx - ql;
+          it.slot = direct ? -1 : (int32_t)(base + (int64_t)s * rows);
+          pb.dec.push_back(it);
+          dec_keys += it.k1 - it.k0;
+        }
+        if (!direct) {
+          for (int r = 0; r < rows; ++r) {
+            MergeRow mr{q0 + r / g, h * g + r % g, (int32_t)pb.mslots.size(), 0};
+            if (cascaded) {
+              pb.mslots.push_back((int32_t)(casc_base[gi][h] + (int64_t)member_idx[i] * g + r));
+              mr.s_count++;
+            }
+            for (int s = 0; s < nsplit; ++s) {
+              pb.mslots.push_back((int32_t)(base + (int64_t)s * rows + r));
+              mr.s_count++;
+            }
+            pb.mrows.push_back(mr);
+          }
+        }
+      }
+    } else {
+      const int rows = ql * g;
+      for (int h = 0; h < Hkv; ++h) {
+        for (int m0 = 0; m0 < rows; m0 += kTileM) {
+          TileItem t{};
+          t.row_src = q0;
+          t.r0 = m0;
+          t.n_rows = std::min(kTileM, rows - m0);
+          t.kv_head = h;
+          t.table_row = i;
+          t.k0 = 0;
+          t.k1 = ctx - ql + (m0 + t.n_rows - 1) / g + 1;
+          t.pos0 = ctx - ql;
+          t.slot = -1;
+          t.flags = kTileCausal;
+          pb.tile.push_back(t);
+        }
+      }
+    }
+  }
+  // longest tiles first (LPT); ties keep (kv_head, m-tile, member) order so concurrently
+  // running CTAs of a group share its prefix blocks in L2
+  std::stable_sort(pb.tile.begin(), pb.tile.end(),
+                   [](const TileItem &a, const TileItem &c) { return a.k1 - a.k0 > c.k1 - c.k0; });
+  pb.stats.n_decode_items = (int64_t)pb.dec.size();
+  pb.stats.n_tile_items = (int64_t)pb.tile.size();
+  pb.stats.n_merge_rows = (int64_t)pb.mrows.size();
+  pb.stats.kv_bytes_algorithmic = kv_tokens * Hkv * d * 2 * 2;
+  const int64_t total_q = b->q_indptr[R];
+  pb.stats.q_bytes = total_q * Hq * d * 2;
+  pb.stats.o_bytes = total_q * Hq * d * 2;
+  pb.stats.decode_kv_bytes = dec_keys * d * 2 * 2;
+  (void)dec_rows;
+}
+
+static size_t plan_bytes(const PlanBuild &pb, int d, size_t *arrays_bytes) {
+  size_t a = align256(sizeof(DecodeItem) * pb.dec.size()) + align256(sizeof(TileItem) * pb.tile.size()) +
+             align256(sizeof(MergeRow) * pb.mrows.size()) + align256(4 * pb.mslots.size()) +
+             align256(4 * pb.row_list.size()) + 5 * 256;
+  if (arrays_bytes) *arrays_bytes = a;
+  return a + align256((size_t)pb.n_slots * d * 4) + align256((size_t)pb.n_slots * 4);
+}
+
+extern "C" kva_status hybrid_attention_workspace_size(const kva_batch_desc *b, size_t *bytes) {
+  if (!b || !bytes) return fail(KVA_ERR_INVALID, "null argument");
+  if (b->num_kv_heads <= 0 || b->num_q_heads % b->num_kv_heads)
+    return fail(KVA_ERR_INVALID, "bad head counts");
+  PlanBuild pb;
+  build_plan(b, pb);
+  *bytes = plan_bytes(pb, b->head_dim, nullptr);
+  return KVA_OK;
+}
+
+extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b, void *ws,
+                                            size_t ws_bytes, kva_stream_t stream, kva_plan **out) {
+  if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
+  *out = nullptr;
+  kva_status st = validate_desc(p, b, 0);
+  if (st != KVA_OK) return st;
+  PlanBuild pb;
+  build_plan(b, pb);
+  size_t arrays = 0;
+  const size_t need = plan_bytes(pb, b->head_dim, &arrays);
+  if (!ws || ws_bytes < need)
+    return fail(KVA_ERR_INVALID, "hybrid_attention workspace too small (%zu < %zu)", ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(KVA_ERR_INVALID, "workspace must be 256-B aligned");
+  DeviceGuard dg(p->desc.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  kva_plan *pl = new kva_plan();
+  pl->device = p->desc.device;
+  pl->tmk = p->tmk;
+  pl->tmv = p->tmv;
+  pl->stats = pb.stats;
+  uint8_t *dws = static_cast<uint8_t *>(ws);
+  if (arrays > 5 * 256) {
+    Staging::Slot *slot = nullptr;
+    cudaError_t e = p->staging.get(arrays, &slot);
+    if (e != cudaSuccess) {
+      delete pl;
+      return fail(KVA_ERR_CUDA, "staging: %s", cudaGetErrorString(e));
+    }
+    uint8_t *h = static_cast<uint8_t *>(slot->host);
+    size_t off = 0;
+    auto put = [&](const void *src, size_t n) {
+      if (n) std::memcpy(h + off, src, n);
+      const size_t o = off;
+      off += align256(std::max<size_t>(n, 4));
+      return dws + o;
+    };
+    pl->d_dec = reinterpret_cast<const DecodeItem *>(put(pb.dec.data(), sizeof(DecodeItem) * pb.dec.size()));
+    pl->d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), sizeof(TileItem) * pb.tile.size()));
+    pl->d_mrows = reinterpret_cast<const MergeRow *>(put(pb.mrows.data(), sizeof(MergeRow) * pb.mrows.size()));
+    pl->d_mslots = reinterpret_cast<const int32_t *>(put(pb.mslots.data(), 4 * pb.mslots.size()));
+    pl->p.row_list = reinterpret_cast<const int32_t *>(put(pb.row_list.data(), 4 * pb.row_list.size()));
+    e = p->staging.upload(slot, ws, off, s);
+    if (e != cudaSuccess) {
+      delete pl;
+      return fail(KVA_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
+    }
+  }
+  pl->n_dec = (int)pb.dec.size();
+  pl->n_tile = (int)pb.tile.size();
+  pl->n_mrows = (int)pb.mrows.size();
+  AttnParams &ap = pl->p;
+  ap.k_pool = static_cast<const uint16_t *>(p->desc.k_pool);
+  ap.v_pool = static_cast<const uint16_t *>(p->desc.v_pool);
+  ap.num_blocks = p->desc.num_blocks;
+  ap.Hkv = b->num_kv_heads;
+  ap.Hq = b->num_q_heads;
+  ap.g = b->num_q_heads / b->num_kv_heads;
+  ap.d = b->head_dim;
+  ap.block_table = b->block_table;
+  ap.max_blocks = b->max_blocks;
+  const double scale = b->sm_scale > 0 ? (double)b->sm_scale : 1.0 / std::sqrt((double)b->head_dim);
+  ap.scale_log2 = (float)(scale * 1.4426950408889634);
+  ap.part_o = reinterpret_cast<float *>(dws + arrays);
+  ap.part_lse = reinterpret_cast<float *>(dws + arrays + align256((size_t)pb.n_slots * b->head_dim * 4));
+  *out = pl;
+  return KVA_OK;
+}
+
+extern "C" kva_status kva_plan_destroy(kva_plan *pl) {
+  delete pl;
+  return KVA_OK;
+}
+
+extern "C" kva_status kva_plan_get_stats(const kva_plan *pl, kva_plan_stats *st) {
+  if (!pl || !st) return fail(KVA_ERR_INVALID, "null argument");
+  *st = pl->stats;
+  return KVA_OK;
+}
+
+extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void *q, int64_t q_st,
+                                                  int64_t q_sh, void *out, int64_t o_st,
+                                                  int64_t o_sh, int32_t out_dtype, float *lse,
+                                                  int32_t phases, kva_stream_t stream) {
+  if (!pl) return fail(KVA_ERR_INVALID, "null plan");
+  if (pl->n_dec + pl->n_tile == 0) return KVA_OK;
+  if (!q || !out) return fail(KVA_ERR_INVALID, "q and out are required");
+  if (out_dtype != KVA_OUT_BF16 && out_dtype != KVA_OUT_F32)
+    return fail(KVA_ERR_INVALID, "out_dtype must be KVA_OUT_BF16 or KVA_OUT_F32");
+  if ((reinterpret_cast<uintptr_t>(q) & 3) || (q_st & 1) || (q_sh & 1))
+    return fail(KVA_ERR_INVALID, "q must be 4-byte aligned with even strides");
+  const int vec = out_dtype == KVA_OUT_F32 ? 16 : 8;
+  if ((reinterpret_cast<uintptr_t>(out) & (vec - 1)) || (o_st % 4) || (o_sh % 4))
+    return fail(KVA_ERR_INVALID, "out must be %d-byte aligned with strides %% 4 == 0", vec);
+  DeviceGuard dg(pl->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AttnParams p = pl->p;
+  p.q = static_cast<const uint16_t *>(q);
+  p.q_stride_tok = q_st;
+  p.q_stride_head = q_sh;
+  p.out = out;
+  p.o_stride_tok = o_st;
+  p.o_stride_head = o_sh;
+  p.out_f32 = out_dtype == KVA_OUT_F32;
+  p.lse = lse;
+  if (phases & KVA_PHASE_TILE) CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, s));
+  if (phases & KVA_PHASE_DECODE) CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
+  if (phases & KVA_PHASE_MERGE) CUDA_TRY(launch_merge(p, pl->d_mrows, pl->d_mslots, pl->n_mrows, s));
+  return KVA_OK;
+}
+
+extern "C" kva_status hybrid_attention_run(const kva_plan *pl, const void *q, int64_t q_st,
+                                           int64_t q_sh, void *out, int64_t o_st, int64_t o_sh,
+                                           int32_t out_dtype, float *lse, kva_stream_t stream) {
+  return hybrid_attention_run_phases(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse,
+                                     KVA_PHASE_ALL, stream);
+}
+
+extern "C" kva_status kva_plan_launch_count(const kva_plan *pl, int32_t phases, int32_t *n) {
+  if (!pl || !n) return fail(KVA_ERR_INVALID, "null argument");
+  *n = ((phases & KVA_PHASE_TILE) && pl->n_tile > 0) + ((phases & KVA_PHASE_DECODE) && pl->n_dec > 0) +
+       ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0);
+  return KVA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// block release (recompute-mode preemption / finished requests)
+// ------------------------------------------------------------------------------------------
+extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t n,
+                                        kva_stream_t stream) {
+  if (!p || n < 0 || (n > 0 && !ids)) return fail(KVA_ERR_INVALID, "bad arguments");
+  if (n == 0) return KVA_OK;
+  const int nb = p->desc.num_blocks;
+  std::vector<uint8_t> seen(nb, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= nb) return fail(KVA_ERR_INVALID, "block id %d out of range", ids[i]);
+    if ((p->free_host[ids[i] >> 5] >> (ids[i] & 31)) & 1u)
+      return fail(KVA_ERR_INVALID, "block %d is already free", ids[i]);
+    if (seen[ids[i]]++) return fail(KVA_ERR_INVALID, "block %d listed twice", ids[i]);
+  }
+  DeviceGuard dg(p->desc.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Staging::Slot *slot = nullptr;
+  const size_t bytes = 16 + n * 4;  // [int64 n][pad][ids]
+  CUDA_TRY(p->staging.get(bytes, &slot));
+  std::memcpy(slot->host, &n, sizeof n);
+  std::memcpy(static_cast<uint8_t *>(slot->host) + 16, ids, n * 4);
+  uint8_t *d_buf = nullptr;
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&d_buf), bytes, s));
+  CUDA_TRY(p->staging.upload(slot, d_buf, bytes, s));
+  CUDA_TRY(launch_free_ids(p->desc.free_bits, reinterpret_cast<const int32_t *>(d_buf + 16),
+                           reinterpret_cast<const int64_t *>(d_buf), n, s));
+  CUDA_TRY(cudaFreeAsync(d_buf, s));
+  for (int64_t i = 0; i < n; ++i) p->free_host[ids[i] >> 5] |= 1u << (ids[i] & 31);
+  p->n_free += n;
+  return KVA_OK;
+}
+
+extern "C" kva_status hybrid_attention(kva_pool *p, const kva_batch_desc *b, const void *q,
+                                       int64_t q_st, int64_t q_sh, void *out, int64_t o_st,
+                                       int64_t o_sh, int32_t out_dtype, float *lse, void *ws,
+                                       size_t ws_bytes, kva_stream_t stream) {
+  kva_plan *pl = nullptr;
+  kva_status st = hybrid_attention_plan(p, b, ws, ws_bytes, stream, &pl);
+  if (st != KVA_OK) return st;
+  st = hybrid_attention_run(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse, stream);
+  kva_plan_destroy(pl);
+  return st;
+}
+
+// ------------------------------------------------------------------------------------------
+// eviction (a8)
+// ------------------------------------------------------------------------------------------
+extern "C" kva_status evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
+                                 const uint16_t *depth, int64_t n, uint64_t *keys,
+                                 kva_stream_t stream) {
+  if (n < 0) return fail(KVA_ERR_INVALID, "n < 0");
+  if (n == 0) return KVA_OK;
+  if (!state || !rc || !lat || !keys) return fail(KVA_ERR_INVALID, "state, rc, lat, keys required");
+  CUDA_TRY(launch_evict_keys(state, rc, lat, depth, n, keys, reinterpret_cast<cudaStream_t>(stream)));
+  return KVA_OK;
+}
+
+extern "C" kva_status evict_select_workspace_size(int64_t n, int64_t k, size_t *bytes) {
+  if (!bytes || n < 0 || k < 0) return fail(KVA_ERR_INVALID, "bad arguments");
+  *bytes = evict_select_ws_bytes(n, k) + 256;
+  return KVA_OK;
+}
+
+extern "C" kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
+                                   int64_t *n_selected, int32_t apply, kva_pool *pool, void *ws,
+                                   size_t ws_bytes, kva_stream_t stream) {
+  if (n < 0 || k < 0) return fail(KVA_ERR_INVALID, "n and k must be >= 0");
+  if (n >= (1ll << 31)) return fail(KVA_ERR_UNSUPPORTED, "n >= 2^31");
+  if (apply && !n_selected) return fail(KVA_ERR_INVALID, "apply requires n_selected");
+  if (n_selected) *n_selected = 0;
+  if (apply && !pool) return fail(KVA_ERR_INVALID, "apply requires the pool");
+  if (apply && pool && n > pool->desc.num_blocks) return fail(KVA_ERR_INVALID, "n > pool blocks");
+  if (k == 0 || n == 0) return k == 0 ? KVA_OK : fail(KVA_EVICTION_SHORT, "no evictable blocks");
+  if (!keys || !out_ids) return fail(KVA_ERR_INVALID, "keys and out_ids required");
+  const size_t need = evict_select_ws_bytes(n, k) + 256;
+  if (!ws || ws_bytes < need) return fail(KVA_ERR_INVALID, "evict_select workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t *w = static_cast<uint8_t *>(ws);
+  int64_t *d_count = reinterpret_cast<int64_t *>(w);
+  CUDA_TRY(launch_evict_select(keys, n, k, out_ids, d_count, w + 256, ws_bytes - 256, s));
+  if (apply) CUDA_TRY(launch_free_ids(pool->desc.free_bits, out_ids, d_count, k, s));
+  if (!n_selected) return KVA_OK;  // asynchronous mode: count stays on the device
+  int64_t cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(&cnt, d_count, sizeof cnt, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *n_selected = cnt;
+  if (apply && cnt > 0) {
+    std::vector<int32_t> ids(cnt);
+    CUDA_TRY(cudaMemcpy(ids.data(), out_ids, cnt * 4, cudaMemcpyDeviceToHost));
+    for (int32_t id : ids) {
+      uint32_t &wd = pool->free_host[id >> 5];
+      if (!((wd >> (id & 31)) & 1u)) {
+        wd |= 1u << (id & 31);
+        pool->n_free++;
+      }
+    }
+  }
+  if (cnt < k) return fail(KVA_EVICTION_SHORT, "only %lld of %lld blocks evictable", (long long)cnt, (long long)k);
+  return KVA_OK;
+}

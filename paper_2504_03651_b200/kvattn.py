@@ -1,0 +1,360 @@
+"""Thin ctypes binding of libkvattn.so (include/kvattn.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; PyTorch only supplies
+device memory, streams and (in bench.py) process groups.  There is no CPU fallback: if the
+library is missing or CUDA is unavailable, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import _build
+
+OK, ERR_INVALID, ERR_UNSUPPORTED, NEEDS_EVICTION, ERR_CAPACITY, EVICTION_SHORT, ERR_GROUP, ERR_CUDA = range(8)
+OUT_BF16, OUT_F32 = 0, 1
+STATUS_NAMES = {0: "OK", 1: "ERR_INVALID", 2: "ERR_UNSUPPORTED", 3: "NEEDS_EVICTION",
+                4: "ERR_CAPACITY", 5: "EVICTION_SHORT", 6: "ERR_GROUP", 7: "ERR_CUDA"}
+
+
+class KvaError(RuntimeError):
+    def __init__(self, status, msg, **extra):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.__dict__.update(extra)
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("num_blocks", ctypes.c_int32), ("block_size", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p),
+                ("free_bits", ctypes.c_void_p), ("device", ctypes.c_int32)]
+
+
+class BatchDesc(ctypes.Structure):
+    _fields_ = [("num_reqs", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("req_type", ctypes.c_void_p), ("q_indptr", ctypes.c_void_p),
+                ("ctx_len", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
+                ("block_table_host", ctypes.c_void_p), ("max_blocks", ctypes.c_int32),
+                ("group_of", ctypes.c_void_p), ("num_groups", ctypes.c_int32),
+                ("group_prefix_blocks", ctypes.c_void_p), ("sm_scale", ctypes.c_float)]
+
+
+class PlanStats(ctypes.Structure):
+    _fields_ = [("n_decode_items", ctypes.c_int64), ("n_tile_items", ctypes.c_int64),
+                ("n_cascade_items", ctypes.c_int64), ("n_merge_rows", ctypes.c_int64),
+                ("kv_bytes_algorithmic", ctypes.c_int64), ("q_bytes", ctypes.c_int64),
+                ("o_bytes", ctypes.c_int64), ("decode_kv_bytes", ctypes.c_int64),
+                ("flops", ctypes.c_int64)]
+
+
+EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_create", "kv_pool_destroy",
+           "kv_pool_free_count", "kv_pool_resync", "kv_append_workspace_size", "kv_append",
+           "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
+           "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_destroy",
+           "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
+           "evict_select_workspace_size", "evict_select"]
+PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
+
+_lib = None
+
+
+def lib_path():
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libkvattn.so (building it with nvcc first if missing/stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and _build.stale():
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"libkvattn.so not built ({_build.LIB}); run __graft_entry__.build()")
+    L = ctypes.CDLL(_build.LIB)
+    P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    sig = {
+        "kva_last_error": ([], ctypes.c_char_p),
+        "kva_version": ([], ctypes.c_char_p),
+        "kva_validate_batch": ([P, i32, i32], ctypes.c_int),
+        "kv_pool_create": ([P, P], ctypes.c_int),
+        "kv_pool_destroy": ([P], ctypes.c_int),
+        "kv_pool_free_count": ([P, P], ctypes.c_int),
+        "kv_pool_resync": ([P], ctypes.c_int),
+        "kv_append_workspace_size": ([P, P], ctypes.c_int),
+        "kv_append": ([P, P, P, P, i64, P, P, sz, P], ctypes.c_int),
+        "hybrid_attention_workspace_size": ([P, P], ctypes.c_int),
+        "hybrid_attention_plan": ([P, P, P, sz, P, P], ctypes.c_int),
+        "hybrid_attention_run": ([P, P, i64, i64, P, i64, i64, i32, P, P], ctypes.c_int),
+        "hybrid_attention_run_phases": ([P, P, i64, i64, P, i64, i64, i32, P, i32, P], ctypes.c_int),
+        "kva_plan_launch_count": ([P, i32, P], ctypes.c_int),
+        "kv_release_blocks": ([P, P, i64, P], ctypes.c_int),
+        "kva_plan_destroy": ([P], ctypes.c_int),
+        "kva_plan_get_stats": ([P, P], ctypes.c_int),
+        "hybrid_attention": ([P, P, P, i64, i64, P, i64, i64, i32, P, P, sz, P], ctypes.c_int),
+        "evict_keys": ([P, P, P, P, i64, P, P], ctypes.c_int),
+        "evict_select_workspace_size": ([i64, i64, P], ctypes.c_int),
+        "evict_select": ([P, i64, i64, P, P, i32, P, P, sz, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(st, **extra):
+    if st != OK:
+        raise KvaError(st, load().kva_last_error().decode(), **extra)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def version() -> str:
+    return load().kva_version().decode()
+
+
+class Pool:
+    """kv_pool_create / kv_pool_destroy around caller-owned torch tensors."""
+
+    def __init__(self, k_pool: torch.Tensor, v_pool: torch.Tensor, free_bits: torch.Tensor):
+        L = load()
+        if not (k_pool.is_cuda and v_pool.is_cuda and free_bits.is_cuda):
+            raise KvaError(ERR_INVALID, "pool tensors must be CUDA tensors (no CPU path)")
+        assert k_pool.dtype == torch.bfloat16 and k_pool.is_contiguous() and v_pool.is_contiguous()
+        nb, hkv, bs, d = k_pool.shape
+        self.k_pool, self.v_pool, self.free_bits = k_pool, v_pool, free_bits
+        self.desc = PoolDesc(nb, bs, hkv, d, k_pool.data_ptr(), v_pool.data_ptr(),
+                             free_bits.data_ptr(), k_pool.device.index or 0)
+        self.handle = ctypes.c_void_p()
+        _check(L.kv_pool_create(ctypes.byref(self.desc), ctypes.byref(self.handle)))
+
+    def free_count(self) -> int:
+        n = ctypes.c_int64()
+        _check(load().kv_pool_free_count(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def resync(self):
+        _check(load().kv_pool_resync(self.handle))
+
+    def close(self):
+        if self.handle:
+            load().kv_pool_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    """The batch descriptor (host numpy arrays + the device block table)."""
+
+    def __init__(self, batch: dict, device):
+        self.q_indptr = np.ascontiguousarray(batch["q_indptr"], np.int32)
+        self.ctx_len = np.ascontiguousarray(batch["ctx_len"], np.int32)
+        self.req_type = np.ascontiguousarray(batch.get("req_type", np.zeros(len(self.ctx_len))), np.int32)
+        self.table_host = np.ascontiguousarray(batch["block_table"], np.int32).copy()
+        self.group_of = (None if batch.get("group_of") is None
+                         else np.ascontiguousarray(batch["group_of"], np.int32))
+        gpb = batch.get("group_prefix_blocks")
+        self.group_prefix_blocks = np.ascontiguousarray(gpb if gpb is not None else [], np.int32)
+        self.table_dev = (torch.from_numpy(self.table_host.copy()).to(device)
+                          if device is not None else torch.from_numpy(self.table_host.copy()))
+        self.num_reqs = len(self.ctx_len)
+        self.num_q_heads = int(batch["num_q_heads"])
+        self.num_kv_heads = int(batch["num_kv_heads"])
+        self.head_dim = int(batch["head_dim"])
+        self.sm_scale = float(batch.get("sm_scale", 0.0) or 0.0)
+        self.total_q = int(self.q_indptr[-1]) if len(self.q_indptr) else 0
+        self._desc = None
+
+    def desc(self):
+        a = lambda x: None if x is None else x.ctypes.data
+        d = BatchDesc(self.num_reqs, self.num_q_heads, self.num_kv_heads, self.head_dim,
+                      a(self.req_type), a(self.q_indptr), a(self.ctx_len), self.table_dev.data_ptr(),
+                      a(self.table_host), self.table_host.shape[1], a(self.group_of),
+                      len(self.group_prefix_blocks), a(self.group_prefix_blocks) if len(self.group_prefix_blocks) else None,
+                      self.sm_scale)
+        self._desc = d  # keep alive
+        return d
+
+    def as_dict(self):
+        """Descriptor as a dict of host arrays (for the oracle in tests)."""
+        return dict(num_reqs=self.num_reqs, num_q_heads=self.num_q_heads,
+                    num_kv_heads=self.num_kv_heads, head_dim=self.head_dim,
+                    q_indptr=self.q_indptr, ctx_len=self.ctx_len, block_table=self.table_host,
+                    group_of=self.group_of, group_prefix_blocks=self.group_prefix_blocks,
+                    sm_scale=self.sm_scale)
+
+
+def validate_batch(batch: "Batch", num_blocks: int, mode: int = 0) -> int:
+    """Host-only descriptor check; returns the status code (0 = OK)."""
+    return load().kva_validate_batch(ctypes.byref(batch.desc()), num_blocks, mode)
+
+
+def last_error() -> str:
+    return load().kva_last_error().decode()
+
+
+def _workspace(nbytes, device):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def kv_append_workspace_size(batch: Batch) -> int:
+    n = ctypes.c_size_t()
+    _check(load().kv_append_workspace_size(ctypes.byref(batch.desc()), ctypes.byref(n)))
+    return n.value
+
+
+def kv_append(pool: Pool, batch: Batch, k_new: torch.Tensor, v_new: torch.Tensor,
+              workspace: torch.Tensor | None = None, stream=None):
+    """Append K/V rows [total_q][Hkv][d] (a2).  Raises KvaError(NEEDS_EVICTION, deficit=...)."""
+    L = load()
+    d = batch.desc()
+    if workspace is None:
+        workspace = _workspace(kv_append_workspace_size(batch), k_new.device)
+    deficit = ctypes.c_int32(0)
+    st = L.kv_append(pool.handle, ctypes.byref(d), _ptr(k_new), _ptr(v_new), k_new.stride(0),
+                     ctypes.byref(deficit), _ptr(workspace), workspace.numel(), _stream(stream))
+    _check(st, deficit=deficit.value)
+    return workspace
+
+
+def hybrid_attention_workspace_size(batch: Batch) -> int:
+    n = ctypes.c_size_t()
+    _check(load().hybrid_attention_workspace_size(ctypes.byref(batch.desc()), ctypes.byref(n)))
+    return n.value
+
+
+class Plan:
+    """hybrid_attention_plan: work lists uploaded into `workspace`; reusable by run()."""
+
+    def __init__(self, pool: Pool, batch: Batch, workspace: torch.Tensor | None = None, stream=None,
+                 device=None):
+        L = load()
+        device = device or pool.k_pool.device
+        if workspace is None:
+            workspace = _workspace(hybrid_attention_workspace_size(batch), device)
+        self.workspace = workspace
+        self.handle = ctypes.c_void_p()
+        _check(L.hybrid_attention_plan(pool.handle, ctypes.byref(batch.desc()), _ptr(workspace),
+                                       workspace.numel(), _stream(stream), ctypes.byref(self.handle)))
+        self.batch = batch
+
+    def stats(self) -> dict:
+        s = PlanStats()
+        _check(load().kva_plan_get_stats(self.handle, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in PlanStats._fields_}
+
+    def run(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None, stream=None,
+            phases: int = PHASE_ALL):
+        out_dtype = OUT_F32 if out.dtype == torch.float32 else OUT_BF16
+        if out.dtype not in (torch.float32, torch.bfloat16):
+            raise KvaError(ERR_INVALID, "out must be bf16 or fp32")
+        _check(load().hybrid_attention_run_phases(self.handle, _ptr(q), q.stride(0), q.stride(1),
+                                                  _ptr(out), out.stride(0), out.stride(1), out_dtype,
+                                                  _ptr(lse), phases, _stream(stream)))
+        return out
+
+    def launch_count(self, phases: int = PHASE_ALL) -> int:
+        n = ctypes.c_int32()
+        _check(load().kva_plan_launch_count(self.handle, phases, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.handle:
+            load().kva_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def hybrid_attention(pool: Pool, batch: Batch, q: torch.Tensor, out: torch.Tensor | None = None,
+                     lse: torch.Tensor | None = None, out_dtype=torch.bfloat16,
+                     workspace: torch.Tensor | None = None, stream=None):
+    """One attention step of the mixed batch (plan + run).  q: [total_q][Hq][d] bf16."""
+    L = load()
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    if workspace is None:
+        workspace = _workspace(hybrid_attention_workspace_size(batch), q.device)
+    od = OUT_F32 if out.dtype == torch.float32 else OUT_BF16
+    _check(L.hybrid_attention(pool.handle, ctypes.byref(batch.desc()), _ptr(q), q.stride(0),
+                              q.stride(1), _ptr(out), out.stride(0), out.stride(1), od, _ptr(lse),
+                              _ptr(workspace), workspace.numel(), _stream(stream)))
+    return out
+
+
+def kv_release_blocks(pool: Pool, ids, stream=None):
+    """Return blocks (host int32 ids) to the free pool (recompute-mode release)."""
+    a = np.ascontiguousarray(ids, np.int32)
+    _check(load().kv_release_blocks(pool.handle, a.ctypes.data if a.size else None, a.size,
+                                    _stream(stream)))
+
+
+def evict_keys(state, rc, lat, depth=None, keys=None, stream=None):
+    """priority_of as u64 keys (a8) on device tensors (uint8/int32-as-u32/int16-as-u16)."""
+    L = load()
+    n = state.numel()
+    if keys is None:
+        keys = torch.empty(n, dtype=torch.int64, device=state.device)
+    _check(L.evict_keys(_ptr(state), _ptr(rc), _ptr(lat), _ptr(depth), n, _ptr(keys), _stream(stream)))
+    return keys
+
+
+def evict_select_workspace_size(n: int, k: int) -> int:
+    b = ctypes.c_size_t()
+    _check(load().evict_select_workspace_size(n, k, ctypes.byref(b)))
+    return b.value
+
+
+def evict_select(keys: torch.Tensor, k: int, out_ids: torch.Tensor | None = None, apply: bool = False,
+                 pool: Pool | None = None, workspace: torch.Tensor | None = None, stream=None,
+                 allow_short: bool = True, sync: bool = True):
+    """The k blocks with the smallest (key, id), in eviction order.  Returns (ids, n_selected);
+    with sync=False nothing waits for the device and n_selected is None."""
+    L = load()
+    n = keys.numel()
+    if out_ids is None:
+        out_ids = torch.empty(max(k, 1), dtype=torch.int32, device=keys.device)
+    if workspace is None:
+        workspace = _workspace(evict_select_workspace_size(n, k), keys.device)
+    nsel = ctypes.c_int64(0)
+    if not sync:
+        _check(L.evict_select(_ptr(keys), n, k, _ptr(out_ids), None, int(bool(apply)),
+                              pool.handle if pool is not None else None, _ptr(workspace),
+                              workspace.numel(), _stream(stream)))
+        return out_ids, None
+    st = L.evict_select(_ptr(keys), n, k, _ptr(out_ids), ctypes.byref(nsel), int(bool(apply)),
+                        pool.handle if pool is not None else None, _ptr(workspace), workspace.numel(),
+                        _stream(stream))
+    if st == EVICTION_SHORT and allow_short:
+        return out_ids[: nsel.value], nsel.value
+    _check(st)
+    return out_ids[: nsel.value], nsel.value
+
+
+def free_bits_tensor(free_bits_np: np.ndarray, device) -> torch.Tensor:
+    """uint32 numpy bitmap -> int32 device tensor with the same bits."""
+    return torch.from_numpy(np.ascontiguousarray(free_bits_np, np.uint32).view(np.int32).copy()).to(device)

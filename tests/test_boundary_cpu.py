@@ -1,0 +1,114 @@
+"""Boundary tests that need no GPU: the C-ABI library loads, exports every symbol declared in
+include/kvattn.h, and its host-side validation returns the contract's status codes
+(SURVEY §8(b) "Errors"; reading #8) before any device work."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def K():
+    import paper_2504_03651_b200 as K
+    K.load()
+    return K
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "kvattn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(?:kva_status|const char \*)\s*(\w+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(K):
+    names = _header_functions()
+    assert len(names) >= 15
+    lib = K.load()
+    for n in names:
+        assert hasattr(lib, n), n
+    from paper_2504_03651_b200.kvattn import EXPORTS
+    assert sorted(EXPORTS) == names
+
+
+def test_version_names_sm100a(K):
+    assert "sm_100a" in K.version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    from paper_2504_03651_b200 import _build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", _build.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _batch(K, wl, **over):
+    b = dict(wl.batch)
+    b.update(over)
+    return K.Batch(b, None)
+
+
+def test_validate_ok_and_errors(K):
+    reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 100, 30, 0), W.ReqSpec(W.OFFLINE_DECODE, 90, 1, 0)]
+    wl = W.make_workload(W.custom_config("v", 4, 2, 64, 13, reqs, [3]), preappended=True)
+    nb = wl.batch["num_blocks"]
+    assert K.validate_batch(_batch(K, wl), nb, 0) == K.OK
+    # queries inside the group prefix -> ERR_GROUP (reading #8)
+    assert K.validate_batch(_batch(K, wl, group_prefix_blocks=np.array([7], np.int32)), nb, 0) == K.ERR_GROUP
+    bt = wl.batch["block_table"].copy()
+    bt[1, 0] = bt[1, 5]
+    assert K.validate_batch(_batch(K, wl, block_table=bt), nb, 0) == K.ERR_GROUP
+    # q_len > ctx, Hq % Hkv, head_dim, unallocated block
+    assert K.validate_batch(_batch(K, wl, q_indptr=np.array([0, 101, 102], np.int32)), nb, 0) == K.ERR_INVALID
+    assert K.validate_batch(_batch(K, wl, num_q_heads=3), nb, 0) == K.ERR_INVALID
+    assert K.validate_batch(_batch(K, wl, head_dim=96), nb, 0) == K.ERR_UNSUPPORTED
+    bt = wl.batch["block_table"].copy()
+    bt[0, 6] = -1
+    assert K.validate_batch(_batch(K, wl, block_table=bt), nb, 0) == K.ERR_INVALID
+    assert "block_table" in K.last_error()
+
+
+def test_validate_append_mode_allows_unallocated_new_blocks(K):
+    wl = W.make_workload("tiny")   # pre-append: new blocks are -1
+    nb = wl.batch["num_blocks"]
+    assert K.validate_batch(_batch(K, wl), nb, 1) == K.OK
+    assert K.validate_batch(_batch(K, wl), nb, 0) == K.ERR_INVALID  # attention needs them
+
+
+def test_workspace_sizes_are_host_only(K):
+    for name in ["tiny", "llama7b", "qwen14b"]:
+        wl = W.make_workload(name) if name == "tiny" else None
+        if wl is None:
+            continue
+        b = _batch(K, wl)
+        assert K.hybrid_attention_workspace_size(b) > 0
+        assert K.kv_append_workspace_size(b) > 0
+    assert K.evict_select_workspace_size(1 << 20, 1 << 16) > (1 << 16) * 12
+
+
+def test_pool_create_rejects_before_cuda(K):
+    import ctypes
+    from paper_2504_03651_b200.kvattn import PoolDesc
+    L = K.load()
+    h = ctypes.c_void_p()
+    d = PoolDesc(16, 8, 1, 64, 1024, 2048, 4096, 0)  # block_size 8
+    assert L.kv_pool_create(ctypes.byref(d), ctypes.byref(h)) == K.ERR_UNSUPPORTED
+    d = PoolDesc(16, 16, 1, 96, 1024, 2048, 4096, 0)  # head_dim 96
+    assert L.kv_pool_create(ctypes.byref(d), ctypes.byref(h)) == K.ERR_UNSUPPORTED
+    assert L.evict_select(None, -1, 1, None, None, 0, None, None, 0, None) == K.ERR_INVALID
+
+
+def test_product_does_not_import_oracle():
+    """The product package never references oracle/ (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2504_03651_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "liboracle" not in txt, f

@@ -1,0 +1,82 @@
+"""GPU parity for evict_keys / evict_select: bit-exact keys and eviction order vs the oracle
+(S:146)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a).view(dtype)).cuda()
+
+
+def _gpu_keys(ev):
+    import paper_2504_03651_b200 as K
+    st = _dev(ev.state, np.uint8)
+    rc = _dev(ev.rc.view(np.int32), np.int32)
+    lat = _dev(ev.lat.view(np.int32), np.int32)
+    dep = _dev(ev.depth.view(np.int16), np.int16) if ev.depth is not None else None
+    return K.evict_keys(st, rc, lat, dep)
+
+
+@pytest.mark.parametrize("straddle", [False, True])
+def test_evict_full_size(straddle):
+    import paper_2504_03651_b200 as K
+    ev = W.make_evict(straddle=straddle)
+    keys = _gpu_keys(ev)
+    s, ref_keys = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    torch.cuda.synchronize()
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), ref_keys)
+    ids, n = K.evict_select(keys, ev.k)
+    s, ref_ids = oracle.evict_select(ref_keys, ev.k)
+    assert n == len(ref_ids) == ev.k
+    assert np.array_equal(ids.cpu().numpy(), ref_ids)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_evict_random_small(seed):
+    import paper_2504_03651_b200 as K
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 50000))
+    ev = W.make_evict(n=n, k=int(rng.integers(1, n + 10)), seed=seed, run_lo=1, run_hi=9)
+    # force many equal keys: coarse lat
+    ev.lat[:] = ev.lat % 3
+    keys = _gpu_keys(ev)
+    s, ref_keys = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    ids, nsel = K.evict_select(keys, ev.k)
+    s2, ref_ids = oracle.evict_select(ref_keys, ev.k)
+    assert nsel == len(ref_ids)
+    assert np.array_equal(ids.cpu().numpy(), ref_ids)
+
+
+def test_evict_apply_marks_free():
+    import paper_2504_03651_b200 as K
+    ev = W.make_evict(n=4096, k=100, seed=9)
+    keys = _gpu_keys(ev)
+    nb = 4096
+    kp = torch.zeros((nb, 1, 16, 64), dtype=torch.bfloat16, device="cuda")
+    bits = np.zeros((nb + 31) // 32, np.uint32)
+    fb = K.free_bits_tensor(bits, "cuda")
+    pool = K.Pool(kp, kp.clone(), fb)
+    ids, n = K.evict_select(keys, 100, apply=True, pool=pool)
+    torch.cuda.synchronize()
+    got = fb.cpu().numpy().view(np.uint32)
+    exp = np.zeros_like(bits)
+    for i in ids.cpu().numpy():
+        exp[i // 32] |= np.uint32(1 << (i % 32))
+    assert np.array_equal(got, exp)
+    assert pool.free_count() == 100
+
+
+def test_evict_short():
+    import paper_2504_03651_b200 as K
+    st = np.array([1, 2, 5, 4, 0], np.uint8)
+    ev = W.EvictWorkload(st, np.zeros(5, np.uint32), np.arange(5, dtype=np.uint32),
+                         np.zeros(5, np.uint16), 4, None, None)
+    keys = _gpu_keys(ev)
+    ids, n = K.evict_select(keys, 4)
+    assert n == 2 and list(ids.cpu().numpy()) == [2, 3]
