@@ -178,9 +178,15 @@ def run_ours(args, rank, world, local):
     h_out = torch.empty((gbuf if world > 1 else out).shape, dtype=out.dtype).pin_memory()
 
     launches = {"n": 0}
-    dec_ev = []
 
-    def step(e2e=False, time_decode=False):
+    tim = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for e4 in tim:
+        for e in e4:
+            e.record(stream)   # materialise the cudaEvent_t handles
+    torch.cuda.synchronize()
+    tim_used = []
+
+    def step(e2e=False, time_idx=None):
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
         batch.table_host[...] = pristine_host
         if e2e:
@@ -190,17 +196,10 @@ def run_ours(args, rank, world, local):
         K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
         n = 2 + plan.launch_count()
-        if time_decode:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            plan.run(q, out, lse, stream=stream, phases=K.PHASE_TILE)
-            a.record(stream)
-            plan.run(q, out, lse, stream=stream, phases=K.PHASE_DECODE)
-            b.record(stream)
-            plan.run(q, out, lse, stream=stream, phases=K.PHASE_MERGE)
-            dec_ev.append((a, b))
-        else:
-            plan.run(q, out, lse, stream=stream)
+        if time_idx is not None:
+            plan.set_timing_events(*tim[time_idx])
+            tim_used.append(tim[time_idx])
+        plan.run(q, out, lse, stream=stream)
         if world > 1:
             import torch.distributed as dist
             dist.all_gather_into_tensor(gbuf, out)
@@ -224,13 +223,13 @@ def run_ours(args, rank, world, local):
             dist.barrier()
             torch.cuda.synchronize()
 
-    def timed(nsteps, e2e=False, time_decode=False):
+    def timed(nsteps, e2e=False, time_kernels=False):
         barrier()
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        for _ in range(nsteps):
-            step(e2e=e2e, time_decode=time_decode)
+        for i in range(nsteps):
+            step(e2e=e2e, time_idx=i if time_kernels else None)
         e.record(stream)
         barrier()
         ms = s.elapsed_time(e) / nsteps
@@ -252,10 +251,11 @@ def run_ours(args, rank, world, local):
     if not args.profile:
         clocks.start()
     launches["n"] = 0
-    ms = timed(args.steps, time_decode=True)
+    ms = timed(args.steps, time_kernels=True)
     gpu_launches = launches["n"]
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
-    dec_ms = [a.elapsed_time(b) for a, b in dec_ev]
+    dec_ms = [e4[2].elapsed_time(e4[3]) for e4 in tim_used if stats["n_decode_items"] > 0]
+    tile_ms = [e4[0].elapsed_time(e4[1]) for e4 in tim_used if stats["n_tile_items"] > 0]
     ms_e2e = None
     if not args.no_e2e and not args.profile:
         for _ in range(2):
@@ -284,7 +284,10 @@ def run_ours(args, rank, world, local):
                            ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+evict_keys+evict_select(1M,k=64k)") +
                            "+release",
                    "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
-                   "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype},
+                   "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
+                   "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
+                   "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
+                   "overlap": "tile (tcgen05) on a side stream concurrent with decode"},
         "roofline": {"bound": "hbm", "kernel": "decode_kernel (split-KV)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(), "bytes_per_launch": dec_bytes, "peak_source": peak_src},

@@ -172,6 +172,11 @@ kva_status hybrid_attention_run_phases(const kva_plan *plan, const void *q, int6
                                        int64_t q_stride_head, void *out, int64_t o_stride_tok,
                                        int64_t o_stride_head, int32_t out_dtype, float *lse,
                                        int32_t phases, kva_stream_t stream);
+/* Instrumentation: cudaEvent_t handles (or NULL) recorded immediately before/after the tile
+ * kernel launch (on the stream it runs on) and the decode kernel launch (on the caller's
+ * stream) by every later run of this plan — per-kernel timing inside an overlapped step. */
+kva_status kva_plan_set_timing_events(kva_plan *plan, void *tile_begin, void *tile_end,
+                                      void *decode_begin, void *decode_end);
 /* Number of kernel launches hybrid_attention_run_phases(plan, phases) enqueues. */
 kva_status kva_plan_launch_count(const kva_plan *plan, int32_t phases, int32_t *n_launches);
 kva_status kva_plan_destroy(kva_plan *plan);
@@ -182,6 +187,7 @@ typedef struct {
   int64_t q_bytes, o_bytes;         /* bf16 Q read + O written */
   int64_t decode_kv_bytes;          /* KV bytes read by the split-KV (decode) kernel */
   int64_t flops;                    /* 4*d per (q-head, query, visible key) */
+  int64_t tile_flops;               /* the part of `flops` done by the tensor-core tile kernel */
 } kva_plan_stats;
 kva_status kva_plan_get_stats(const kva_plan *plan, kva_plan_stats *stats);
 kva_status hybrid_attention(kva_pool *pool, const kva_batch_desc *desc, const void *q,

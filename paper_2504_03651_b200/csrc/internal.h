@@ -11,7 +11,8 @@ namespace kva {
 constexpr int kBlock = 16;        // tokens per KV block (reading #5)
 constexpr int kSplitKeys = 512;   // fixed split-KV length (depends only on ctx, H9)
 constexpr int kDecodeRows = 16;   // rows (q tokens x g heads) one decode warp handles
-constexpr int kTileM = 64;        // rows per tile-kernel CTA (4 warps x 16)
+constexpr int kTileMMma = 64;     // rows per legacy mma.sync tile CTA (4 warps x 16)
+constexpr int kTileMTc = 128;     // rows per tcgen05 tile CTA (UMMA M = TMEM lanes)
 constexpr int kTileN = 64;        // keys per tile-kernel pipeline stage (4 blocks)
 
 // One decode warp: <= 16 rows (tok*g + hh) of one request and kv-head over keys [k0, k1).
@@ -73,6 +74,8 @@ cudaError_t launch_decode(const AttnParams &p, const void *tmap_k, const void *t
                           const DecodeItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                         const TileItem *items, int n_items, cudaStream_t s);
+cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
+                           const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
                          int n_rows, cudaStream_t s);
 cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,
@@ -87,6 +90,8 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 size_t evict_select_ws_bytes(int64_t n, int64_t k);
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t s);
+constexpr int kReleaseBatch = 4000;  // ids per release launch (kernel-parameter payload)
+cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s);
 cudaError_t launch_free_ids(uint32_t *free_bits, const int32_t *ids, const int64_t *d_count,
                             int64_t k, cudaStream_t s);
 

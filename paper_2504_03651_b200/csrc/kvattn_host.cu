@@ -154,6 +154,10 @@ struct kva_pool {
   int64_t n_free = 0;
   CUtensorMap tmk, tmv;
   Staging staging;
+  // side stream for the tensor-core tile kernel (runs concurrently with the HBM-bound
+  // decode kernel on the caller's stream; fork/join by events)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static int64_t count_free(const std::vector<uint32_t> &w, int nb) {
@@ -188,6 +192,16 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
     return fail(KVA_ERR_CUDA, "reading free_bits: %s", cudaGetErrorString(e));
   }
   p->n_free = count_free(p->free_host, d->num_blocks);
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      delete p;
+      return fail(KVA_ERR_CUDA, "creating the side stream/events failed");
+    }
+  }
   const int64_t rows = (int64_t)d->num_blocks * d->num_kv_heads * kBlock;
   kva_status st = make_pool_map(&p->tmk, d->k_pool, rows, d->head_dim);
   if (st == KVA_OK) st = make_pool_map(&p->tmv, d->v_pool, rows, d->head_dim);
@@ -204,6 +218,9 @@ extern "C" kva_status kv_pool_destroy(kva_pool *p) {
   {
     DeviceGuard dg(p->desc.device);
     p->staging.release();
+    if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
   }
   delete p;
   return KVA_OK;
@@ -417,6 +434,12 @@ struct kva_plan {
   const int32_t *d_mslots = nullptr;
   int n_dec = 0, n_tile = 0, n_mrows = 0;
   int device = 0;
+  bool tile_tc = true;
+  int tile_ctas = 0;              // persistent tile-kernel grid (0 = all SMs)
+  bool overlap = true;            // tile kernel on the side stream, concurrent with decode
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t t_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events
   kva_plan_stats stats{};
 };
 
@@ -426,10 +449,23 @@ struct PlanBuild {
   std::vector<MergeRow> mrows;
   std::vector<int32_t> mslots, row_list;
   int64_t n_slots = 0;
+  int64_t tile_flops = 0;
   kva_plan_stats stats{};
 };
 
+// Tile kernel: tcgen05/TMEM (128-row tiles, default) or the legacy mma.sync kernel (64-row
+// tiles) kept as an independent cross-check (KVA_TILE_IMPL=mma).
+static bool tile_use_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("KVA_TILE_IMPL");
+    v = (e && std::string(e) == "mma") ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
+  const int kTileM = tile_use_tc() ? kTileMTc : kTileMMma;
   const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
   const int d = b->head_dim;
   const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
@@ -544,6 +580,14 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   }
   // longest tiles first (LPT); ties keep (kv_head, m-tile, member) order so concurrently
   // running CTAs of a group share its prefix blocks in L2
+  for (const TileItem &t : pb.tile) {
+    if (t.flags & kTileCausal) {  // row r sees keys [0, pos0 + r/g]
+      for (int r = t.r0; r < t.r0 + t.n_rows; ++r) pb.stats.tile_flops += (int64_t)(t.pos0 + r / g + 1) * 4 * d;
+    } else {
+      pb.stats.tile_flops += (int64_t)t.n_rows * (t.k1 - t.k0) * 4 * d;
+    }
+  }
+  pb.tile_flops = pb.stats.tile_flops;
   std::stable_sort(pb.tile.begin(), pb.tile.end(),
                    [](const TileItem &a, const TileItem &c) { return a.k1 - a.k0 > c.k1 - c.k0; });
   pb.stats.n_decode_items = (int64_t)pb.dec.size();
@@ -622,6 +666,27 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       return fail(KVA_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
     }
   }
+  pl->tile_tc = tile_use_tc();
+  pl->aux = p->aux;
+  pl->ev_fork = p->ev_fork;
+  pl->ev_join = p->ev_join;
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->desc.device);
+    const char *e = getenv("KVA_TILE_CTAS");
+    const char *o = getenv("KVA_OVERLAP");
+    pl->overlap = !(o && std::string(o) == "0");
+    if (e) pl->tile_ctas = atoi(e);
+    else if (pb.dec.empty() || !pl->overlap) pl->tile_ctas = nsm;
+    else {
+      // split the SMs between the tensor-bound tile kernel and the HBM-bound decode kernel in
+      // proportion to their standalone times (measured rates), >= 1/4 each
+      const double t_tile = (double)pb.tile_flops / (nsm * 2.5e12);
+      const double t_dec = (double)pb.stats.decode_kv_bytes / 6.7e12;
+      const double f = t_tile / (t_tile + t_dec);
+      pl->tile_ctas = std::max(nsm / 4, std::min(nsm - nsm / 4, (int)(nsm * f + 0.5)));
+    }
+  }
   pl->n_dec = (int)pb.dec.size();
   pl->n_tile = (int)pb.tile.size();
   pl->n_mrows = (int)pb.mrows.size();
@@ -679,8 +744,29 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.o_stride_head = o_sh;
   p.out_f32 = out_dtype == KVA_OUT_F32;
   p.lse = lse;
-  if (phases & KVA_PHASE_TILE) CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, s));
-  if (phases & KVA_PHASE_DECODE) CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
+  const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
+  const bool do_dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
+  const bool fork = do_tile && do_dec && pl->overlap && pl->tile_tc;
+  cudaStream_t ts = s;
+  if (fork) {  // tile kernel first on the high-priority side stream, then decode on `s`
+    CUDA_TRY(cudaEventRecord(pl->ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(pl->aux, pl->ev_fork, 0));
+    ts = pl->aux;
+  }
+  if (do_tile && pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
+  if (do_tile) {
+    if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+                                             fork ? pl->tile_ctas : 0, ts));
+    else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
+  }
+  if (do_tile && pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], ts));
+  if (do_dec && pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
+  if (do_dec) CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
+  if (do_dec && pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(pl->ev_join, pl->aux));
+    CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_join, 0));
+  }
   if (phases & KVA_PHASE_MERGE) CUDA_TRY(launch_merge(p, pl->d_mrows, pl->d_mslots, pl->n_mrows, s));
   return KVA_OK;
 }
@@ -690,6 +776,16 @@ extern "C" kva_status hybrid_attention_run(const kva_plan *pl, const void *q, in
                                            int32_t out_dtype, float *lse, kva_stream_t stream) {
   return hybrid_attention_run_phases(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse,
                                      KVA_PHASE_ALL, stream);
+}
+
+extern "C" kva_status kva_plan_set_timing_events(kva_plan *pl, void *tile_begin, void *tile_end,
+                                                 void *decode_begin, void *decode_end) {
+  if (!pl) return fail(KVA_ERR_INVALID, "null plan");
+  pl->t_ev[0] = static_cast<cudaEvent_t>(tile_begin);
+  pl->t_ev[1] = static_cast<cudaEvent_t>(tile_end);
+  pl->t_ev[2] = static_cast<cudaEvent_t>(decode_begin);
+  pl->t_ev[3] = static_cast<cudaEvent_t>(decode_end);
+  return KVA_OK;
 }
 
 extern "C" kva_status kva_plan_launch_count(const kva_plan *pl, int32_t phases, int32_t *n) {
@@ -716,17 +812,12 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
   }
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Staging::Slot *slot = nullptr;
-  const size_t bytes = 16 + n * 4;  // [int64 n][pad][ids]
-  CUDA_TRY(p->staging.get(bytes, &slot));
-  std::memcpy(slot->host, &n, sizeof n);
-  std::memcpy(static_cast<uint8_t *>(slot->host) + 16, ids, n * 4);
-  uint8_t *d_buf = nullptr;
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&d_buf), bytes, s));
-  CUDA_TRY(p->staging.upload(slot, d_buf, bytes, s));
-  CUDA_TRY(launch_free_ids(p->desc.free_bits, reinterpret_cast<const int32_t *>(d_buf + 16),
-                           reinterpret_cast<const int64_t *>(d_buf), n, s));
-  CUDA_TRY(cudaFreeAsync(d_buf, s));
+  // ids travel as kernel parameters (<= kReleaseBatch per launch): no device scratch,
+  // no host<->device copy, stream-ordered like every other call
+  for (int64_t off = 0; off < n; off += kReleaseBatch) {
+    const int cnt = (int)std::min<int64_t>(kReleaseBatch, n - off);
+    CUDA_TRY(launch_release_ids(p->desc.free_bits, ids + off, cnt, s));
+  }
   for (int64_t i = 0; i < n; ++i) p->free_host[ids[i] >> 5] |= 1u << (ids[i] & 31);
   p->n_free += n;
   return KVA_OK;

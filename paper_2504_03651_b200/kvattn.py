@@ -49,13 +49,14 @@ class PlanStats(ctypes.Structure):
                 ("n_cascade_items", ctypes.c_int64), ("n_merge_rows", ctypes.c_int64),
                 ("kv_bytes_algorithmic", ctypes.c_int64), ("q_bytes", ctypes.c_int64),
                 ("o_bytes", ctypes.c_int64), ("decode_kv_bytes", ctypes.c_int64),
-                ("flops", ctypes.c_int64)]
+                ("flops", ctypes.c_int64), ("tile_flops", ctypes.c_int64)]
 
 
 EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_create", "kv_pool_destroy",
            "kv_pool_free_count", "kv_pool_resync", "kv_append_workspace_size", "kv_append",
            "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
-           "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_destroy",
+           "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
+           "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
            "evict_select_workspace_size", "evict_select"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
@@ -93,6 +94,7 @@ def load(build_if_missing: bool = True):
         "hybrid_attention_run": ([P, P, i64, i64, P, i64, i64, i32, P, P], ctypes.c_int),
         "hybrid_attention_run_phases": ([P, P, i64, i64, P, i64, i64, i32, P, i32, P], ctypes.c_int),
         "kva_plan_launch_count": ([P, i32, P], ctypes.c_int),
+        "kva_plan_set_timing_events": ([P, P, P, P, P], ctypes.c_int),
         "kv_release_blocks": ([P, P, i64, P], ctypes.c_int),
         "kva_plan_destroy": ([P], ctypes.c_int),
         "kva_plan_get_stats": ([P, P], ctypes.c_int),
@@ -272,6 +274,12 @@ class Plan:
                                                   _ptr(out), out.stride(0), out.stride(1), out_dtype,
                                                   _ptr(lse), phases, _stream(stream)))
         return out
+
+    def set_timing_events(self, tile_begin=None, tile_end=None, decode_begin=None, decode_end=None):
+        """torch.cuda.Event objects (already recorded once, so their handles exist)."""
+        h = lambda e: None if e is None else ctypes.c_void_p(e.cuda_event)
+        _check(load().kva_plan_set_timing_events(self.handle, h(tile_begin), h(tile_end),
+                                                 h(decode_begin), h(decode_end)))
 
     def launch_count(self, phases: int = PHASE_ALL) -> int:
         n = ctypes.c_int32()
