@@ -67,6 +67,7 @@ struct AttnParams {
   float *part_o;          // [slots][d]
   float *part_lse;        // [slots]
   const int32_t *row_list;
+  unsigned long long *dbg;  // optional timestamps (diagnostics; KVA_DEBUG_TS), nullable
 };
 
 // launchers (kernels_*.cu)
@@ -76,6 +77,8 @@ cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tma
                         const TileItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
+cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
+                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
                          int n_rows, cudaStream_t s);
 cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,

@@ -435,6 +435,7 @@ struct kva_plan {
   int n_dec = 0, n_tile = 0, n_mrows = 0;
   int device = 0;
   bool tile_tc = true;
+  int tile_impl = 2;
   int tile_ctas = 0;              // persistent tile-kernel grid (0 = all SMs)
   bool overlap = true;            // tile kernel on the side stream, concurrent with decode
   cudaStream_t aux = nullptr;
@@ -455,17 +456,21 @@ struct PlanBuild {
 
 // Tile kernel: tcgen05/TMEM (128-row tiles, default) or the legacy mma.sync kernel (64-row
 // tiles) kept as an independent cross-check (KVA_TILE_IMPL=mma).
-static bool tile_use_tc() {
+// 0 = legacy mma.sync (64-row tiles), 1 = tcgen05 one-Q-tile (128 rows), 2 = tcgen05
+// two-Q-tile (256 rows, default).  KVA_TILE_IMPL=mma|tc1|tc2 selects one (cross-checks).
+static int tile_impl() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("KVA_TILE_IMPL");
-    v = (e && std::string(e) == "mma") ? 0 : 1;
+    const std::string s = e ? e : "";
+    v = s == "mma" ? 0 : s == "tc1" ? 1 : 2;
   }
-  return v == 1;
+  return v;
 }
+static bool tile_use_tc() { return tile_impl() != 0; }
 
 static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
-  const int kTileM = tile_use_tc() ? kTileMTc : kTileMMma;
+  const int kTileM = tile_impl() == 2 ? 2 * kTileMTc : tile_impl() == 1 ? kTileMTc : kTileMMma;
   const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
   const int d = b->head_dim;
   const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
@@ -667,6 +672,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     }
   }
   pl->tile_tc = tile_use_tc();
+  pl->tile_impl = tile_impl();
   pl->aux = p->aux;
   pl->ev_fork = p->ev_fork;
   pl->ev_join = p->ev_join;
@@ -679,11 +685,14 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     if (e) pl->tile_ctas = atoi(e);
     else if (pb.dec.empty() || !pl->overlap) pl->tile_ctas = nsm;
     else {
-      // split the SMs between the tensor-bound tile kernel and the HBM-bound decode kernel in
-      // proportion to their standalone times (measured rates), >= 1/4 each
-      const double t_tile = (double)pb.tile_flops / (nsm * 2.5e12);
+      // split the SMs between the tensor-bound tile kernel and the HBM-bound decode kernel:
+      // proportional to their standalone times (measured ~3.9 TFLOP/s per SM and 6.7 TB/s),
+      // skewed 1.75x towards the tile kernel because the decode stream keeps HBM saturated
+      // with fewer SMs than its standalone share (measured optimum on llama7b);
+      // >= 1/4 of the SMs each
+      const double t_tile = (double)pb.tile_flops / (nsm * 3.9e12);
       const double t_dec = (double)pb.stats.decode_kv_bytes / 6.7e12;
-      const double f = t_tile / (t_tile + t_dec);
+      const double f = 1.75 * t_tile / (t_tile + t_dec);
       pl->tile_ctas = std::max(nsm / 4, std::min(nsm - nsm / 4, (int)(nsm * f + 0.5)));
     }
   }
@@ -744,6 +753,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.o_stride_head = o_sh;
   p.out_f32 = out_dtype == KVA_OUT_F32;
   p.lse = lse;
+  p.dbg = nullptr;
+  if (const char *e = getenv("KVA_DEBUG_TS")) p.dbg = reinterpret_cast<unsigned long long *>(strtoull(e, nullptr, 0));
   const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
   const bool do_dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
   const bool fork = do_tile && do_dec && pl->overlap && pl->tile_tc;
@@ -755,8 +766,10 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   }
   if (do_tile && pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
   if (do_tile) {
-    if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
-                                             fork ? pl->tile_ctas : 0, ts));
+    if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+                                                     fork ? pl->tile_ctas : 0, ts));
+    else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+                                                  fork ? pl->tile_ctas : 0, ts));
     else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
   }
   if (do_tile && pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], ts));
