@@ -142,6 +142,7 @@ def ncu_traffic(kernel="decode_kernel"):
 def run_ours(args, rank, world, local):
     import paper_2504_03651_b200 as K
     import workloads as W
+    from paper_2504_03651_b200 import dist as kdist
 
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -201,8 +202,7 @@ def run_ours(args, rank, world, local):
             tim_used.append(tim[time_idx])
         plan.run(q, out, lse, stream=stream)
         if world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gbuf, out)
+            kdist.gather_outputs(out, gbuf)
         if ev is not None:
             K.evict_keys(ev["state"], ev["rc"], ev["lat"], ev["depth"], keys=ev["keys"], stream=stream)
             K.evict_select(ev["keys"], ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=stream,

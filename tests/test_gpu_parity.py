@@ -190,7 +190,28 @@ def test_needs_eviction_atomic_gpu():
     assert pool.free_count() == 19
 
 
-@pytest.mark.parametrize("name", ["llama7b", "qwen14b"])
+def test_gqa8_long_chunks_with_group():
+    """llama70b-shaped (g = 8) at small size: 256-row tcgen05 items over both Q tiles,
+    prefix read through the member tables, causal tails, ragged chunk lengths."""
+    reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 600 + 300, 300, 0), W.ReqSpec(W.OFFLINE_PREFILL, 600 + 173, 173, 0),
+            W.ReqSpec(W.ONLINE_DECODE, 2000, 1), W.ReqSpec(W.ONLINE_DECODE, 77, 1)]
+    wl = W.make_workload(W.custom_config("g8", 16, 2, 128, 41, reqs, [600 // 16]))
+    gg = gpu_step(wl)
+    r = oracle_step(wl)
+    _check_append(gg, r)
+    assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
+
+
+def test_d64_chunks_and_cascade():
+    reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 400, 250, 0)] + [W.ReqSpec(W.OFFLINE_DECODE, 160 + i, 1, 0) for i in range(30)]
+    wl = W.make_workload(W.custom_config("d64", 8, 2, 64, 43, reqs, [9]))
+    gg = gpu_step(wl)
+    r = oracle_step(wl)
+    _check_append(gg, r)
+    assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
+
+
+@pytest.mark.parametrize("name", ["llama7b", "qwen14b", "llama70b"])
 def test_full_size_sampled(name):
     """BASELINE configs at full size, in the bench's launch configuration; sampled rows."""
     wl = W.make_workload(name, device="cuda")
