@@ -188,6 +188,7 @@ typedef struct {
   int64_t decode_kv_bytes;          /* KV bytes read by the split-KV (decode) kernel */
   int64_t flops;                    /* 4*d per (q-head, query, visible key) */
   int64_t tile_flops;               /* the part of `flops` done by the tensor-core tile kernel */
+  int64_t host_validate_ns, host_build_ns, host_total_ns;  /* host cost of this plan call */
 } kva_plan_stats;
 kva_status kva_plan_get_stats(const kva_plan *plan, kva_plan_stats *stats);
 kva_status hybrid_attention(kva_pool *pool, const kva_batch_desc *desc, const void *q,

@@ -17,13 +17,15 @@
 #include <cuda.h>
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace kva {
 using namespace dev;
 
-template <int D, int NST>
+template <int D, int NST, int PF>
 __global__ void __launch_bounds__(128, 2)
     decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
                   const __grid_constant__ CUtensorMap tmv, const DecodeItem *__restrict__ items,
@@ -69,10 +71,25 @@ __global__ void __launch_bounds__(128, 2)
     for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
   };
 
+  // L2 prefetch PF blocks beyond the TMA ring: keeps more HBM requests in flight per SM than
+  // shared memory could hold, so the stream saturates HBM on fewer SMs (co-running kernels)
+  auto prefetch = [&](int id) {  // lane 0 only
+    const int row = id * p.Hkv * kBlock + row_base;
+#pragma unroll
+    for (int h = 0; h < HALVES; ++h) {
+      tma_prefetch_2d(&tmk, h * 64, row);
+      tma_prefetch_2d(&tmv, h * 64, row);
+    }
+  };
 #pragma unroll
   for (int s = 0; s < NST; ++s) {
     const int id = __shfl_sync(0xffffffffu, my_id, s);
     if (lane == 0 && s < nblk) issue(s, id);
+  }
+#pragma unroll
+  for (int s = NST; s < NST + PF; ++s) {
+    const int id = __shfl_sync(0xffffffffu, my_id, s & 31);
+    if (lane == 0 && s < nblk) prefetch(id);
   }
 
   // Q fragments (A operand, rows = tok*g + hh)
@@ -109,6 +126,7 @@ __global__ void __launch_bounds__(128, 2)
   for (int j = 0; j < nblk; ++j) {
     const int st = j % NST;
     const int next_id = __shfl_sync(0xffffffffu, my_id, (j + NST) & 31);
+    const int pf_id = __shfl_sync(0xffffffffu, my_id, (j + NST + PF) & 31);
     mbar_wait(&bar[st], (j / NST) & 1);
     const uint32_t kb = smem_u32(ws + st * STAGE), vb = kb + KBYTES;
     const int key0 = (b0 + j) * kBlock;
@@ -204,6 +222,7 @@ __global__ void __launch_bounds__(128, 2)
     if (lane == 0 && j + NST < nblk) {
       fence_proxy_async();
       issue(st, next_id);
+      if (j + NST + PF < nblk) prefetch(pf_id);
     }
   }
   // row sums across the quad
@@ -249,12 +268,15 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-template <int D, int NST>
+template <int D, int NST, int PF>
 static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const void *tmv,
                                    const DecodeItem *items, int n, cudaStream_t s) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;  // + alignment slack
-  auto kern = decode_kernel<D, NST>;
+  auto kern = decode_kernel<D, NST, PF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
   const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
@@ -265,8 +287,17 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
                           const DecodeItem *items, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  if (p.d == 128) return launch_decode_t<128, 3>(p, tmk, tmv, items, n, s);
-  return launch_decode_t<64, 4>(p, tmk, tmv, items, n, s);
+  static const int pf = [] {
+    const char *e = getenv("KVA_DECODE_PF");
+    return e ? atoi(e) : 0;  // L2 prefetch measured counter-productive
+  }();
+  if (p.d == 128) {
+    if (pf <= 0) return launch_decode_t<128, 3, 0>(p, tmk, tmv, items, n, s);
+    if (pf <= 4) return launch_decode_t<128, 3, 4>(p, tmk, tmv, items, n, s);
+    if (pf <= 6) return launch_decode_t<128, 3, 6>(p, tmk, tmv, items, n, s);
+    return launch_decode_t<128, 3, 10>(p, tmk, tmv, items, n, s);
+  }
+  return launch_decode_t<64, 4, 6>(p, tmk, tmv, items, n, s);
 }
 
 }  // namespace kva

@@ -58,10 +58,10 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 
 // ---------------------------------------------------------------------------------------
 namespace {
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;  // leaves registers/smem for a co-resident decode CTA
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCtas = 1024;
-constexpr int kCandCap = 16384;  // candidate indices per CTA slice (u16)
+constexpr int kCandCap = 65535;  // candidate lists use u16 slice indices
 
 struct SelWs {  // global scratch (zeroed by the host before launch)
   unsigned long long t[32];      // phase timestamps of CTA 0 (%globaltimer, ns; diagnostics)
@@ -145,7 +145,7 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long a,
   return t;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     evict_select_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t k,
                         int32_t *__restrict__ out_ids, int64_t *__restrict__ d_count,
                         SelWs *__restrict__ sw, SortWs *__restrict__ so, uint64_t *pk0,
@@ -168,16 +168,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ long long s_warp64[32];
   __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_sel[4];
-  __shared__ __align__(16) unsigned int s_wcnt[kWarps][256];  // 32 KB
+  __shared__ __align__(16) unsigned int s_wcnt[kWarps][256];  // 16 KB
   const int C = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const int64_t per = (n + C - 1) / C;
   const int64_t lo = std::min<int64_t>(n, c * per), hi = std::min<int64_t>(n, lo + per);
   const int64_t cnt = hi - lo;
   // candidate index lists (u16, double-buffered) after the cached keys: every select round
   // scans only the keys still matching the chosen digit prefix
+  const bool use_cand = cache_keys && per <= kCandCap;
   uint16_t *cand[2] = {reinterpret_cast<uint16_t *>(s_keys + (cache_keys ? per : 0)), nullptr};
-  cand[1] = cand[0] + kCandCap;
-  const bool use_cand = cache_keys && cnt <= kCandCap;
+  cand[1] = cand[0] + per;
   __shared__ int s_ncand[2];
   if (tid == 0) s_ncand[0] = s_ncand[1] = 0;
   __syncthreads();
@@ -338,47 +338,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   stamp();
   // ---------------- 3. stable LSD radix sort of (key, id) by key ----------------
-  // S = ceil(m / 1024) sorter CTAs hold ONE element per thread (<= 64 for k = 64k).  Per
-  // 8-bit pass: warp match_any ranks + per-warp digit counts give each element's stable rank
-  // inside its CTA and the CTA's digit histogram; one grid barrier publishes histograms,
-  // each sorter derives its digit bases (digits below, same digit in earlier CTAs) and
-  // scatters; a second barrier ends the pass.
+  // S = min(#CTAs, ceil(m / kThreads)) sorter CTAs own contiguous ranges (one element per
+  // thread for k = 64k).  Per 8-bit pass over the varying bytes only: (A) each sorter's digit
+  // histogram -> global; grid barrier; (B) digit bases = digits below (all sorters) + same
+  // digit in earlier sorters, then a stable scatter chunk by chunk (warp match_any ranks +
+  // exclusive per-warp digit prefix); grid barrier ends the pass.
   uint64_t *ka = pk0, *kb = pk1;
   int32_t *ia = pi0, *ib = pi1;
   const int64_t m = (int64_t)n_sel;
   const int S = (int)std::min<int64_t>(C, std::max<int64_t>(1, (m + kThreads - 1) / kThreads));
+  const int64_t sper = (m + S - 1) / S;
   const bool sorter = c < S;
-  const int64_t i_el = (int64_t)c * kThreads + tid;
-  const bool have = sorter && i_el < m;
+  const int64_t slo = sorter ? std::min<int64_t>(m, c * sper) : 0;
+  const int64_t shi = sorter ? std::min<int64_t>(m, slo + sper) : 0;
   const int w = tid >> 5;
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 8 * pass;
     if (((vary >> shift) & 0xFF) == 0) continue;
-    uint64_t x = 0;
-    int32_t xid = 0;
-    int dg = 256, wr = 0;
     if (sorter) {
-      if (have) {
-        x = ka[i_el];
-        xid = ia[i_el];
-        dg = (int)((x >> shift) & 0xFF);
-      }
-      uint4 *z = reinterpret_cast<uint4 *>(&s_wcnt[0][0]);
-      for (int e = tid; e < kWarps * 256 / 4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
+      for (int i = tid; i < 256; i += kThreads) s_hist[i] = 0;
       __syncthreads();
-      const unsigned peers = __match_any_sync(0xffffffffu, dg);
-      wr = __popc(peers & lanemask_lt());
-      if (dg < 256 && wr == 0) s_wcnt[w][dg] = __popc(peers);
-      __syncthreads();
-      if (tid < 256) {  // exclusive prefix over warps per digit; total = CTA histogram
-        unsigned int acc = 0;
-        for (int ww = 0; ww < kWarps; ++ww) {
-          const unsigned int v = s_wcnt[ww][tid];
-          s_wcnt[ww][tid] = acc;
-          acc += v;
-        }
-        so->hist[c][tid] = acc;
+      for (int64_t base = slo; base < shi; base += kThreads) {
+        const int64_t i = base + tid;
+        hist_add_fast(s_hist, i < shi ? (int)((ka[i] >> shift) & 0xFF) : 256);
       }
+      __syncthreads();
+      for (int i = tid; i < 256; i += kThreads) so->hist[c][i] = s_hist[i];
     }
     grid.sync();
     if (sorter) {
@@ -395,10 +380,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int below = block_excl_scan(tid < 256 ? (int)tot : 0, s_warp, all);
       if (tid < 256) s_base[tid] = (unsigned int)below + earlier;
       __syncthreads();
-      if (have) {
-        const unsigned int pos = s_base[dg] + s_wcnt[w][dg] + wr;
-        kb[pos] = x;
-        ib[pos] = xid;
+      for (int64_t base = slo; base < shi; base += kThreads) {
+        const int64_t i = base + tid;
+        const bool have = i < shi;
+        const uint64_t x = have ? ka[i] : 0;
+        const int32_t xid = have ? ia[i] : 0;
+        const int dg = have ? (int)((x >> shift) & 0xFF) : 256;
+        uint4 *z = reinterpret_cast<uint4 *>(&s_wcnt[0][0]);
+        for (int e = tid; e < kWarps * 256 / 4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        const int wr = __popc(peers & lanemask_lt());
+        if (dg < 256 && wr == 0) s_wcnt[w][dg] = __popc(peers);
+        __syncthreads();
+        for (int d = tid; d < 256; d += kThreads) {  // exclusive prefix over warps per digit
+          unsigned int acc = 0;
+          for (int ww = 0; ww < kWarps; ++ww) {
+            const unsigned int v = s_wcnt[ww][d];
+            s_wcnt[ww][d] = acc;
+            acc += v;
+          }
+        }
+        __syncthreads();
+        if (have) {
+          const unsigned int pos = s_base[dg] + s_wcnt[w][dg] + wr;
+          kb[pos] = x;
+          ib[pos] = xid;
+        }
+        __syncthreads();
+        if (have && wr == 0) atomicAdd(&s_base[dg], (unsigned)__popc(peers));  // next chunk
+        __syncthreads();
       }
     }
     grid.sync();
@@ -454,11 +465,14 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   int C = std::max(1, std::min(nsm, kMaxCtas));
   if (const char *e = getenv("KVA_EVICT_CTAS")) C = std::max(1, std::min(atoi(e), C));
   const int64_t per = (n + C - 1) / C;
-  const size_t static_smem = 2 * 256 * 4 + 32 * 4 + 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;
-  size_t dyn = (size_t)per * sizeof(uint64_t) + (per <= kCandCap ? 2 * kCandCap * sizeof(uint16_t) : 0);
+  const size_t static_smem = 2 * 256 * 4 + 32 * 4 + 2 * 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;
+  size_t dyn = (size_t)per * sizeof(uint64_t) + (per <= kCandCap ? 2 * (size_t)per * sizeof(uint16_t) : 0);
   int cache = 1;
   if (dyn + static_smem > (size_t)max_smem) { dyn = 0; cache = 0; }
   cudaError_t e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
+  e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   uint8_t *p = reinterpret_cast<uint8_t *>(ws);
   SelWs *sw = reinterpret_cast<SelWs *>(p);

@@ -128,6 +128,9 @@ cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t 
                           cudaStream_t s) {
   const int64_t units = (int64_t)total_new_tok * Hkv;
   if (units <= 0) return cudaSuccess;
+  static bool carve = (cudaFuncSetAttribute(append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared), true);
+  (void)carve;
   append_kernel<<<(unsigned)((units + 7) / 8), 256, 0, s>>>(k_new, v_new, stride_tok, k_pool, v_pool,
                                                              Hkv, d, block_table, max_blocks, reqs,
                                                              q_indptr, num_reqs, total_new_tok);

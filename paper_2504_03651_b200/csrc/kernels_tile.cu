@@ -277,6 +277,9 @@ static cudaError_t launch_tile_t(const AttnParams &p, const void *tmk, const voi
   auto kern = tile_kernel<D, NST>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   kern<<<n, 128, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
                             *reinterpret_cast<const CUtensorMap *>(tmv), items);
   return cudaGetLastError();

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -518,13 +519,26 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     }
   }
   // --- per request ---
+  {
+    size_t nd = 0, nm = 0;
+    for (int i = 0; i < R; ++i)
+      if (dec_class(i)) {
+        const int ns = cdiv(b->ctx_len[i], kSplitKeys) + 1;
+        nd += (size_t)ns * Hkv;
+        nm += (size_t)qlen(b, i) * g * Hkv;
+      }
+    pb.dec.reserve(nd);
+    pb.mrows.reserve(nm);
+    pb.mslots.reserve(nm * 4);
+  }
   int64_t kv_tokens = 0, dec_keys = 0, dec_rows = 0;
   for (int gi = 0; gi < G; ++gi) kv_tokens += (int64_t)b->group_prefix_blocks[gi] * kBlock;
   for (int i = 0; i < R; ++i) {
     const int ql = qlen(b, i), ctx = b->ctx_len[i], gi = grp(i), q0 = b->q_indptr[i];
     const int np = gi >= 0 ? b->group_prefix_blocks[gi] : 0;
     kv_tokens += ctx - np * kBlock;
-    for (int j = 0; j < ql; ++j) pb.stats.flops += (int64_t)(ctx - ql + j + 1) * Hq * 4 * d;
+    // sum_{j<ql} (ctx - ql + j + 1) visible keys per q-head
+    pb.stats.flops += ((int64_t)ql * (ctx - ql + 1) + (int64_t)ql * (ql - 1) / 2) * Hq * 4 * d;
     if (dec_class(i)) {
       const bool cascaded = gi >= 0 && member_idx[i] >= 0;
       const int kb = cascaded ? np * kBlock : 0;
@@ -585,9 +599,12 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   }
   // longest tiles first (LPT); ties keep (kv_head, m-tile, member) order so concurrently
   // running CTAs of a group share its prefix blocks in L2
+  // F(x) = sum_{r<x} floor(r/g) (closed form), so a causal tile's visible keys are exact
+  auto F = [g](int64_t x) { const int64_t q = x / g; return g * q * (q - 1) / 2 + q * (x - q * g); };
   for (const TileItem &t : pb.tile) {
     if (t.flags & kTileCausal) {  // row r sees keys [0, pos0 + r/g]
-      for (int r = t.r0; r < t.r0 + t.n_rows; ++r) pb.stats.tile_flops += (int64_t)(t.pos0 + r / g + 1) * 4 * d;
+      const int64_t keys = (int64_t)t.n_rows * (t.pos0 + 1) + F(t.r0 + t.n_rows) - F(t.r0);
+      pb.stats.tile_flops += keys * 4 * d;
     } else {
       pb.stats.tile_flops += (int64_t)t.n_rows * (t.k1 - t.k0) * 4 * d;
     }
@@ -628,10 +645,13 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
                                             size_t ws_bytes, kva_stream_t stream, kva_plan **out) {
   if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
   *out = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   kva_status st = validate_desc(p, b, 0);
   if (st != KVA_OK) return st;
+  const auto t1 = std::chrono::steady_clock::now();
   PlanBuild pb;
   build_plan(b, pb);
+  const auto t2 = std::chrono::steady_clock::now();
   size_t arrays = 0;
   const size_t need = plan_bytes(pb, b->head_dim, &arrays);
   if (!ws || ws_bytes < need)
@@ -682,20 +702,28 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     const char *e = getenv("KVA_TILE_CTAS");
     const char *o = getenv("KVA_OVERLAP");
     pl->overlap = !(o && std::string(o) == "0");
-    if (e) pl->tile_ctas = atoi(e);
-    else if (pb.dec.empty() || !pl->overlap) pl->tile_ctas = nsm;
-    else {
-      // split the SMs between the tensor-bound tile kernel and the HBM-bound decode kernel:
-      // proportional to their standalone times (measured ~3.9 TFLOP/s per SM and 6.7 TB/s),
-      // skewed 1.75x towards the tile kernel because the decode stream keeps HBM saturated
-      // with fewer SMs than its standalone share (measured optimum on llama7b);
-      // >= 1/4 of the SMs each
-      const double t_tile = (double)pb.tile_flops / (nsm * 3.9e12);
-      const double t_dec = (double)pb.stats.decode_kv_bytes / 6.7e12;
+    // standalone time estimates from measured rates: ~3.9 TFLOP/s per SM for
+    // the tcgen05 tile kernel, 6.7 TB/s for the decode stream
+    const double t_tile = (double)pb.tile_flops / (nsm * 3.9e12);
+    const double t_dec = (double)pb.stats.decode_kv_bytes / 6.7e12;
+    if (e) {
+      pl->tile_ctas = atoi(e);
+    } else if (pb.dec.empty() || pb.tile.empty() || !pl->overlap || t_tile > 1.5 * t_dec) {
+      // tile-dominated batches (e.g. 8k chunks): run the tile kernel on every SM, then decode
+      pl->overlap = false;
+      pl->tile_ctas = nsm;
+    } else {
+      // split the SMs: proportional to the standalone times, skewed 1.75x towards the tile
+      // kernel because the decode stream keeps HBM saturated with fewer SMs than its
+      // standalone share (measured optimum on llama7b: 64 of 148); >= 1/4 of the SMs each
       const double f = 1.75 * t_tile / (t_tile + t_dec);
       pl->tile_ctas = std::max(nsm / 4, std::min(nsm - nsm / 4, (int)(nsm * f + 0.5)));
     }
   }
+  const auto t3 = std::chrono::steady_clock::now();
+  pl->stats.host_validate_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  pl->stats.host_build_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+  pl->stats.host_total_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t3 - t0).count();
   pl->n_dec = (int)pb.dec.size();
   pl->n_tile = (int)pb.tile.size();
   pl->n_mrows = (int)pb.mrows.size();
@@ -764,18 +792,32 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     CUDA_TRY(cudaStreamWaitEvent(pl->aux, pl->ev_fork, 0));
     ts = pl->aux;
   }
-  if (do_tile && pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
-  if (do_tile) {
+  auto run_tile = [&]() -> kva_status {
+    if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
     if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
     else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                   fork ? pl->tile_ctas : 0, ts));
     else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
+    if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], ts));
+    return KVA_OK;
+  };
+  auto run_decode = [&]() -> kva_status {
+    if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
+    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
+    if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
+    return KVA_OK;
+  };
+  // sequential mode: decode first (its CTAs share SMs with a concurrently running eviction
+  // selection on another stream), then the tile kernel on every SM
+  kva_status rs = KVA_OK;
+  if (fork) {
+    if (do_tile && (rs = run_tile()) != KVA_OK) return rs;
+    if (do_dec && (rs = run_decode()) != KVA_OK) return rs;
+  } else {
+    if (do_dec && (rs = run_decode()) != KVA_OK) return rs;
+    if (do_tile && (rs = run_tile()) != KVA_OK) return rs;
   }
-  if (do_tile && pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], ts));
-  if (do_dec && pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
-  if (do_dec) CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
-  if (do_dec && pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
   if (fork) {
     CUDA_TRY(cudaEventRecord(pl->ev_join, pl->aux));
     CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_join, 0));

@@ -49,7 +49,9 @@ class PlanStats(ctypes.Structure):
                 ("n_cascade_items", ctypes.c_int64), ("n_merge_rows", ctypes.c_int64),
                 ("kv_bytes_algorithmic", ctypes.c_int64), ("q_bytes", ctypes.c_int64),
                 ("o_bytes", ctypes.c_int64), ("decode_kv_bytes", ctypes.c_int64),
-                ("flops", ctypes.c_int64), ("tile_flops", ctypes.c_int64)]
+                ("flops", ctypes.c_int64), ("tile_flops", ctypes.c_int64),
+                ("host_validate_ns", ctypes.c_int64), ("host_build_ns", ctypes.c_int64),
+                ("host_total_ns", ctypes.c_int64)]
 
 
 EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_create", "kv_pool_destroy",

@@ -48,7 +48,7 @@ def main():
         batch.table_dev.copy_(pr_dev)
         batch.table_host[...] = pr_host
         K.kv_append(pool, batch, wl.k_new, wl.v_new, ws)
-        K.kv_release_blocks(pool, batch.table_host[mask])
+        K.kv_release_blocks(pool, batch.table_host[mask & (batch.table_host >= 0)])
 
     res["kv_append+release_us"] = timeit(app)
     import time
@@ -108,8 +108,44 @@ def evict_phases():
     print(json.dumps({"evict_phase_ns": (ts - ts[0]).tolist()}))
 
 
+def host_costs(cfg="llama7b"):
+    """Host-side cost of each per-step API call (GPU drained before each call so that no
+    staging wait is included)."""
+    import time
+    dev = torch.device("cuda", 0)
+    wl = W.make_workload(cfg, device=dev)
+    pool = K.Pool(wl.k_pool, wl.v_pool, K.free_bits_tensor(wl.free_bits, dev))
+    batch = K.Batch(wl.batch, dev)
+    pr_dev, pr_host = batch.table_dev.clone(), batch.table_host.copy()
+    mask = pr_host == -1
+    ws = torch.empty(K.kv_append_workspace_size(batch), dtype=torch.uint8, device=dev)
+    wsa = torch.empty(K.hybrid_attention_workspace_size(batch), dtype=torch.uint8, device=dev)
+    out = torch.empty(wl.q.shape, dtype=torch.bfloat16, device=dev)
+    acc = {}
+
+    def t(name, fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        acc.setdefault(name, []).append((time.perf_counter() - t0) * 1e6)
+        return r
+    for _ in range(20):
+        t("table_reset", lambda: (batch.table_dev.copy_(pr_dev), batch.table_host.__setitem__(Ellipsis, pr_host)))
+        t("kv_append", lambda: K.kv_append(pool, batch, wl.k_new, wl.v_new, ws))
+        pl = t("plan", lambda: K.Plan(pool, batch, wsa))
+        t("run", lambda: pl.run(wl.q, out))
+        st = pl.stats()
+        for k in ("host_validate_ns", "host_build_ns", "host_total_ns"):
+            acc.setdefault("c++_" + k, []).append(st[k] / 1e3)
+        t("release", lambda: K.kv_release_blocks(pool, batch.table_host[mask & (batch.table_host >= 0)]))
+        t("plan_close", lambda: pl.close())
+    print(json.dumps({k: round(statistics.median(v), 1) for k, v in acc.items()}))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "evict":
         evict_phases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "host":
+        host_costs(sys.argv[2] if len(sys.argv) > 2 else "llama7b")
     else:
         main()

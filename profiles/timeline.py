@@ -1,0 +1,44 @@
+"""GPU kernel timeline of a few bench steps via torch.profiler (CUPTI activity records):
+start/end of every kernel per stream, relative to the first kernel of the last step.
+
+python profiles/timeline.py [config] [--out file.json]
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "llama7b"
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    sys.argv = [sys.argv[0], "--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+                "--no-e2e", "--profile"]
+    import bench
+    from torch.profiler import ProfilerActivity, profile
+    args = bench.parse()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        bench.run_ours(args, 0, 1, 0)
+    evs = []
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0:
+            evs.append((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)))
+    evs.sort()
+    mine = [x for x in evs if any(k in x[2] for k in ("kva::", "decode_kernel", "tile_", "merge_kernel",
+                                                      "append_kernel", "alloc_write", "evict_", "release_ids"))]
+    # last step = kernels after the last append_kernel's preceding evict_keys
+    starts = [i for i, x in enumerate(mine) if "evict_keys" in x[2]] or [0]
+    last = mine[starts[-1]:]
+    t0 = last[0][0]
+    rows = [{"kernel": n.split("(")[0][-40:], "stream": s, "start_us": round(a - t0, 1),
+             "end_us": round(b - t0, 1), "dur_us": round(b - a, 1)} for a, b, n, s in last]
+    for r in rows:
+        print(f"{r['kernel']:42s} stream={r['stream']:<4} {r['start_us']:9.1f} -> {r['end_us']:9.1f}  ({r['dur_us']:.1f} us)")
+    if out:
+        json.dump(rows, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
