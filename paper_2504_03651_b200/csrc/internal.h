@@ -68,6 +68,7 @@ struct AttnParams {
   float *part_lse;        // [slots]
   const int32_t *row_list;
   unsigned long long *dbg;  // optional timestamps (diagnostics; KVA_DEBUG_TS), nullable
+  int32_t debug_flags;      // diagnostics only (KVA_DEBUG_FLAGS): 1 = tile softmax skipped
 };
 
 // launchers (kernels_*.cu)

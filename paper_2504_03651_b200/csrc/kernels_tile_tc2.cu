@@ -231,6 +231,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         __syncwarp();
       }
     }
+    // drain: observe the final release of every ring slot (keeps each mbarrier phase waited)
+    for (int k = max(0, KT - 2); k < KT; ++k) {
+      mbar_wait(&bar_ke[k & 1], (k >> 1) & 1);
+      mbar_wait(&bar_ve[k & 1], (k >> 1) & 1);
+    }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer (whole warp loops, lane 0 issues) ------
     const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
@@ -347,8 +352,14 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       for (int j = 0; j < G.nt_t[t]; ++j, ++Gs) {
         if (warp == 4 || warp == 8) ts(1 + t);
         mbar_wait(&bar_s[t], Gs & 1);  // QK_t(j) done; so is PV_t(j-1) (issued earlier)
+        if (j >= 1) mbar_wait(&bar_o[t], (Gs - 1) & 1);  // observe that completion (no-op wait)
         if (warp == 4 || warp == 8) ts(1 + t);
         fence_after();
+        if (p.debug_flags & 1) {  // diagnostics: measure the MMA/TMA pipeline without softmax
+          fence_before();
+          mbar_arrive(&bar_p[t]);
+          continue;
+        }
         // valid keys of this row in this tile: [key0, min(k1, pos + 1)) -> columns [0, lim)
         const int key0 = it.k0 + j * N;
         const int lim = max(0, min(min(k1, pos == INT32_MAX ? k1 : pos + 1) - key0, N));

@@ -782,6 +782,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.out_f32 = out_dtype == KVA_OUT_F32;
   p.lse = lse;
   p.dbg = nullptr;
+  p.debug_flags = 0;
+  if (const char *e = getenv("KVA_DEBUG_FLAGS")) p.debug_flags = atoi(e);
   if (const char *e = getenv("KVA_DEBUG_TS")) p.dbg = reinterpret_cast<unsigned long long *>(strtoull(e, nullptr, 0));
   const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
   const bool do_dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
