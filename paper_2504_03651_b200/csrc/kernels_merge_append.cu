@@ -96,29 +96,62 @@ cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const 
   return cudaGetLastError();
 }
 
+// One CTA moves kUnitsPerCta (token, kv-head) rows of K and V: phase 1 resolves each unit's
+// destination slot (binary search of q_indptr + one table read) into shared memory, phase 2
+// copies with every thread issuing all its 16-byte loads before its stores (ILP).
+constexpr int kUnitsPerCta = 32;
 __global__ void __launch_bounds__(256) append_kernel(
     const uint16_t *__restrict__ k_new, const uint16_t *__restrict__ v_new, int64_t stride_tok,
     uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
     const int32_t *__restrict__ block_table, int32_t max_blocks, const AppendReq *__restrict__ reqs,
     const int32_t *__restrict__ q_indptr, int32_t num_reqs, int32_t total_new_tok) {
-  const int64_t unit = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // (token, head)
-  const int lane = threadIdx.x & 31;
-  if (unit >= (int64_t)total_new_tok * Hkv) return;
-  const int row = (int)(unit / Hkv), h = (int)(unit % Hkv);
-  int lo = 0, hi = num_reqs - 1;  // request of this token: last i with q_indptr[i] <= row
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(q_indptr + mid) <= row) lo = mid; else hi = mid - 1;
+  __shared__ int64_t s_src[kUnitsPerCta], s_dst[kUnitsPerCta];
+  const int64_t n_units = (int64_t)total_new_tok * Hkv;
+  const int64_t u0 = (int64_t)blockIdx.x * kUnitsPerCta;
+  if (threadIdx.x < kUnitsPerCta) {
+    const int64_t unit = u0 + threadIdx.x;
+    int64_t src = -1, dst = -1;
+    if (unit < n_units) {
+      const int row = (int)(unit / Hkv), h = (int)(unit % Hkv);
+      int lo = 0, hi = num_reqs - 1;  // request of this token: last i with q_indptr[i] <= row
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(q_indptr + mid) <= row) lo = mid; else hi = mid - 1;
+      }
+      const AppendReq rq = reqs[lo];
+      const int t = rq.pos0 + (row - rq.q_row0);
+      const int32_t id = block_table[(int64_t)rq.table_row * max_blocks + t / kBlock];
+      src = (int64_t)row * stride_tok + (int64_t)h * d;
+      dst = (((int64_t)id * Hkv + h) * kBlock + t % kBlock) * d;
+    }
+    s_src[threadIdx.x] = src;
+    s_dst[threadIdx.x] = dst;
   }
-  const AppendReq rq = reqs[lo];
-  const int t = rq.pos0 + (row - rq.q_row0);
-  const int32_t id = block_table[(int64_t)rq.table_row * max_blocks + t / kBlock];
-  const int chunks = d / 8;  // 16-B chunks per row
-  const int tensor = lane >> 4, c = lane & 15;
-  if (c >= chunks) return;
-  const uint16_t *src = (tensor ? v_new : k_new) + (int64_t)row * stride_tok + (int64_t)h * d + c * 8;
-  uint16_t *dst = (tensor ? v_pool : k_pool) + (((int64_t)id * Hkv + h) * kBlock + t % kBlock) * d + c * 8;
-  *reinterpret_cast<uint4 *>(dst) = __ldg(reinterpret_cast<const uint4 *>(src));
+  __syncthreads();
+  const int cpr = d / 8;                    // 16-byte chunks per row
+  const int per_unit = 2 * cpr;             // K and V
+  const int total = kUnitsPerCta * per_unit;
+  constexpr int kMaxIt = kUnitsPerCta * 2 * 16 / 256;  // 4 for d = 128
+  uint4 v[kMaxIt];
+  int64_t dsto[kMaxIt];
+  bool isv[kMaxIt];
+#pragma unroll
+  for (int k = 0; k < kMaxIt; ++k) {
+    const int c = threadIdx.x + k * 256;
+    dsto[k] = -1;
+    if (c < total) {
+      const int u = c / per_unit, r = c % per_unit;
+      const int tensor = r / cpr, part = r % cpr;
+      if (s_src[u] >= 0) {
+        isv[k] = tensor;
+        v[k] = __ldg(reinterpret_cast<const uint4 *>((tensor ? v_new : k_new) + s_src[u] + part * 8));
+        dsto[k] = s_dst[u] + part * 8;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxIt; ++k)
+    if (dsto[k] >= 0) *reinterpret_cast<uint4 *>((isv[k] ? v_pool : k_pool) + dsto[k]) = v[k];
 }
 
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
@@ -131,9 +164,9 @@ cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t 
   static bool carve = (cudaFuncSetAttribute(append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared), true);
   (void)carve;
-  append_kernel<<<(unsigned)((units + 7) / 8), 256, 0, s>>>(k_new, v_new, stride_tok, k_pool, v_pool,
-                                                             Hkv, d, block_table, max_blocks, reqs,
-                                                             q_indptr, num_reqs, total_new_tok);
+  append_kernel<<<(unsigned)((units + kUnitsPerCta - 1) / kUnitsPerCta), 256, 0, s>>>(
+      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, reqs, q_indptr,
+      num_reqs, total_new_tok);
   return cudaGetLastError();
 }
 
