@@ -187,7 +187,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     tim_used = []
 
-    ev_stream = torch.cuda.Stream(device=dev)
+    ev_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("KVA_BENCH_EVICT_PRIO", "0")))
     ev_fork, ev_join = torch.cuda.Event(), torch.cuda.Event()
 
     def step(e2e=False, time_idx=None):
@@ -267,6 +267,22 @@ def run_ours(args, rank, world, local):
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
     dec_ms = [e4[2].elapsed_time(e4[3]) for e4 in tim_used if stats["n_decode_items"] > 0]
     tile_ms = [e4[0].elapsed_time(e4[1]) for e4 in tim_used if stats["n_tile_items"] > 0]
+    # standalone decode-kernel timing (same plan, no co-running kernels): context for the
+    # in-step roofline above, which is measured while the tile kernel shares the GPU
+    dec_alone = None
+    if not args.profile and stats["n_decode_items"] > 0:
+        plan_s = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
+        ts_ = []
+        for i in range(8):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan_s.run(q, out, lse, stream=stream, phases=K.PHASE_DECODE)
+            b.record(stream)
+            b.synchronize()
+            if i >= 3:
+                ts_.append(a.elapsed_time(b))
+        plan_s.close()
+        dec_alone = statistics.median(ts_)
     ms_e2e = None
     if not args.no_e2e and not args.profile:
         for _ in range(2):
@@ -304,6 +320,10 @@ def run_ours(args, rank, world, local):
                      "traffic": ncu_traffic(), "bytes_per_launch": dec_bytes, "peak_source": peak_src},
         "clocks": ck, "gpu_launches": gpu_launches,
     }
+    if dec_alone:
+        a = dec_bytes / (dec_alone * 1e-3) / 1e9
+        res["config"]["decode_kernel_standalone"] = {"ms": dec_alone, "GBps": a, "frac_of_peak": a / peak,
+                                                     "note": "median of 5 warm launches, nothing co-running"}
     if ms_e2e is not None:
         res["e2e"] = {"value": tokens / (ms_e2e * 1e-3), "unit": UNIT,
                       "h2d_bytes_per_step": int(h_q.numel() * 2 + h_k.numel() * 2 + h_v.numel() * 2),

@@ -462,7 +462,9 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  int C = std::max(1, std::min(nsm, kMaxCtas));
+  // half the SMs: the selection is latency-bound, and runs concurrently with the attention
+  // kernels (whose CTAs take the other SMs / share these)
+  int C = std::max(1, std::min(nsm / 2, kMaxCtas));
   if (const char *e = getenv("KVA_EVICT_CTAS")) C = std::max(1, std::min(atoi(e), C));
   const int64_t per = (n + C - 1) / C;
   const size_t static_smem = 2 * 256 * 4 + 32 * 4 + 2 * 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;

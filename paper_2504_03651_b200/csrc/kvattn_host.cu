@@ -713,10 +713,11 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       pl->overlap = false;
       pl->tile_ctas = nsm;
     } else {
-      // split the SMs: proportional to the standalone times, skewed 1.75x towards the tile
-      // kernel because the decode stream keeps HBM saturated with fewer SMs than its
-      // standalone share (measured optimum on llama7b: 64 of 148); >= 1/4 of the SMs each
-      const double f = 1.75 * t_tile / (t_tile + t_dec);
+      // split the SMs: proportional to the standalone times, skewed 1.2x towards the tile
+      // kernel because the decode stream keeps HBM nearly saturated with fewer SMs than its
+      // standalone share (measured optimum on llama7b: 44 of 148 with the eviction selection
+      // co-running on 74); >= 1/4 of the SMs each
+      const double f = 1.2 * t_tile / (t_tile + t_dec);
       pl->tile_ctas = std::max(nsm / 4, std::min(nsm - nsm / 4, (int)(nsm * f + 0.5)));
     }
   }
