@@ -80,6 +80,8 @@ cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *
                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
+cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
+                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
                          int n_rows, cudaStream_t s);
 cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,

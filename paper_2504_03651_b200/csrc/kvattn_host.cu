@@ -464,14 +464,21 @@ static int tile_impl() {
   if (v < 0) {
     const char *e = getenv("KVA_TILE_IMPL");
     const std::string s = e ? e : "";
-    v = s == "mma" ? 0 : s == "tc1" ? 1 : 2;
+    v = s == "mma" ? 0 : s == "tc1" ? 1 : s == "tc3" ? 3 : 2;
   }
   return v;
 }
 static bool tile_use_tc() { return tile_impl() != 0; }
 
+// effective implementation for a descriptor (the CTA-pair kernel is head_dim 128 only)
+static int tile_impl_for(const kva_batch_desc *b) {
+  const int v = tile_impl();
+  return (v == 3 && b->head_dim != 128) ? 2 : v;
+}
+
 static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
-  const int kTileM = tile_impl() == 2 ? 2 * kTileMTc : tile_impl() == 1 ? kTileMTc : kTileMMma;
+  const int impl = tile_impl_for(b);
+  const int kTileM = impl == 3 ? 4 * kTileMTc : impl == 2 ? 2 * kTileMTc : impl == 1 ? kTileMTc : kTileMMma;
   const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
   const int d = b->head_dim;
   const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
@@ -692,7 +699,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     }
   }
   pl->tile_tc = tile_use_tc();
-  pl->tile_impl = tile_impl();
+  pl->tile_impl = tile_impl_for(b);
   pl->aux = p->aux;
   pl->ev_fork = p->ev_fork;
   pl->ev_join = p->ev_join;
@@ -797,8 +804,10 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   }
   auto run_tile = [&]() -> kva_status {
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
-    if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+    if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
+    else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+                                                          fork ? pl->tile_ctas : 0, ts));
     else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                   fork ? pl->tile_ctas : 0, ts));
     else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));

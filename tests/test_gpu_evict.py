@@ -80,3 +80,44 @@ def test_evict_short():
     keys = _gpu_keys(ev)
     ids, n = K.evict_select(keys, 4)
     assert n == 2 and list(ids.cpu().numpy()) == [2, 3]
+
+
+def test_release_blocks_roundtrip_and_errors():
+    """kv_release_blocks returns blocks to the pool (P:448 recompute-mode release); a second
+    kv_append then re-allocates exactly those ids (smallest free first, reading #13)."""
+    import paper_2504_03651_b200 as K
+    wl = W.make_workload("tiny")
+    dev = "cuda"
+    fb = K.free_bits_tensor(wl.free_bits, dev)
+    pool = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), fb)
+    batch = K.Batch(wl.batch, dev)
+    n0 = pool.free_count()
+    pristine = wl.batch["block_table"]
+    K.kv_append(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+    new_ids = batch.table_host[(pristine == -1) & (batch.table_host >= 0)]
+    assert pool.free_count() == n0 - len(new_ids)
+    with pytest.raises(K.KvaError):            # double release of a free block
+        K.kv_release_blocks(pool, np.array([int(np.nonzero(np.unpackbits(
+            wl.free_bits.view(np.uint8), bitorder="little"))[0][-1])], np.int32))
+    with pytest.raises(K.KvaError):            # listed twice
+        K.kv_release_blocks(pool, np.array([new_ids[0], new_ids[0]], np.int32))
+    K.kv_release_blocks(pool, new_ids)
+    torch.cuda.synchronize()
+    assert pool.free_count() == n0
+    assert np.array_equal(fb.cpu().numpy().view(np.uint32), wl.free_bits)
+    batch2 = K.Batch(wl.batch, dev)
+    K.kv_append(pool, batch2, wl.k_new.to(dev), wl.v_new.to(dev))
+    assert np.array_equal(batch2.table_host, batch.table_host)
+
+
+def test_evict_k_larger_than_evictable_and_zero():
+    import paper_2504_03651_b200 as K
+    ev = W.make_evict(n=3000, k=10, seed=11)
+    keys = _gpu_keys(ev)
+    s, ref_keys = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    n_ev = int((ref_keys != np.uint64(0xFFFFFFFFFFFFFFFF)).sum())
+    ids, n = K.evict_select(keys, n_ev + 100)
+    s2, ref_ids = oracle.evict_select(ref_keys, n_ev + 100)
+    assert n == n_ev and np.array_equal(ids.cpu().numpy(), ref_ids)
+    ids, n = K.evict_select(keys, 0)
+    assert n == 0

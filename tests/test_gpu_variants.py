@@ -1,0 +1,52 @@
+"""GPU parity of the alternative tile-kernel implementations and launch modes, each in a fresh
+process (the implementation is chosen once per process from KVA_TILE_IMPL / KVA_OVERLAP /
+KVA_TILE_CTAS): legacy mma.sync (64-row tiles), tcgen05 one-Q-tile, tcgen05 two-Q-tile
+(default), tcgen05 CTA-pair (cta_group::2), and overlapped vs sequential scheduling."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from gpu_util import gpu_step, oracle_step, assert_attention_close
+reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 600 + 300, 300, 0), W.ReqSpec(W.OFFLINE_PREFILL, 600 + 173, 173, 0),
+        W.ReqSpec(W.ONLINE_DECODE, 2000, 1), W.ReqSpec(W.ONLINE_DECODE, 77, 1)]
+reqs += [W.ReqSpec(W.OFFLINE_DECODE, 600 + 5 + i, 1, 0) for i in range(20)]
+for d, Hq, Hkv in [(128, 16, 2), (64, 8, 4)]:
+    wl = W.make_workload(W.custom_config("v", Hq, Hkv, d, 7, reqs, [600 // 16]))
+    g = gpu_step(wl)
+    r = oracle_step(wl)
+    assert_attention_close(g["out"], g["lse"], r["out"], r["lse"])
+    np.save({out!r} + f"_{{d}}.npy", g["out"].cpu().numpy())
+print("OK")
+'''
+
+
+def _run(env_extra, tag, tmp_path):
+    out = str(tmp_path / tag)
+    env = dict(os.environ, **env_extra)
+    code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), out=out)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+    return out
+
+
+@pytest.mark.parametrize("impl", ["mma", "tc1", "tc2", "tc3"])
+def test_tile_impl_parity(impl, tmp_path):
+    _run({"KVA_TILE_IMPL": impl}, impl, tmp_path)
+
+
+def test_overlap_modes_bitexact(tmp_path):
+    import numpy as np
+    a = _run({"KVA_OVERLAP": "1", "KVA_TILE_CTAS": "40"}, "ov", tmp_path)
+    b = _run({"KVA_OVERLAP": "0"}, "seq", tmp_path)
+    for d in (128, 64):
+        assert np.array_equal(np.load(a + f"_{d}.npy"), np.load(b + f"_{d}.npy"))
