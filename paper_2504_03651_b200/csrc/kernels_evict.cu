@@ -5,15 +5,16 @@
 // entry, and then the last access time"; priorities P:331-334.  Keys are
 // order-preserving u64 codes (readings #18-#20); equal keys are broken by block id.
 //
-// evict_select is one cooperative persistent kernel (grid = #SMs, 1024 threads, keys of a
+// evict_select is one cooperative persistent kernel (grid = #SMs / 2, 512 threads, keys of a
 // CTA's slice cached in shared memory):
-//   1. MSD radix select, 8 rounds of 8-bit digits -> the k-th smallest evictable key T and
-//      count(< T);
-//   2. order-preserving compaction of {key < T} u {first k - count(<T) blocks with key == T}
-//      (block-id order) into a (key, id) array;
+//   1. MSD radix select over 8-bit digits (only bytes that vary among the evictable keys, and
+//      only until the chosen bin is taken whole) -> threshold prefix P at bit level lvl and
+//      count(key >> lvl < P);
+//   2. order-preserving compaction of {key >> lvl < P} u {first quota blocks with
+//      key >> lvl == P} (block-id order) into a (key, id) array;
 //   3. stable LSD radix sort of that array by key over only the bytes that vary (stability
-//      keeps block-id order among equal keys).
-// Grid-wide steps are separated by cooperative-groups grid barriers.
+//      keeps block-id order among equal keys), one grid barrier per pass.
+// Grid-wide steps are separated by cooperative-groups grid barriers (select rounds + 2 + passes).
 #include <cooperative_groups.h>
 
 #include <cstdlib>
@@ -60,17 +61,20 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 namespace {
 constexpr int kThreads = 512;  // leaves registers/smem for a co-resident decode CTA
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCtas = 1024;
-constexpr int kCandCap = 65535;  // candidate lists use u16 slice indices
+constexpr int kMaxCtas = kThreads;  // the compaction scans one value per CTA block-wide
 
 struct SelWs {  // global scratch (zeroed by the host before launch)
   unsigned long long t[32];      // phase timestamps of CTA 0 (%globaltimer, ns; diagnostics)
   unsigned long long hist[8][256];
-  unsigned long long cnt_eq[kMaxCtas], cnt_sel[kMaxCtas];
-  unsigned long long key_or, key_and_inv;  // OR of selected keys, OR of their complements
+  unsigned long long cnt[kMaxCtas];           // per CTA: (#eq << 32) | #less
+  unsigned long long ev_or, ev_and_inv;       // OR of evictable keys, OR of their complements
+  unsigned long long key_or, key_and_inv;     // same over the selected keys
 };
 struct SortWs {
-  unsigned int hist[kMaxCtas][256];  // per-CTA digit counts of one LSD pass
+  // digit counts of one LSD pass, [digit][sorter CTA] (row stride Sp = S rounded up to 4),
+  // triple-buffered: pass p reads buffer p%3, its scatter accumulates pass p+1's counts into
+  // buffer (p+1)%3, and buffer (p+2)%3 (last read in pass p-1) is zeroed
+  unsigned int hist[3][256 * kMaxCtas];
 };
 }  // namespace
 
@@ -125,26 +129,6 @@ __device__ __forceinline__ void hist_add_fast(unsigned int *hist, int dg) {
   }
 }
 
-// Warp-aggregated shared-memory histogram increment (digit 256 = skip): one atomic per
-// distinct digit per warp instead of one per lane (keys are highly skewed: e.g. the priority
-// code byte is identical for most blocks).
-__device__ __forceinline__ void warp_hist_add(unsigned int *hist, int dg) {
-  const unsigned peers = __match_any_sync(0xffffffffu, dg);
-  if (dg < 256 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
-}
-
-// Sum over threads of a u64 (result valid in all threads).
-__device__ __forceinline__ unsigned long long block_sum(unsigned long long a,
-                                                        unsigned long long *s_red) {
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = a;
-  __syncthreads();
-  unsigned long long t = 0;
-  for (int w = 0; w < kWarps; ++w) t += s_red[w];
-  __syncthreads();
-  return t;
-}
-
 __global__ void __launch_bounds__(kThreads, 2)
     evict_select_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t k,
                         int32_t *__restrict__ out_ids, int64_t *__restrict__ d_count,
@@ -156,235 +140,357 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (tp < 32) sw->t[tp] = t;
+      if (tp < 32) sw->t[tp] = t;  // (a sorter when c == 0)
     }
     ++tp;
   };
   stamp();
-  extern __shared__ uint64_t s_keys[];
+  extern __shared__ __align__(16) uint64_t s_keys[];
   __shared__ unsigned int s_hist[256];
   __shared__ unsigned int s_base[256];
+  __shared__ unsigned int s_part[256];
   __shared__ int s_warp[32];
   __shared__ long long s_warp64[32];
-  __shared__ unsigned long long s_red[32];
   __shared__ unsigned long long s_sel[4];
   __shared__ __align__(16) unsigned int s_wcnt[kWarps][256];  // 16 KB
-  const int C = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
-  const int64_t per = (n + C - 1) / C;
+  const int C = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // even: 16-B aligned slices
   const int64_t lo = std::min<int64_t>(n, c * per), hi = std::min<int64_t>(n, lo + per);
   const int64_t cnt = hi - lo;
-  // candidate index lists (u16, double-buffered) after the cached keys: every select round
-  // scans only the keys still matching the chosen digit prefix
-  const bool use_cand = cache_keys && per <= kCandCap;
-  uint16_t *cand[2] = {reinterpret_cast<uint16_t *>(s_keys + (cache_keys ? per : 0)), nullptr};
-  cand[1] = cand[0] + per;
-  __shared__ int s_ncand[2];
-  if (tid == 0) s_ncand[0] = s_ncand[1] = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < cnt; base += kThreads) {
-    const int64_t i = base + tid;
-    uint64_t x = kInf;
-    if (i < cnt) {
-      x = keys[lo + i];
-      if (cache_keys) s_keys[i] = x;
+  auto key_at = [&](int64_t i) -> uint64_t { return cache_keys ? s_keys[i] : keys[lo + i]; };
+
+  // ---------------- 0. slice -> shared memory (16-B vector loads, 8 in flight) ----------------
+  if (cache_keys && (reinterpret_cast<uintptr_t>(keys) & 15)) {
+    for (int64_t i = tid; i < cnt; i += kThreads) s_keys[i] = keys[lo + i];
+  } else if (cache_keys) {
+    const int64_t nv = cnt >> 1;
+    const uint4 *src = reinterpret_cast<const uint4 *>(keys + lo);
+    uint4 *dst = reinterpret_cast<uint4 *>(s_keys);
+    for (int64_t b = 0; b < nv; b += 8 * kThreads) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = b + u * kThreads + tid;
+        if (i < nv) v[u] = __ldg(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = b + u * kThreads + tid;
+        if (i < nv) dst[i] = v[u];
+      }
     }
-    if (use_cand) {  // initial candidates: every evictable key (warp-aggregated append)
-      const bool keep = x != kInf;
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      int off = 0;
-      if ((tid & 31) == 0 && bal) off = atomicAdd(&s_ncand[0], __popc(bal));
-      off = __shfl_sync(0xffffffffu, off, 0);
-      if (keep) cand[0][off + __popc(bal & lanemask_lt())] = (uint16_t)i;
-    }
+    if ((cnt & 1) && tid == 0) s_keys[cnt - 1] = keys[lo + cnt - 1];
+  }
+  {
+    uint4 *z = reinterpret_cast<uint4 *>(&s_wcnt[0][0]);
+    for (int e = tid; e < kWarps * 256 / 4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  auto key_at = [&](int64_t i) -> uint64_t { return cache_keys ? s_keys[i] : keys[lo + i]; };
-  stamp();  // 1: keys cached
 
-  // ---------------- 1. radix select: T = k-th smallest evictable key ----------------
-  // 8 rounds of 8-bit digits: warp-aggregated shared-memory histograms (keys are heavily
-  // skewed, e.g. the priority byte), one global atomic per (CTA, bin), grid barrier, then
-  // every CTA scans the 256 global bins block-wide and the owner of rank kr publishes.
-  uint64_t prefix = 0;
+  // Digit histogram of one select round over the whole cached slice: keys matching the
+  // current prefix (bits above `shift + 8`) count their digit at `shift`.  Each thread keeps a
+  // run-length counter (keys are heavily skewed: long runs of one digit) flushed into its
+  // warp's private histogram; the warp histograms are summed into the global one.
+  auto round_hist = [&](int r, int shift, uint64_t prefix, bool all) -> void {
+    int run_d = -1;
+    unsigned run_n = 0;
+    for (int64_t base = 0; base < cnt; base += 4 * kThreads) {
+      uint64_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = base + u * kThreads + tid;
+        x[u] = i < cnt ? key_at(i) : kInf;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool match = x[u] != kInf && (all || (x[u] >> (shift + 8)) == prefix);
+        const int d = match ? (int)((x[u] >> shift) & 0xFF) : -1;
+        if (d != run_d) {
+          if (run_n) atomicAdd(&s_wcnt[w][run_d], run_n);
+          run_d = d;
+          run_n = 0;
+        }
+        run_n += d >= 0;
+      }
+    }
+    if (run_n) atomicAdd(&s_wcnt[w][run_d], run_n);
+    __syncthreads();
+    for (int d = tid; d < 256; d += kThreads) {
+      unsigned t = 0;
+#pragma unroll
+      for (int ww = 0; ww < kWarps; ++ww) {
+        t += s_wcnt[ww][d];
+        s_wcnt[ww][d] = 0;
+      }
+      if (t) atomicAdd(&sw->hist[r][d], (unsigned long long)t);
+    }
+  };
+
+  // round 0 + OR / AND of the evictable keys (the bytes that vary decide which rounds run)
+  {
+    uint64_t lor = 0, linv = 0;
+    for (int64_t i = tid; i < cnt; i += kThreads) {
+      const uint64_t x = key_at(i);
+      if (x != kInf) {
+        lor |= x;
+        linv |= ~x;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lor |= __shfl_xor_sync(0xffffffffu, lor, o);
+      linv |= __shfl_xor_sync(0xffffffffu, linv, o);
+    }
+    if (lane == 0 && (lor | linv)) {
+      atomicOr(&sw->ev_or, (unsigned long long)lor);
+      atomicOr(&sw->ev_and_inv, (unsigned long long)linv);
+    }
+  }
+  round_hist(0, 56, 0, true);
+  stamp();  // 1: keys cached, round-0 histogram built
+
+  // ---------------- 1. radix select: threshold prefix P at bit level lvl ----------------
+  // MSD rounds of 8-bit digits; rounds whose byte is constant over the evictable keys are
+  // skipped without a barrier; the select stops as soon as the chosen bin is taken whole or
+  // no lower bit varies.  Selected = {key >> lvl < P} + the first need_eq (block-id order)
+  // of {key >> lvl == P}.
+  uint64_t prefix = 0, ev_or = 0, vary_ev = 0;
   unsigned long long kr = (unsigned long long)k, less = 0, total_ev = 0;
   bool take_all = false;
-  int cb = 0;  // current candidate buffer
+  int lvl = 56;
   for (int r = 0; r < 8; ++r) {
     const int shift = 56 - 8 * r;
-    for (int i = tid; i < 256; i += kThreads) s_hist[i] = 0;
-    __syncthreads();
-    const int64_t scan_n = use_cand ? s_ncand[cb] : cnt;
-    for (int64_t base = 0; base < scan_n; base += kThreads) {  // warp-uniform trip count
-      const int64_t i = base + tid;
-      int dg = 256;  // sentinel: not a candidate
-      if (i < scan_n) {
-        const uint64_t x = key_at(use_cand ? (int64_t)cand[cb][i] : i);
-        if (x != kInf && (r == 0 || (x >> (shift + 8)) == prefix)) dg = (int)((x >> shift) & 0xFF);
+    lvl = shift;
+    if (r > 0) {
+      if (((vary_ev >> shift) & 0xFF) == 0) {  // constant byte: every candidate has it
+        prefix = (prefix << 8) | ((ev_or >> shift) & 0xFF);
+        continue;
       }
-      hist_add_fast(s_hist, dg);
+      round_hist(r, shift, prefix, false);
     }
-    __syncthreads();
-    for (int i = tid; i < 256; i += kThreads)
-      if (s_hist[i]) atomicAdd(&sw->hist[r][i], (unsigned long long)s_hist[i]);
     stamp();
     grid.sync();
     stamp();
-    {
-      const int h = tid < 256 ? (int)sw->hist[r][tid] : 0;
-      int tot;
-      const int excl = block_excl_scan(h, s_warp, tot);
-      if (r == 0) {
-        total_ev = (unsigned long long)tot;
-        take_all = total_ev <= kr;
-      }
-      if (!take_all && tid < 256 && (unsigned long long)excl < kr && kr <= (unsigned long long)(excl + h)) {
-        s_sel[0] = (prefix << 8) | (uint64_t)tid;
-        s_sel[1] = less + excl;
-        s_sel[2] = kr - excl;
-      }
-      __syncthreads();
-      if (!take_all) {
-        prefix = s_sel[0];
-        less = s_sel[1];
-        kr = s_sel[2];
-      }
-      __syncthreads();
+    if (r == 0) {
+      ev_or = sw->ev_or;
+      vary_ev = ev_or & sw->ev_and_inv;
     }
+    const int h = tid < 256 ? (int)sw->hist[r][tid] : 0;
+    int tot;
+    const int excl = block_excl_scan(h, s_warp, tot);
+    if (r == 0) {
+      total_ev = (unsigned long long)tot;
+      take_all = total_ev <= kr;
+    }
+    if (!take_all && tid < 256 && (unsigned long long)excl < kr && kr <= (unsigned long long)(excl + h)) {
+      s_sel[0] = (prefix << 8) | (uint64_t)tid;
+      s_sel[1] = less + excl;
+      s_sel[2] = kr - excl;
+      s_sel[3] = (unsigned long long)h;
+    }
+    __syncthreads();
     if (take_all) break;
-    if (use_cand && r < 7) {  // keep candidates whose top 8(r+1) bits equal the prefix
-      const int nb = cb ^ 1;
-      if (tid == 0) s_ncand[nb] = 0;
-      __syncthreads();
-      for (int64_t base = 0; base < scan_n; base += kThreads) {
-        const int64_t i = base + tid;
-        bool keep = false;
-        uint16_t idx = 0;
-        if (i < scan_n) {
-          idx = cand[cb][i];
-          keep = (key_at(idx) >> shift) == prefix;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        int off = 0;
-        if ((tid & 31) == 0 && bal) off = atomicAdd(&s_ncand[nb], __popc(bal));
-        off = __shfl_sync(0xffffffffu, off, 0);
-        if (keep) cand[nb][off + __popc(bal & lanemask_lt())] = idx;
-      }
-      __syncthreads();
-      cb = nb;
-    }
+    prefix = s_sel[0];
+    less = s_sel[1];
+    kr = s_sel[2];
+    const bool whole_bin = kr == s_sel[3];
+    __syncthreads();
+    if (whole_bin || (vary_ev & ((1ull << shift) - 1)) == 0) break;
   }
-  const uint64_t T = take_all ? kInf : prefix;           // every evictable key < kInf
-  const unsigned long long need_eq = take_all ? 0 : kr;  // keys == T to take, id order
+  if (take_all) {
+    prefix = kInf;
+    lvl = 0;
+  }
+  const uint64_t P = prefix;
+  const unsigned long long need_eq = take_all ? 0 : kr;  // keys with key >> lvl == P to take
   const unsigned long long n_sel = take_all ? total_ev : (unsigned long long)k;
 
   stamp();
   // ---------------- 2. order-preserving compaction (block-id order) ----------------
-  // Blocked arrangement: thread t owns the contiguous slice range [t*ept, (t+1)*ept), so one
-  // block scan of packed (eq << 16 | less) counts ranks every element in id order; equal
-  // keys are taken in id order until the grid-wide quota need_eq is met.
-  const int ept = (int)((cnt + kThreads - 1) / kThreads);
-  const int64_t e0 = std::min<int64_t>(cnt, (int64_t)tid * ept), e1 = std::min<int64_t>(cnt, e0 + ept);
-  int my_less = 0, my_eq = 0;
-  for (int64_t i = e0; i < e1; ++i) {
-    const uint64_t x = key_at(i);
-    if (x == kInf) continue;
-    my_less += x < T;
-    my_eq += x == T;
+  // Warp-blocked arrangement: warp w owns the contiguous slice range [w*wlen, (w+1)*wlen),
+  // walked 32 keys at a time, so ballots rank every key in id order.  After one grid barrier
+  // every CTA scans all CTAs' (less, eq) counts itself: keys with key >> lvl == P are taken in
+  // id order until the grid-wide quota need_eq is met.
+  const int64_t wlen = ((cnt + kThreads - 1) / kThreads) * 32;
+  const int64_t w0 = std::min<int64_t>(cnt, (int64_t)w * wlen), w1 = std::min<int64_t>(cnt, w0 + wlen);
+  const unsigned lt = lanemask_lt();
+  auto classify = [&](int64_t i, bool &is_less, bool &is_eq, uint64_t &x) {
+    x = i < w1 ? key_at(i) : kInf;
+    const uint64_t xh = x >> lvl;
+    is_less = x != kInf && xh < P;
+    is_eq = x != kInf && xh == P;
+  };
+  unsigned my_less = 0, my_eq = 0;
+  for (int64_t i0 = w0; i0 < w1; i0 += 32) {
+    bool l, e;
+    uint64_t x;
+    classify(i0 + lane, l, e, x);
+    my_less += __popc(__ballot_sync(0xffffffffu, l));
+    my_eq += __popc(__ballot_sync(0xffffffffu, e));
   }
   long long tot_pk;
-  const long long pk = block_excl_scan<long long>(((long long)my_eq << 32) | my_less, s_warp64, tot_pk);
-  const long long tot_less = tot_pk & 0xFFFFFFFFll, tot_eq = tot_pk >> 32;
-  if (tid == 0) sw->cnt_eq[c] = tot_eq;
+  const long long pk = block_excl_scan<long long>(lane == 0 ? ((long long)my_eq << 32) | my_less : 0ll,
+                                                  s_warp64, tot_pk);
+  const long long wbase = __shfl_sync(0xffffffffu, pk, 0);  // this warp's (eq, less) base
+  if (tid == 0) sw->cnt[c] = (unsigned long long)tot_pk;
+  stamp();
   grid.sync();
-  unsigned long long a = 0;
-  for (int j = tid; j < c; j += kThreads) a += sw->cnt_eq[j];
-  const unsigned long long eq_before = block_sum(a, s_red);
-  const unsigned long long quota = eq_before >= need_eq ? 0ull : need_eq - eq_before;  // eq keys this CTA may take
-  const unsigned long long eq_take = std::min<unsigned long long>((unsigned long long)tot_eq, quota);
-  if (tid == 0) sw->cnt_sel[c] = (unsigned long long)tot_less + eq_take;
-  grid.sync();
-  a = 0;
-  for (int j = tid; j < c; j += kThreads) a += sw->cnt_sel[j];
-  const unsigned long long sel_before = block_sum(a, s_red);
+  stamp();
+  {
+    const unsigned long long v = tid < C ? sw->cnt[tid] : 0ull;
+    const long long eq_j = (long long)(v >> 32), less_j = (long long)(v & 0xFFFFFFFFull);
+    long long t1, t2;
+    const long long eq_before = block_excl_scan<long long>(eq_j, s_warp64, t1);
+    const long long quota = (long long)need_eq > eq_before ? (long long)need_eq - eq_before : 0;
+    const long long sel_j = less_j + std::min(eq_j, quota);
+    const long long sel_before = block_excl_scan<long long>(sel_j, s_warp64, t2);
+    if (tid == c) {
+      s_sel[0] = (unsigned long long)sel_before;
+      s_sel[1] = (unsigned long long)quota;
+    }
+    __syncthreads();
+  }
+  const unsigned long long sel_before = s_sel[0], quota = s_sel[1];
   uint64_t loc_or = 0, loc_and_inv = 0;
   {
-    unsigned long long less_r = (unsigned long long)(pk & 0xFFFFFFFFll), eq_r = (unsigned long long)(pk >> 32);
-    for (int64_t i = e0; i < e1; ++i) {
-      const uint64_t x = key_at(i);
-      if (x == kInf) continue;
-      const bool is_eq = x == T;
-      if (x < T || (is_eq && eq_r < quota)) {
-        const unsigned long long pos = sel_before + less_r + std::min(eq_r, quota);
+    unsigned long long less_r = (unsigned long long)(wbase & 0xFFFFFFFFll), eq_r = (unsigned long long)(wbase >> 32);
+    for (int64_t i0 = w0; i0 < w1; i0 += 32) {
+      bool l, e;
+      uint64_t x;
+      classify(i0 + lane, l, e, x);
+      const unsigned bl = __ballot_sync(0xffffffffu, l), be = __ballot_sync(0xffffffffu, e);
+      const unsigned long long lr = less_r + __popc(bl & lt), er = eq_r + __popc(be & lt);
+      if (l || (e && er < quota)) {
+        const unsigned long long pos = sel_before + lr + std::min(er, quota);
         pk0[pos] = x;
-        pi0[pos] = (int32_t)(lo + i);
+        pi0[pos] = (int32_t)(lo + i0 + lane);
         loc_or |= x;
         loc_and_inv |= ~x;
       }
-      less_r += x < T;
-      eq_r += is_eq;
+      less_r += __popc(bl);
+      eq_r += __popc(be);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
     loc_or |= __shfl_xor_sync(0xffffffffu, loc_or, o);
     loc_and_inv |= __shfl_xor_sync(0xffffffffu, loc_and_inv, o);
   }
-  if ((tid & 31) == 0 && (loc_or | loc_and_inv)) {
+  if (lane == 0 && (loc_or | loc_and_inv)) {
     atomicOr(&sw->key_or, (unsigned long long)loc_or);
     atomicOr(&sw->key_and_inv, (unsigned long long)loc_and_inv);
   }
   if (c == 0 && tid == 0) *d_count = (int64_t)n_sel;
+  stamp();
   grid.sync();
   const uint64_t vary = sw->key_or & sw->key_and_inv;  // bits that differ among selected keys
 
   stamp();
   // ---------------- 3. stable LSD radix sort of (key, id) by key ----------------
-  // S = min(#CTAs, ceil(m / kThreads)) sorter CTAs own contiguous ranges (one element per
-  // thread for k = 64k).  Per 8-bit pass over the varying bytes only: (A) each sorter's digit
-  // histogram -> global; grid barrier; (B) digit bases = digits below (all sorters) + same
-  // digit in earlier sorters, then a stable scatter chunk by chunk (warp match_any ranks +
-  // exclusive per-warp digit prefix); grid barrier ends the pass.
+  // Only the bytes that vary among the selected keys are passes.  S sorter CTAs own contiguous
+  // ranges of the array (<= one element per thread at k = 64k), cached in shared memory.
+  // Per pass: digit bases = digits below (all sorters) + same digit in earlier sorters, read
+  // from the [digit][sorter] count table; stable scatter chunk by chunk (warp match_any ranks
+  // + exclusive per-warp digit prefix); the scatter also counts the NEXT pass's digits per
+  // destination sorter, so each pass costs one grid barrier.  The last pass scatters ids
+  // straight into out_ids.
+  const int64_t m = (int64_t)n_sel;
+  if (m == 0) return;
+  int shifts[8], npass = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+    if ((vary >> (8 * b)) & 0xFF) shifts[npass++] = 8 * b;
+  if (npass == 0) {  // all selected keys equal: block-id order is the answer
+    for (int64_t i = (int64_t)c * kThreads + tid; i < m; i += (int64_t)C * kThreads) out_ids[i] = pi0[i];
+    return;
+  }
+  const int S = (int)std::min<int64_t>(C, (m + kThreads - 1) / kThreads);
+  const int Sp = (S + 3) & ~3;
+  const int sper = (int)((m + S - 1) / S);
+  const bool sorter = c < S;
+  const int slo = sorter ? (int)std::min<int64_t>(m, (int64_t)c * sper) : 0;
+  const int ns = sorter ? (int)std::min<int64_t>(m - slo, sper) : 0;
+  const bool scache = cache_keys && (int64_t)ns * 12 <= per * 8;
+  uint64_t *ck = s_keys;
+  int32_t *ci = reinterpret_cast<int32_t *>(s_keys + ns);
+  unsigned int *B[3] = {so->hist[0], so->hist[1], so->hist[2]};
+  const int tbl = 256 * Sp;
+  if (npass > 1)
+    for (int e = c * kThreads + tid; e < tbl; e += C * kThreads) B[1][e] = 0u;
   uint64_t *ka = pk0, *kb = pk1;
   int32_t *ia = pi0, *ib = pi1;
-  const int64_t m = (int64_t)n_sel;
-  const int S = (int)std::min<int64_t>(C, std::max<int64_t>(1, (m + kThreads - 1) / kThreads));
-  const int64_t sper = (m + S - 1) / S;
-  const bool sorter = c < S;
-  const int64_t slo = sorter ? std::min<int64_t>(m, c * sper) : 0;
-  const int64_t shi = sorter ? std::min<int64_t>(m, slo + sper) : 0;
-  const int w = tid >> 5;
-  for (int pass = 0; pass < 8; ++pass) {
-    const int shift = 8 * pass;
-    if (((vary >> shift) & 0xFF) == 0) continue;
-    if (sorter) {
-      for (int i = tid; i < 256; i += kThreads) s_hist[i] = 0;
-      __syncthreads();
-      for (int64_t base = slo; base < shi; base += kThreads) {
-        const int64_t i = base + tid;
-        hist_add_fast(s_hist, i < shi ? (int)((ka[i] >> shift) & 0xFF) : 256);
-      }
-      __syncthreads();
-      for (int i = tid; i < 256; i += kThreads) so->hist[c][i] = s_hist[i];
-    }
-    grid.sync();
-    if (sorter) {
-      unsigned int tot = 0, earlier = 0;
-      if (tid < 256) {
-#pragma unroll 16
-        for (int j = 0; j < S; ++j) {
-          const unsigned int h = so->hist[j][tid];
-          tot += h;
-          earlier += j < c ? h : 0u;
+  if (sorter) {  // pass-0 digit counts of this sorter's range
+    for (int i = tid; i < 256; i += kThreads) s_hist[i] = 0;
+    __syncthreads();
+    for (int base = 0; base < ns; base += kThreads) {
+      const int i = base + tid;
+      uint64_t x = 0;
+      if (i < ns) {
+        x = ka[slo + i];
+        if (scache) {
+          ck[i] = x;
+          ci[i] = ia[slo + i];
         }
       }
-      int all;
-      const int below = block_excl_scan(tid < 256 ? (int)tot : 0, s_warp, all);
-      if (tid < 256) s_base[tid] = (unsigned int)below + earlier;
-      __syncthreads();
-      for (int64_t base = slo; base < shi; base += kThreads) {
-        const int64_t i = base + tid;
-        const bool have = i < shi;
-        const uint64_t x = have ? ka[i] : 0;
-        const int32_t xid = have ? ia[i] : 0;
+      hist_add_fast(s_hist, i < ns ? (int)((x >> shifts[0]) & 0xFF) : 256);
+    }
+    __syncthreads();
+    for (int d = tid; d < 256; d += kThreads) B[0][d * Sp + c] = s_hist[d];
+  }
+  stamp();
+  grid.sync();
+  for (int pass = 0; pass < npass; ++pass) {
+    const int shift = shifts[pass];
+    const bool last = pass + 1 == npass;
+    const int nshift = last ? 0 : shifts[pass + 1];
+    unsigned int *Bc = B[pass % 3], *Bn = B[(pass + 1) % 3];
+    if (pass + 2 < npass) {
+      unsigned int *Bz = B[(pass + 2) % 3];
+      for (int e = c * kThreads + tid; e < tbl; e += C * kThreads) Bz[e] = 0u;
+    }
+    if (sorter) {
+      if (pass > 0 && scache) {
+        for (int i = tid; i < ns; i += kThreads) {
+          ck[i] = ka[slo + i];
+          ci[i] = ia[slo + i];
+        }
+      }
+      {  // digit bases: two threads per digit, each summing half of the sorter columns
+        const int d = tid & 255, half = tid >> 8;
+        const int S4 = Sp >> 2, h4 = (S4 + 1) >> 1;
+        const int j4a = half * h4, j4b = min(S4, j4a + h4);
+        const uint4 *row = reinterpret_cast<const uint4 *>(Bc + d * Sp);
+        unsigned int tot = 0, earlier = 0;
+#pragma unroll 8
+        for (int j4 = j4a; j4 < j4b; ++j4) {
+          const uint4 v = row[j4];
+          const unsigned int e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = 4 * j4 + q;
+            const unsigned int h = j < S ? e[q] : 0u;
+            tot += h;
+            earlier += j < c ? h : 0u;
+          }
+        }
+        if (half == 1) {
+          s_part[d] = tot;
+          s_base[d] = earlier;
+        }
+        __syncthreads();
+        if (half == 0) {
+          tot += s_part[d];
+          earlier += s_base[d];
+        }
+        int all;
+        const int below = block_excl_scan(half == 0 ? (int)tot : 0, s_warp, all);
+        if (half == 0) s_base[d] = (unsigned int)below + earlier;
+        __syncthreads();
+      }
+      stamp();
+      for (int base = 0; base < ns; base += kThreads) {
+        const int i = base + tid;
+        const bool have = i < ns;
+        const uint64_t x = have ? (scache ? ck[i] : ka[slo + i]) : 0;
+        const int32_t xid = have ? (scache ? ci[i] : ia[slo + i]) : 0;
         const int dg = have ? (int)((x >> shift) & 0xFF) : 256;
         uint4 *z = reinterpret_cast<uint4 *>(&s_wcnt[0][0]);
         for (int e = tid; e < kWarps * 256 / 4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
@@ -395,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();
         for (int d = tid; d < 256; d += kThreads) {  // exclusive prefix over warps per digit
           unsigned int acc = 0;
+#pragma unroll
           for (int ww = 0; ww < kWarps; ++ww) {
             const unsigned int v = s_wcnt[ww][d];
             s_wcnt[ww][d] = acc;
@@ -402,22 +509,35 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         __syncthreads();
+        const unsigned int pos = have ? s_base[dg] + s_wcnt[w][dg] + wr : 0u;
         if (have) {
-          const unsigned int pos = s_base[dg] + s_wcnt[w][dg] + wr;
-          kb[pos] = x;
-          ib[pos] = xid;
+          if (last) {
+            out_ids[pos] = xid;
+          } else {
+            kb[pos] = x;
+            ib[pos] = xid;
+          }
+        }
+        if (!last) {  // next pass's digit counts per destination sorter (warp-aggregated)
+          const int nd = (int)((x >> nshift) & 0xFF);
+          const int key2 = have ? (int)(pos / (unsigned)sper) * 256 + nd : -1;
+          const unsigned p2 = __match_any_sync(0xffffffffu, key2);
+          if (have && __popc(p2 & lanemask_lt()) == 0)
+            atomicAdd(&Bn[nd * Sp + key2 / 256], (unsigned)__popc(p2));
         }
         __syncthreads();
         if (have && wr == 0) atomicAdd(&s_base[dg], (unsigned)__popc(peers));  // next chunk
         __syncthreads();
       }
     }
-    grid.sync();
     stamp();
-    uint64_t *tk = ka; ka = kb; kb = tk;
-    int32_t *ti = ia; ia = ib; ib = ti;
+    if (!last) {
+      grid.sync();
+      stamp();
+      uint64_t *tk = ka; ka = kb; kb = tk;
+      int32_t *ti = ia; ia = ib; ib = ti;
+    }
   }
-  for (int64_t i = (int64_t)c * kThreads + tid; i < m; i += (int64_t)C * kThreads) out_ids[i] = ia[i];
 }
 
 __global__ void free_ids_kernel(uint32_t *free_bits, const int32_t *ids, const int64_t *d_count,
@@ -465,12 +585,13 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   // half the SMs: the selection is latency-bound, and runs concurrently with the attention
   // kernels (whose CTAs take the other SMs / share these)
   int C = std::max(1, std::min(nsm / 2, kMaxCtas));
-  if (const char *e = getenv("KVA_EVICT_CTAS")) C = std::max(1, std::min(atoi(e), C));
-  const int64_t per = (n + C - 1) / C;
-  const size_t static_smem = 2 * 256 * 4 + 32 * 4 + 2 * 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;
-  size_t dyn = (size_t)per * sizeof(uint64_t) + (per <= kCandCap ? 2 * (size_t)per * sizeof(uint16_t) : 0);
+  if (const char *e = getenv("KVA_EVICT_CTAS")) C = std::max(1, std::min(atoi(e), std::min(nsm, kMaxCtas)));
+  const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // as in the kernel
+  const size_t static_smem = 3 * 256 * 4 + 32 * 4 + 2 * 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;
+  size_t dyn = (size_t)per * sizeof(uint64_t);
   int cache = 1;
   if (dyn + static_smem > (size_t)max_smem) { dyn = 0; cache = 0; }
+  if (const char *e = getenv("KVA_EVICT_NOCACHE")) if (atoi(e)) { dyn = 0; cache = 0; }
   cudaError_t e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   // full shared-memory carveout so CTAs of concurrently running kernels can share an SM

@@ -183,6 +183,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int g = p.g;
+  int dbg_n = 0;
+  auto ts = [&](int role) {  // diagnostics: CTA 0 role timelines into p.dbg (KVA_DEBUG_TS)
+    if (p.dbg && blockIdx.x == 0 && lane == 0 && dbg_n < 512) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      p.dbg[role * 512 + dbg_n] = tt;
+    }
+    ++dbg_n;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -228,10 +237,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
         int rows[NBLK];
 #pragma unroll
         for (int q = 0; q < NBLK; ++q) rows[q] = (__shfl_sync(0xffffffffu, id, q) * p.Hkv + it.kv_head) * kBlock;
-        if (KT >= STAGES) {
-          mbar_wait(&bar_ke[s], (use - 1) & 1);
-          mbar_wait(&bar_ve[s], (use - 1) & 1);
-        }
+        ts(3);
+        if (KT >= STAGES) mbar_wait(&bar_ke[s], (use - 1) & 1);  // K slot freed after the QKs
+        ts(3);
         if (lane == 0) {
           // K: keys [64 rank, 64 rank + 64) of the tile = blocks 4 rank .. 4 rank + 3, all channels
           const int kq0 = 4 * (int)rank;
@@ -243,6 +251,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
                 tma_load_2d(sK + s * KHALF + h * (64 * 128) + q * 2048, &tmk, &bar_kf[s], h * 64, rows[kq0 + q]);
+        }
+        __syncwarp();
+        if (KT >= STAGES) mbar_wait(&bar_ve[s], (use - 1) & 1);  // V slot freed after the PVs
+        ts(3);
+        if (lane == 0) {
           // V: all keys of the tile, channels [64 rank, 64 rank + 64)
           mbar_arrive_expect_tx(&bar_vf[s], nb * 2048);
 #pragma unroll
@@ -313,7 +326,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
       };
       auto pv = [&](int t, int j) {
         const int KT = KT0 + j, s = KT % STAGES;
+        ts(0);
         mbar_wait(&bar_p[t], Gp[t] & 1);
+        ts(0);
         fence_after();
         if (lane == 0) {
 #pragma unroll
@@ -336,14 +351,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
         if (vready >= j) return;
         fwd_v(j);  // own half (leader) -> arrival on own bar_vr
         const int KT = KT0 + j, s = KT % STAGES;
+        ts(0);
         mbar_wait(&bar_vr[s], (KT / STAGES) & 1);
+        ts(0);
         vready = j;
       };
       for (int j = 0; j <= G.nt; ++j) {
+        ts(0);
         if (j < G.nt) {
           fwd_k(j);
+          ts(0);
           const int KT = KT0 + j;
           mbar_wait(&bar_kr[KT % STAGES], (KT / STAGES) & 1);
+          ts(0);
           fence_after();
         }
         if (j < nt0) qk(0, j);
@@ -400,8 +420,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
       const float sl2 = p.scale_log2;
       float m_used = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < G.nt_t[t]; ++j, ++Gs) {
+        if (warp == 4 || warp == 8) ts(1 + t);
         mbar_wait(&bar_s[t], Gs & 1);
         if (j >= 1) mbar_wait(&bar_o[t], (Gs - 1) & 1);
+        if (warp == 4 || warp == 8) ts(1 + t);
         fence_after();
         const int key0 = it.k0 + j * N;
         const int lim = max(0, min(min(k1, pos == INT32_MAX ? k1 : pos + 1) - key0, N));
@@ -476,6 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc3::THREADS, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) arrive_remote(bar_p_l);
+        if (warp == 4 || warp == 8) ts(1 + t);
       }
       // ------------------------------- epilogue -------------------------------
       mbar_wait(&bar_o[t], (Gs - 1) & 1);

@@ -21,7 +21,7 @@ torch.cuda.synchronize()
 b = buf.cpu().numpy().reshape(4, 512)
 t0 = b[b > 0].min()
 res = {}
-for r, name in enumerate(["mma", "sm0", "sm1"]):
+for r, name in enumerate(["mma", "sm0", "sm1", "prod"]):
     v = b[r][b[r] > 0] - t0
     res[name] = v[:120].tolist()
 print(json.dumps(res))

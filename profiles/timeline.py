@@ -27,7 +27,8 @@ def main():
             evs.append((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)))
     evs.sort()
     mine = [x for x in evs if any(k in x[2] for k in ("kva::", "decode_kernel", "tile_", "merge_kernel",
-                                                      "append_kernel", "alloc_write", "evict_", "release_ids"))]
+                                                      "append_kernel", "alloc_write", "evict_", "release_ids",
+                                                      "Memcpy", "Memset", "elementwise", "copy"))]
     # last step = kernels after the last append_kernel's preceding evict_keys
     starts = [i for i, x in enumerate(mine) if "evict_keys" in x[2]] or [0]
     last = mine[starts[-1]:]
