@@ -182,7 +182,7 @@ kva_status kva_plan_launch_count(const kva_plan *plan, int32_t phases, int32_t *
 kva_status kva_plan_destroy(kva_plan *plan);
 /* Plan statistics: counts of work items per kernel and algorithmic bytes/flops. */
 typedef struct {
-  int64_t n_decode_items, n_tile_items, n_cascade_items, n_merge_rows;
+  int64_t n_decode_items, n_tile_items, n_cascade_items, n_merge_rows;  /* decode/merge: per kv head */
   int64_t kv_bytes_algorithmic;     /* distinct KV bytes (prefix once per group/kv-head) */
   int64_t q_bytes, o_bytes;         /* bf16 Q read + O written */
   int64_t decode_kv_bytes;          /* KV bytes read by the split-KV (decode) kernel */

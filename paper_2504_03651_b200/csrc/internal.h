@@ -16,14 +16,12 @@ constexpr int kTileMTc = 128;     // rows per tcgen05 tile CTA (UMMA M = TMEM la
 constexpr int kTileN = 64;        // keys per tile-kernel pipeline stage (4 blocks)
 
 // One decode warp: <= 16 rows (tok*g + hh) of one request and kv-head over keys [k0, k1).
-struct DecodeItem {
-  int32_t q_row0;    // first q row of the request
-  int32_t n_tok;     // q_len (rows = n_tok * g <= 16)
-  int32_t kv_head;   // local kv head
-  int32_t table_row; // row of the device block table
-  int32_t k0, k1;    // key range (k0 multiple of 16)
-  int32_t pos0;      // absolute position of token 0 (ctx - q_len)
-  int32_t slot;      // partial slot of row 0 (rows consecutive); -1 = write output directly
+// One decode-class request: keys [kb, ctx) are cut into nsplit splits of
+// kSplitKeys; the decode kernel runs every (split, kv head) as one warp.  Partial slot of
+// (head h, split s, row r) = slot + (h * nsplit + s) * rows + r, rows = n_tok * g; slot < 0:
+// single split, the output is written directly.
+struct DecodeReq {
+  int32_t q_row0, n_tok, table_row, kb, ctx, slot, nsplit, pad;
 };
 
 // One tile CTA: <= kTileM rows of one row space (r = tok*g + hh) over keys [k0, k1).
@@ -40,8 +38,25 @@ struct TileItem {
   int32_t flags;
 };
 
-struct MergeRow {
-  int32_t q_row, q_head, s_begin, s_count;
+// One request whose partials are merged (a6): each of its rows r < rows is merged for every
+// kv head h (q head = h * g + r % g) from the cascade-prefix slot casc_slot + h*casc_hstride + r
+// (casc_slot < 0: none) and the split slots split_slot + (h * nsplit + s) * rows + r.
+struct MergeReq {
+  int32_t q_row0, rows, casc_slot, casc_hstride, split_slot, nsplit, pad0, pad1;
+};
+
+// Request list + exclusive prefix of work units (splits or rows) per request, handed to the
+// decode / merge kernels as a __grid_constant__ kernel parameter when n <= kInlineReqs (no
+// host->device copy between kv_append and the attention launches), else uploaded with the
+// plan (ptr / pre_ptr set).
+constexpr int kInlineReqs = 400;
+template <class R>
+struct ReqList {
+  int32_t n;
+  const R *ptr;
+  const int32_t *pre_ptr;
+  int32_t pre[kInlineReqs + 1];
+  R req[kInlineReqs];
 };
 
 // Per-request append info (kv_append).
@@ -73,7 +88,7 @@ struct AttnParams {
 
 // launchers (kernels_*.cu)
 cudaError_t launch_decode(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                          const DecodeItem *items, int n_items, cudaStream_t s);
+                          const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s);
 cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                         const TileItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
@@ -82,8 +97,7 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void 
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
-cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
-                         int n_rows, cudaStream_t s);
+cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);
 cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,
                                const int32_t *ids, int32_t n, cudaStream_t s);
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,

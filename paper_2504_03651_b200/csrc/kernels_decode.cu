@@ -28,8 +28,8 @@ using namespace dev;
 template <int D, int NST, int PF>
 __global__ void __launch_bounds__(128, 2)
     decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
-                  const __grid_constant__ CUtensorMap tmv, const DecodeItem *__restrict__ items,
-                  int n_items) {
+                  const __grid_constant__ CUtensorMap tmv, const __grid_constant__ ReqList<DecodeReq> L,
+                  int n_units) {
   constexpr int HALVES = D / 64;
   constexpr int KBYTES = 16 * D * 2;  // K (or V) of one block for one head
   constexpr int STAGE = 2 * KBYTES;
@@ -39,9 +39,29 @@ __global__ void __launch_bounds__(128, 2)
   __shared__ uint64_t bars[4][NST];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item_idx = blockIdx.x * 4 + warp;
-  if (item_idx >= n_items) return;  // no CTA-wide barrier below
-  const DecodeItem it = items[item_idx];
+  const int unit = blockIdx.x * 4 + warp;  // (item, kv head), head fastest
+  if (unit >= n_units) return;             // no CTA-wide barrier below
+  const int item = unit / p.Hkv, kv_head = unit - item * p.Hkv;  // item = (request, split)
+  const DecodeReq *reqs = L.ptr ? L.ptr : L.req;
+  const int32_t *pre = L.ptr ? L.pre_ptr : L.pre;
+  int lo = 0, hi = L.n - 1;  // request: pre[lo] <= item < pre[lo + 1] (warp-uniform search)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  const DecodeReq rq = reqs[lo];
+  const int split = item - pre[lo];
+  struct {
+    int q_row0, n_tok, table_row, k0, k1, pos0;
+  } it;
+  it.q_row0 = rq.q_row0;
+  it.n_tok = rq.n_tok;
+  it.table_row = rq.table_row;
+  it.k0 = rq.kb + split * kSplitKeys;
+  it.k1 = min(rq.ctx, it.k0 + kSplitKeys);
+  it.pos0 = rq.ctx - rq.n_tok;
+  const int slot = rq.slot < 0 ? -1 : rq.slot + (kv_head * rq.nsplit + split) * (rq.n_tok * p.g);
   uint8_t *sbase = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
   uint8_t *ws = sbase + warp * NST * STAGE;
   uint64_t *bar = bars[warp];
@@ -58,7 +78,7 @@ __global__ void __launch_bounds__(128, 2)
   const int nblk = (it.k1 + kBlock - 1) / kBlock - b0;  // <= 32
   const int32_t *trow = p.block_table + (int64_t)it.table_row * p.max_blocks + b0;
   const int my_id = lane < nblk ? __ldg(trow + lane) : 0;
-  const int row_base = it.kv_head * kBlock;  // + id*Hkv*16
+  const int row_base = kv_head * kBlock;  // + id*Hkv*16
 
   auto issue = [&](int st, int id) {  // lane 0 only
     uint64_t *b = &bar[st];
@@ -101,11 +121,11 @@ __global__ void __launch_bounds__(128, 2)
     if (r_lo < n_rows)
       qlo = reinterpret_cast<const uint32_t *>(
           p.q + (int64_t)(it.q_row0 + r_lo / g) * p.q_stride_tok +
-          (int64_t)(it.kv_head * g + r_lo % g) * p.q_stride_head);
+          (int64_t)(kv_head * g + r_lo % g) * p.q_stride_head);
     if (r_hi < n_rows)
       qhi = reinterpret_cast<const uint32_t *>(
           p.q + (int64_t)(it.q_row0 + r_hi / g) * p.q_stride_tok +
-          (int64_t)(it.kv_head * g + r_hi % g) * p.q_stride_head);
+          (int64_t)(kv_head * g + r_hi % g) * p.q_stride_head);
 #pragma unroll
     for (int kk = 0; kk < KT; ++kk) {
       const int c = kk * 16 + cq;
@@ -239,8 +259,8 @@ __global__ void __launch_bounds__(128, 2)
     const float l = half ? l_hi : l_lo, m = half ? m_hi : m_lo;
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const float lse = l > 0.f ? (m + __log2f(l)) * kLn2 : -CUDART_INF_F;
-    const int tok = r / g, hq = it.kv_head * g + r % g;
-    if (it.slot < 0) {
+    const int tok = r / g, hq = kv_head * g + r % g;
+    if (slot < 0) {
       const int64_t qrow = it.q_row0 + tok;
       if (p.out_f32) {
         float *dst = reinterpret_cast<float *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head;
@@ -258,19 +278,19 @@ __global__ void __launch_bounds__(128, 2)
       }
       if (p.lse && (lane & 3) == 0) p.lse[qrow * p.Hq + hq] = lse;
     } else {
-      float *dst = p.part_o + (int64_t)(it.slot + r) * D;
+      float *dst = p.part_o + (int64_t)(slot + r) * D;
 #pragma unroll
       for (int n = 0; n < NT; ++n)
         *reinterpret_cast<float2 *>(dst + n * 8 + cq) =
             make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
-      if ((lane & 3) == 0) p.part_lse[it.slot + r] = lse;
+      if ((lane & 3) == 0) p.part_lse[slot + r] = lse;
     }
   }
 }
 
 template <int D, int NST, int PF>
 static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const void *tmv,
-                                   const DecodeItem *items, int n, cudaStream_t s) {
+                                   const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;  // + alignment slack
   auto kern = decode_kernel<D, NST, PF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -280,24 +300,24 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
   if (e != cudaSuccess) return e;
   const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
   const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
-  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, items, n);
+  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, L, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
-                          const DecodeItem *items, int n, cudaStream_t s) {
+                          const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   static const int pf = [] {
     const char *e = getenv("KVA_DECODE_PF");
     return e ? atoi(e) : 0;  // L2 prefetch measured counter-productive
   }();
   if (p.d == 128) {
-    if (pf <= 0) return launch_decode_t<128, 3, 0>(p, tmk, tmv, items, n, s);
-    if (pf <= 4) return launch_decode_t<128, 3, 4>(p, tmk, tmv, items, n, s);
-    if (pf <= 6) return launch_decode_t<128, 3, 6>(p, tmk, tmv, items, n, s);
-    return launch_decode_t<128, 3, 10>(p, tmk, tmv, items, n, s);
+    if (pf <= 0) return launch_decode_t<128, 3, 0>(p, tmk, tmv, L, n, s);
+    if (pf <= 4) return launch_decode_t<128, 3, 4>(p, tmk, tmv, L, n, s);
+    if (pf <= 6) return launch_decode_t<128, 3, 6>(p, tmk, tmv, L, n, s);
+    return launch_decode_t<128, 3, 10>(p, tmk, tmv, L, n, s);
   }
-  return launch_decode_t<64, 4, 6>(p, tmk, tmv, items, n, s);
+  return launch_decode_t<64, 4, 6>(p, tmk, tmv, L, n, s);
 }
 
 }  // namespace kva

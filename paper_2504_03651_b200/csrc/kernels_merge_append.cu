@@ -11,26 +11,42 @@ using namespace dev;
 // ---------------------------------------------------------------------------------------
 // a6: for each output (row, q-head) with partials {(O_j, lse_j)}:
 //   lse = ln sum_j e^{lse_j},  O = sum_j e^{lse_j - lse} O_j.
-// One warp per output row; each lane owns D/32 contiguous channels (16-B / 8-B vectors).
+// One warp per (request row, kv head); each lane owns D/32 contiguous channels (16-B / 8-B
+// vectors).  Partials in order: the cascade prefix slot (if any), then the key splits.
 // ---------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
-                                                    const MergeRow *__restrict__ rows,
-                                                    const int32_t *__restrict__ slots, int n_rows) {
+                                                    const __grid_constant__ ReqList<MergeReq> RL,
+                                                    int n_units) {
   constexpr int V = D / 32;  // 4 (d=128) or 2 (d=64)
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= n_rows) return;
-  const MergeRow mr = rows[w];
+  if (w >= n_units) return;
+  const int m = w / p.Hkv, h = w - m * p.Hkv;  // m = (request, row)
+  const MergeReq *reqs = RL.ptr ? RL.ptr : RL.req;
+  const int32_t *pre = RL.ptr ? RL.pre_ptr : RL.pre;
+  int lo = 0, hi = RL.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= m) lo = mid;
+    else hi = mid - 1;
+  }
+  const MergeReq mq = reqs[lo];
+  const int r = m - pre[lo];
+  const bool casc = mq.casc_slot >= 0;
+  const int n = (int)casc + mq.nsplit;
+  const int casc_sl = mq.casc_slot + h * mq.casc_hstride + r;
+  const int split0 = mq.split_slot + h * mq.nsplit * mq.rows + r;
+  auto slot_of = [&](int i) { return casc && i == 0 ? casc_sl : split0 + (i - (int)casc) * mq.rows; };
   float L = -CUDART_INF_F;
-  for (int i = lane; i < mr.s_count; i += 32) L = fmaxf(L, p.part_lse[slots[mr.s_begin + i]]);
+  for (int i = lane; i < n; i += 32) L = fmaxf(L, p.part_lse[slot_of(i)]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xffffffffu, L, o));
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   float sum = 0.f;
-  for (int i = 0; i < mr.s_count; ++i) {
-    const int sl = __ldg(slots + mr.s_begin + i);
+  for (int i = 0; i < n; ++i) {
+    const int sl = slot_of(i);
     const float lj = __ldg(p.part_lse + sl);
     const float wgt = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
     sum += wgt;
@@ -44,7 +60,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
     }
   }
   const float inv = 1.f / sum;
-  const int64_t off = (int64_t)mr.q_row * p.o_stride_tok + (int64_t)mr.q_head * p.o_stride_head + lane * V;
+  const int q_head = h * p.g + r % p.g, q_row = mq.q_row0 + r / p.g;
+  const int64_t off = (int64_t)q_row * p.o_stride_tok + (int64_t)q_head * p.o_stride_head + lane * V;
   if (p.out_f32) {
     float *dst = reinterpret_cast<float *>(p.out) + off;
     if constexpr (V == 4)
@@ -59,17 +76,16 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
     else
       *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
   }
-  if (p.lse && lane == 0) p.lse[(int64_t)mr.q_row * p.Hq + mr.q_head] = L + __logf(sum);
+  if (p.lse && lane == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
 }
 
-cudaError_t launch_merge(const AttnParams &p, const MergeRow *rows, const int32_t *slots,
-                         int n_rows, cudaStream_t s) {
-  if (n_rows <= 0) return cudaSuccess;
-  const int grid = (n_rows + 7) / 8;
+cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n_units, cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  const int grid = (n_units + 7) / 8;
   if (p.d == 128)
-    merge_kernel<128><<<grid, 256, 0, s>>>(p, rows, slots, n_rows);
+    merge_kernel<128><<<grid, 256, 0, s>>>(p, RL, n_units);
   else
-    merge_kernel<64><<<grid, 256, 0, s>>>(p, rows, slots, n_rows);
+    merge_kernel<64><<<grid, 256, 0, s>>>(p, RL, n_units);
   return cudaGetLastError();
 }
 

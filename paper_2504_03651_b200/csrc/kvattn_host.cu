@@ -429,11 +429,18 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
 struct kva_plan {
   AttnParams p;
   CUtensorMap tmk, tmv;
-  const DecodeItem *d_dec = nullptr;
+  ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
+  ReqList<MergeReq> mrg;                   // merged requests (idem)
   const TileItem *d_tile = nullptr;
-  const MergeRow *d_mrows = nullptr;
-  const int32_t *d_mslots = nullptr;
-  int n_dec = 0, n_tile = 0, n_mrows = 0;
+  int n_dec = 0, n_tile = 0, n_mrows = 0;  // work units: decode (split, head), tiles, merge (row, head)
+  // the plan arrays are uploaded on the pool's side stream (ordered after `stream`'s prior work
+  // by ev_up0); a kernel that reads uploaded arrays on `stream` first waits ev_up1
+  cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
+  bool uploaded = false;
+  ~kva_plan() {
+    if (ev_up0) cudaEventDestroy(ev_up0);
+    if (ev_up1) cudaEventDestroy(ev_up1);
+  }
   int device = 0;
   bool tile_tc = true;
   int tile_impl = 2;
@@ -446,10 +453,12 @@ struct kva_plan {
 };
 
 struct PlanBuild {
-  std::vector<DecodeItem> dec;
+  std::vector<DecodeReq> dec;
+  std::vector<int32_t> dec_pre{0};   // exclusive prefix of splits per decode request
   std::vector<TileItem> tile;
-  std::vector<MergeRow> mrows;
-  std::vector<int32_t> mslots, row_list;
+  std::vector<MergeReq> mrg;
+  std::vector<int32_t> mrg_pre{0};   // exclusive prefix of rows per merged request
+  std::vector<int32_t> row_list;
   int64_t n_slots = 0;
   int64_t tile_flops = 0;
   kva_plan_stats stats{};
@@ -530,13 +539,13 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     size_t nd = 0, nm = 0;
     for (int i = 0; i < R; ++i)
       if (dec_class(i)) {
-        const int ns = cdiv(b->ctx_len[i], kSplitKeys) + 1;
-        nd += (size_t)ns * Hkv;
-        nm += (size_t)qlen(b, i) * g * Hkv;
+        ++nd;
+        ++nm;
       }
     pb.dec.reserve(nd);
-    pb.mrows.reserve(nm);
-    pb.mslots.reserve(nm * 4);
+    pb.dec_pre.reserve(nd + 1);
+    pb.mrg.reserve(nm);
+    pb.mrg_pre.reserve(nm + 1);
   }
   int64_t kv_tokens = 0, dec_keys = 0, dec_rows = 0;
   for (int gi = 0; gi < G; ++gi) kv_tokens += (int64_t)b->group_prefix_blocks[gi] * kBlock;
@@ -553,36 +562,32 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
       const bool direct = !cascaded && nsplit == 1;
       const int rows = ql * g;
       dec_rows += rows * Hkv;
-      for (int h = 0; h < Hkv; ++h) {
-        const int64_t base = direct ? -1 : pb.n_slots;
-        if (!direct) pb.n_slots += (int64_t)nsplit * rows;
-        for (int s = 0; s < nsplit; ++s) {
-          DecodeItem it{};
-          it.q_row0 = q0;
-          it.n_tok = ql;
-          it.kv_head = h;
-          it.table_row = i;
-          it.k0 = kb + s * kSplitKeys;
-          it.k1 = std::min(ctx, kb + (s + 1) * kSplitKeys);
-          it.pos0 = ctx - ql;
-          it.slot = direct ? -1 : (int32_t)(base + (int64_t)s * rows);
-          pb.dec.push_back(it);
-          dec_keys += it.k1 - it.k0;
-        }
-        if (!direct) {
-          for (int r = 0; r < rows; ++r) {
-            MergeRow mr{q0 + r / g, h * g + r % g, (int32_t)pb.mslots.size(), 0};
-            if (cascaded) {
-              pb.mslots.push_back((int32_t)(casc_base[gi][h] + (int64_t)member_idx[i] * g + r));
-              mr.s_count++;
-            }
-            for (int s = 0; s < nsplit; ++s) {
-              pb.mslots.push_back((int32_t)(base + (int64_t)s * rows + r));
-              mr.s_count++;
-            }
-            pb.mrows.push_back(mr);
-          }
-        }
+      // head-factored: one request entry; the kernel runs every (split, kv head); partial slot
+      // of (head h, split s, row r) = base + (h * nsplit + s) * rows + r
+      const int64_t base = direct ? -1 : pb.n_slots;
+      if (!direct) pb.n_slots += (int64_t)nsplit * rows * Hkv;
+      DecodeReq dq{};
+      dq.q_row0 = q0;
+      dq.n_tok = ql;
+      dq.table_row = i;
+      dq.kb = kb;
+      dq.ctx = ctx;
+      dq.slot = direct ? -1 : (int32_t)base;
+      dq.nsplit = nsplit;
+      pb.dec.push_back(dq);
+      pb.dec_pre.push_back(pb.dec_pre.back() + nsplit);
+      dec_keys += (int64_t)(ctx - kb) * Hkv;
+      if (!direct) {
+        MergeReq mq{};
+        mq.q_row0 = q0;
+        mq.rows = rows;
+        // casc_base[gi][h] = casc_base[gi][0] + h * group_rows[gi]
+        mq.casc_slot = cascaded ? (int32_t)(casc_base[gi][0] + (int64_t)member_idx[i] * g) : -1;
+        mq.casc_hstride = cascaded ? group_rows[gi] : 0;
+        mq.split_slot = (int32_t)base;
+        mq.nsplit = nsplit;
+        pb.mrg.push_back(mq);
+        pb.mrg_pre.push_back(pb.mrg_pre.back() + rows);
       }
     } else {
       const int rows = ql * g;
@@ -619,9 +624,9 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   pb.tile_flops = pb.stats.tile_flops;
   std::stable_sort(pb.tile.begin(), pb.tile.end(),
                    [](const TileItem &a, const TileItem &c) { return a.k1 - a.k0 > c.k1 - c.k0; });
-  pb.stats.n_decode_items = (int64_t)pb.dec.size();
+  pb.stats.n_decode_items = (int64_t)pb.dec_pre.back() * Hkv;  // (split, head) units
   pb.stats.n_tile_items = (int64_t)pb.tile.size();
-  pb.stats.n_merge_rows = (int64_t)pb.mrows.size();
+  pb.stats.n_merge_rows = (int64_t)pb.mrg_pre.back() * Hkv;
   pb.stats.kv_bytes_algorithmic = kv_tokens * Hkv * d * 2 * 2;
   const int64_t total_q = b->q_indptr[R];
   pb.stats.q_bytes = total_q * Hq * d * 2;
@@ -631,9 +636,10 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
 }
 
 static size_t plan_bytes(const PlanBuild &pb, int d, size_t *arrays_bytes) {
-  size_t a = align256(sizeof(DecodeItem) * pb.dec.size()) + align256(sizeof(TileItem) * pb.tile.size()) +
-             align256(sizeof(MergeRow) * pb.mrows.size()) + align256(4 * pb.mslots.size()) +
-             align256(4 * pb.row_list.size()) + 5 * 256;
+  // upper bound: the request lists count even when they travel as kernel parameters
+  size_t a = align256(sizeof(DecodeReq) * pb.dec.size()) + align256(4 * pb.dec_pre.size()) +
+             align256(sizeof(MergeReq) * pb.mrg.size()) + align256(4 * pb.mrg_pre.size()) +
+             align256(sizeof(TileItem) * pb.tile.size()) + align256(4 * pb.row_list.size()) + 6 * 256;
   if (arrays_bytes) *arrays_bytes = a;
   return a + align256((size_t)pb.n_slots * d * 4) + align256((size_t)pb.n_slots * 4);
 }
@@ -672,7 +678,21 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->tmv = p->tmv;
   pl->stats = pb.stats;
   uint8_t *dws = static_cast<uint8_t *>(ws);
-  if (arrays > 5 * 256) {
+  // request lists: kernel parameters when they fit, else uploaded with the tile items
+  const bool dec_inline = pb.dec.size() <= (size_t)kInlineReqs;
+  const bool mrg_inline = pb.mrg.size() <= (size_t)kInlineReqs;
+  pl->dec.n = (int32_t)pb.dec.size();
+  pl->mrg.n = (int32_t)pb.mrg.size();
+  if (dec_inline) {
+    std::copy(pb.dec.begin(), pb.dec.end(), pl->dec.req);
+    std::copy(pb.dec_pre.begin(), pb.dec_pre.end(), pl->dec.pre);
+  }
+  if (mrg_inline) {
+    std::copy(pb.mrg.begin(), pb.mrg.end(), pl->mrg.req);
+    std::copy(pb.mrg_pre.begin(), pb.mrg_pre.end(), pl->mrg.pre);
+  }
+  const bool need_upload = !pb.tile.empty() || !dec_inline || !mrg_inline;
+  if (need_upload) {
     Staging::Slot *slot = nullptr;
     cudaError_t e = p->staging.get(arrays, &slot);
     if (e != cudaSuccess) {
@@ -687,16 +707,30 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       off += align256(std::max<size_t>(n, 4));
       return dws + o;
     };
-    pl->d_dec = reinterpret_cast<const DecodeItem *>(put(pb.dec.data(), sizeof(DecodeItem) * pb.dec.size()));
     pl->d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), sizeof(TileItem) * pb.tile.size()));
-    pl->d_mrows = reinterpret_cast<const MergeRow *>(put(pb.mrows.data(), sizeof(MergeRow) * pb.mrows.size()));
-    pl->d_mslots = reinterpret_cast<const int32_t *>(put(pb.mslots.data(), 4 * pb.mslots.size()));
     pl->p.row_list = reinterpret_cast<const int32_t *>(put(pb.row_list.data(), 4 * pb.row_list.size()));
-    e = p->staging.upload(slot, ws, off, s);
+    if (!dec_inline) {
+      pl->dec.ptr = reinterpret_cast<const DecodeReq *>(put(pb.dec.data(), sizeof(DecodeReq) * pb.dec.size()));
+      pl->dec.pre_ptr = reinterpret_cast<const int32_t *>(put(pb.dec_pre.data(), 4 * pb.dec_pre.size()));
+    }
+    if (!mrg_inline) {
+      pl->mrg.ptr = reinterpret_cast<const MergeReq *>(put(pb.mrg.data(), sizeof(MergeReq) * pb.mrg.size()));
+      pl->mrg.pre_ptr = reinterpret_cast<const int32_t *>(put(pb.mrg_pre.data(), 4 * pb.mrg_pre.size()));
+    }
+    // upload on the side stream, ordered after everything already enqueued on `stream`
+    // (WAR on the workspace), so the decode launch on `stream` does not queue behind a
+    // copy-engine transfer
+    e = cudaEventCreateWithFlags(&pl->ev_up0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_up1, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(pl->ev_up0, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->aux, pl->ev_up0, 0);
+    if (e == cudaSuccess) e = p->staging.upload(slot, ws, off, p->aux);
+    if (e == cudaSuccess) e = cudaEventRecord(pl->ev_up1, p->aux);
     if (e != cudaSuccess) {
       delete pl;
       return fail(KVA_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
     }
+    pl->uploaded = true;
   }
   pl->tile_tc = tile_use_tc();
   pl->tile_impl = tile_impl_for(b);
@@ -732,9 +766,9 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->stats.host_validate_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
   pl->stats.host_build_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
   pl->stats.host_total_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t3 - t0).count();
-  pl->n_dec = (int)pb.dec.size();
+  pl->n_dec = pb.dec_pre.back() * b->num_kv_heads;
   pl->n_tile = (int)pb.tile.size();
-  pl->n_mrows = (int)pb.mrows.size();
+  pl->n_mrows = pb.mrg_pre.back() * b->num_kv_heads;
   AttnParams &ap = pl->p;
   ap.k_pool = static_cast<const uint16_t *>(p->desc.k_pool);
   ap.v_pool = static_cast<const uint16_t *>(p->desc.v_pool);
@@ -802,7 +836,14 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     CUDA_TRY(cudaStreamWaitEvent(pl->aux, pl->ev_fork, 0));
     ts = pl->aux;
   }
+  // kernels reading uploaded plan arrays on `s` wait for the side-stream upload (the tile
+  // kernel on the side stream is ordered after it already)
+  auto wait_upload = [&](bool needed) -> kva_status {
+    if (needed && pl->uploaded) CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_up1, 0));
+    return KVA_OK;
+  };
   auto run_tile = [&]() -> kva_status {
+    if (ts == s && wait_upload(true) != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
     if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
@@ -815,8 +856,9 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     return KVA_OK;
   };
   auto run_decode = [&]() -> kva_status {
+    if (wait_upload(pl->dec.ptr != nullptr) != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
-    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->d_dec, pl->n_dec, s));
+    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     return KVA_OK;
   };
@@ -834,7 +876,10 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     CUDA_TRY(cudaEventRecord(pl->ev_join, pl->aux));
     CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_join, 0));
   }
-  if (phases & KVA_PHASE_MERGE) CUDA_TRY(launch_merge(p, pl->d_mrows, pl->d_mslots, pl->n_mrows, s));
+  if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) {
+    if (wait_upload(pl->mrg.ptr != nullptr) != KVA_OK) return KVA_ERR_CUDA;
+    CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
+  }
   return KVA_OK;
 }
 
