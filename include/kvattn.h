@@ -87,6 +87,9 @@ kva_status kv_pool_destroy(kva_pool *pool);
 kva_status kv_pool_free_count(const kva_pool *pool, int64_t *n_free);
 /* Re-read free_bits from the device (synchronous) after the caller edited it. */
 kva_status kv_pool_resync(kva_pool *pool);
+/* Make `stream` wait (device-side, no host sync) for the pool's side-stream kv_append writes
+ * (see kv_append "Ordering"). */
+kva_status kv_pool_sync(kva_pool *pool, kva_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
  * Batch descriptor: the iteration's batch T_i of prefill chunks + decode tokens (P:172,
@@ -135,6 +138,13 @@ kva_status kva_validate_batch(const kva_batch_desc *desc, int32_t num_blocks, in
  *   k_new, v_new : device bf16 [total_q][num_kv_heads][head_dim]; token stride
  *                  new_stride_tok elements (>= num_kv_heads*head_dim), heads contiguous.
  *   workspace    : device scratch of kv_append_workspace_size() bytes (16-B aligned).
+ * Ordering: the table update and the rows of decode-class requests (q_len * Hq/Hkv <= 16,
+ *   read by the decode kernel) are written in order on `stream`; the rows of the other
+ *   requests (read only by the tensor-core tile kernel) are written on the pool's side stream
+ *   so that the decode kernel does not queue behind them.  Every later call taking this pool
+ *   (kv_append, hybrid_attention_run with the tile or all phases, kv_release_blocks) orders
+ *   itself after those writes; other work on `stream` that reads the pool or reuses
+ *   k_new / v_new calls kv_pool_sync(pool, stream) first.
  * Errors: KVA_NEEDS_EVICTION (needed > free, *deficit_blocks = needed - free, nothing
  * enqueued); KVA_ERR_CAPACITY (ceil(ctx/16) > num_blocks for some request);
  * KVA_ERR_GROUP (an appended position inside a group prefix); KVA_ERR_INVALID.

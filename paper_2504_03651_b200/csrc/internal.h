@@ -98,13 +98,20 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void 
 cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);
-cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,
-                               const int32_t *ids, int32_t n, cudaStream_t s);
+// Newly allocated blocks (table entry index, block id): kernel parameter when n <= kInlineAlloc,
+// else uploaded (tbl_ptr / ids_ptr set).
+constexpr int kInlineAlloc = 1536;
+struct AllocList {
+  int32_t n;
+  const int32_t *tbl_ptr, *ids_ptr;
+  int32_t tbl[kInlineAlloc];
+  int32_t ids[kInlineAlloc];
+};
+cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const AllocList &al, cudaStream_t s);
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
-                          const int32_t *block_table, int32_t max_blocks, const AppendReq *reqs,
-                          const int32_t *q_indptr, int32_t num_reqs, int32_t total_new_tok,
-                          cudaStream_t s);
+                          const int32_t *block_table, int32_t max_blocks,
+                          const ReqList<AppendReq> &reqs, int32_t total_new_tok, cudaStream_t s);
 cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
                               const uint16_t *depth, int64_t n, uint64_t *keys, cudaStream_t s);
 size_t evict_select_ws_bytes(int64_t n, int64_t k);

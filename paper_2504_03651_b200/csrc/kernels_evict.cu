@@ -589,9 +589,13 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // as in the kernel
   const size_t static_smem = 3 * 256 * 4 + 32 * 4 + 2 * 32 * 8 + 4 * 8 + kWarps * 256 * 4 + 1024;
   size_t dyn = (size_t)per * sizeof(uint64_t);
-  int cache = 1;
-  if (dyn + static_smem > (size_t)max_smem) { dyn = 0; cache = 0; }
-  if (const char *e = getenv("KVA_EVICT_NOCACHE")) if (atoi(e)) { dyn = 0; cache = 0; }
+  // Keys are re-read from L2 each round by default (8 MB << 126 MB L2): without the 110 KB
+  // shared-memory slice cache a selection CTA co-resides with a decode CTA, which measured
+  // better for the whole step although the kernel alone is ~15% slower.
+  // KVA_EVICT_CACHE=1 caches the slice in shared memory.
+  int cache = 0;
+  if (const char *e = getenv("KVA_EVICT_CACHE")) cache = atoi(e) != 0;
+  if (!cache || dyn + static_smem > (size_t)max_smem) { dyn = 0; cache = 0; }
   cudaError_t e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   // full shared-memory carveout so CTAs of concurrently running kernels can share an SM

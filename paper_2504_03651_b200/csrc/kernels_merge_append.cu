@@ -92,23 +92,21 @@ cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n
 // ---------------------------------------------------------------------------------------
 // a2: KV append.  (1) alloc_write publishes the ids the host allocator chose (smallest free
 // first, reading #13) in the device block table and clears their free bits; (2) the scatter
-// copies every (new token, local kv-head) row to slot (table[i][t/16], t % 16): one warp per
-// unit, lanes 0-15 move K and 16-31 move V in 16-byte vectors (one d=128 bf16 row each).
+// copies every (new token, local kv-head) row of a request list (exclusive token prefix
+// tok_pre) to slot (table[i][t/16], t % 16).
 // ---------------------------------------------------------------------------------------
 __global__ void alloc_write_kernel(int32_t *__restrict__ block_table, uint32_t *__restrict__ free_bits,
-                                   const int32_t *__restrict__ tbl_idx, const int32_t *__restrict__ ids,
-                                   int32_t n) {
+                                   const __grid_constant__ AllocList al) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t id = ids[i];
-  block_table[tbl_idx[i]] = id;
+  if (i >= al.n) return;
+  const int32_t id = al.ids_ptr ? al.ids_ptr[i] : al.ids[i];
+  block_table[al.tbl_ptr ? al.tbl_ptr[i] : al.tbl[i]] = id;
   atomicAnd(free_bits + (id >> 5), ~(1u << (id & 31)));
 }
 
-cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const int32_t *tbl_idx,
-                               const int32_t *ids, int32_t n, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  alloc_write_kernel<<<(n + 255) / 256, 256, 0, s>>>(block_table, free_bits, tbl_idx, ids, n);
+cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const AllocList &al, cudaStream_t s) {
+  if (al.n <= 0) return cudaSuccess;
+  alloc_write_kernel<<<(al.n + 255) / 256, 256, 0, s>>>(block_table, free_bits, al);
   return cudaGetLastError();
 }
 
@@ -119,8 +117,11 @@ constexpr int kUnitsPerCta = 32;
 __global__ void __launch_bounds__(256) append_kernel(
     const uint16_t *__restrict__ k_new, const uint16_t *__restrict__ v_new, int64_t stride_tok,
     uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
-    const int32_t *__restrict__ block_table, int32_t max_blocks, const AppendReq *__restrict__ reqs,
-    const int32_t *__restrict__ q_indptr, int32_t num_reqs, int32_t total_new_tok) {
+    const int32_t *__restrict__ block_table, int32_t max_blocks, const __grid_constant__ ReqList<AppendReq> L,
+    int32_t total_new_tok) {
+  const AppendReq *reqs = L.ptr ? L.ptr : L.req;
+  const int32_t *tok_pre = L.ptr ? L.pre_ptr : L.pre;
+  const int num_reqs = L.n;
   __shared__ int64_t s_src[kUnitsPerCta], s_dst[kUnitsPerCta];
   const int64_t n_units = (int64_t)total_new_tok * Hkv;
   const int64_t u0 = (int64_t)blockIdx.x * kUnitsPerCta;
@@ -128,16 +129,17 @@ __global__ void __launch_bounds__(256) append_kernel(
     const int64_t unit = u0 + threadIdx.x;
     int64_t src = -1, dst = -1;
     if (unit < n_units) {
-      const int row = (int)(unit / Hkv), h = (int)(unit % Hkv);
-      int lo = 0, hi = num_reqs - 1;  // request of this token: last i with q_indptr[i] <= row
+      const int j = (int)(unit / Hkv), h = (int)(unit % Hkv);  // j-th new token of the list
+      int lo = 0, hi = num_reqs - 1;  // its request: last i with tok_pre[i] <= j
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(q_indptr + mid) <= row) lo = mid; else hi = mid - 1;
+        if (tok_pre[mid] <= j) lo = mid; else hi = mid - 1;
       }
       const AppendReq rq = reqs[lo];
-      const int t = rq.pos0 + (row - rq.q_row0);
+      const int off = j - tok_pre[lo];
+      const int t = rq.pos0 + off;
       const int32_t id = block_table[(int64_t)rq.table_row * max_blocks + t / kBlock];
-      src = (int64_t)row * stride_tok + (int64_t)h * d;
+      src = (int64_t)(rq.q_row0 + off) * stride_tok + (int64_t)h * d;
       dst = (((int64_t)id * Hkv + h) * kBlock + t % kBlock) * d;
     }
     s_src[threadIdx.x] = src;
@@ -172,17 +174,15 @@ __global__ void __launch_bounds__(256) append_kernel(
 
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
-                          const int32_t *block_table, int32_t max_blocks, const AppendReq *reqs,
-                          const int32_t *q_indptr, int32_t num_reqs, int32_t total_new_tok,
-                          cudaStream_t s) {
+                          const int32_t *block_table, int32_t max_blocks,
+                          const ReqList<AppendReq> &L, int32_t total_new_tok, cudaStream_t s) {
   const int64_t units = (int64_t)total_new_tok * Hkv;
-  if (units <= 0) return cudaSuccess;
+  if (units <= 0 || L.n <= 0) return cudaSuccess;
   static bool carve = (cudaFuncSetAttribute(append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared), true);
   (void)carve;
   append_kernel<<<(unsigned)((units + kUnitsPerCta - 1) / kUnitsPerCta), 256, 0, s>>>(
-      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, reqs, q_indptr,
-      num_reqs, total_new_tok);
+      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, L, total_new_tok);
   return cudaGetLastError();
 }
 

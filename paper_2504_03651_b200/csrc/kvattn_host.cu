@@ -159,6 +159,11 @@ struct kva_pool {
   // decode kernel on the caller's stream; fork/join by events)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // kv_append's side-stream part (rows read only by the tile kernel): ev_app marks its end;
+  // later calls on the pool order themselves after it (kv_pool_sync for anything else)
+  cudaEvent_t ev_afork = nullptr, ev_app = nullptr;
+  bool app_pending = false;
+  cudaStream_t aux_lo = nullptr;  // least-priority side stream of those writes (yields to decode)
 };
 
 static int64_t count_free(const std::vector<uint32_t> &w, int nb) {
@@ -197,8 +202,11 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&p->aux_lo, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_afork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_app, cudaEventDisableTiming) != cudaSuccess) {
       delete p;
       return fail(KVA_ERR_CUDA, "creating the side stream/events failed");
     }
@@ -220,10 +228,21 @@ extern "C" kva_status kv_pool_destroy(kva_pool *p) {
     DeviceGuard dg(p->desc.device);
     p->staging.release();
     if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->aux_lo) cudaStreamDestroy(p->aux_lo);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->ev_afork) cudaEventDestroy(p->ev_afork);
+    if (p->ev_app) cudaEventDestroy(p->ev_app);
   }
   delete p;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_pool_sync(kva_pool *p, kva_stream_t stream) {
+  if (!p) return fail(KVA_ERR_INVALID, "null pool");
+  if (!p->app_pending) return KVA_OK;
+  DeviceGuard dg(p->desc.device);
+  CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), p->ev_app, 0));
   return KVA_OK;
 }
 
@@ -317,16 +336,14 @@ extern "C" kva_status kva_validate_batch(const kva_batch_desc *b, int32_t num_bl
 // kv_append (a2)
 // ------------------------------------------------------------------------------------------
 struct AppendPlan {
-  std::vector<AppendReq> reqs;
   std::vector<int32_t> tbl_idx, ids;
   int64_t need = 0;
-  int total_q = 0;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static size_t append_upload_bytes(int R, int64_t nalloc) {
-  return align256(sizeof(AppendReq) * std::max(R, 1)) + align256(4 * (R + 1)) +
+static size_t append_upload_bytes(int R, int64_t nalloc) {  // both request lists + allocations
+  return 2 * align256(sizeof(AppendReq) * std::max(R, 1)) + 2 * align256(4 * (R + 1)) +
          2 * align256(4 * std::max<int64_t>(nalloc, 1));
 }
 
@@ -356,7 +373,6 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       (stride_tok % 8))
     return fail(KVA_ERR_INVALID, "k_new/v_new must be 16-byte aligned with stride %% 8 == 0");
   AppendPlan ap;
-  ap.reqs.resize(b->num_reqs);
   // count needed blocks (entries == -1 among new positions' blocks), validate the rest
   for (int i = 0; i < b->num_reqs; ++i) {
     const int ql = qlen(b, i), ctx = b->ctx_len[i], start = ctx - ql;
@@ -368,7 +384,6 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       else if (row[k] < 0 || row[k] >= nb)
         return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid", i, k, row[k]);
     }
-    ap.reqs[i] = AppendReq{b->q_indptr[i], ql, start, i};
   }
   if (ap.need > p->n_free) {
     if (deficit) *deficit = (int32_t)(ap.need - p->n_free);
@@ -392,30 +407,92 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       ap.ids.push_back(scan);
     }
   }
-  ap.total_q = b->q_indptr[b->num_reqs];
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Staging::Slot *slot = nullptr;
-  CUDA_TRY(p->staging.get(up, &slot));
-  uint8_t *h = static_cast<uint8_t *>(slot->host);
-  uint8_t *dws = static_cast<uint8_t *>(workspace);
-  size_t off = 0;
-  auto put = [&](const void *src, size_t n) {
-    std::memcpy(h + off, src, n);
-    const size_t o = off;
-    off += align256(std::max<size_t>(n, 4));
-    return dws + o;
-  };
-  auto *d_reqs = reinterpret_cast<AppendReq *>(put(ap.reqs.data(), sizeof(AppendReq) * ap.reqs.size()));
-  auto *d_qi = reinterpret_cast<int32_t *>(put(b->q_indptr, 4 * (b->num_reqs + 1)));
-  auto *d_tbl = reinterpret_cast<int32_t *>(put(ap.tbl_idx.data(), 4 * ap.tbl_idx.size()));
-  auto *d_ids = reinterpret_cast<int32_t *>(put(ap.ids.data(), 4 * ap.ids.size()));
-  CUDA_TRY(p->staging.upload(slot, workspace, off, s));
-  CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, d_tbl, d_ids, (int)ap.ids.size(), s));
+  // earlier side-stream appends may still read this workspace / write the pool
+  if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));
+  // Split by the kernel that reads the new rows: decode-class requests (served by the decode
+  // kernel on `stream`) are appended on `stream`; the rest (read only by the tile kernel, which
+  // runs on the pool's side stream) are appended on the side stream, off the decode kernel's
+  // critical path.  Lists travel as kernel parameters unless they overflow the inline capacity.
+  const int g = b->num_q_heads / b->num_kv_heads;
+  std::vector<AppendReq> ra, rb;
+  std::vector<int32_t> pa{0}, pbv{0};
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int ql = qlen(b, i);
+    if (ql == 0) continue;
+    const AppendReq rq{b->q_indptr[i], ql, b->ctx_len[i] - ql, i};
+    if (ql * g <= kDecodeRows) {
+      ra.push_back(rq);
+      pa.push_back(pa.back() + ql);
+    } else {
+      rb.push_back(rq);
+      pbv.push_back(pbv.back() + ql);
+    }
+  }
+  ReqList<AppendReq> la{}, lb{};
+  AllocList al{};
+  la.n = (int32_t)ra.size();
+  lb.n = (int32_t)rb.size();
+  al.n = (int32_t)ap.ids.size();
+  const bool up_a = ra.size() > (size_t)kInlineReqs, up_b = rb.size() > (size_t)kInlineReqs;
+  const bool up_al = ap.ids.size() > (size_t)kInlineAlloc;
+  if (!up_a) {
+    std::copy(ra.begin(), ra.end(), la.req);
+    std::copy(pa.begin(), pa.end(), la.pre);
+  }
+  if (!up_b) {
+    std::copy(rb.begin(), rb.end(), lb.req);
+    std::copy(pbv.begin(), pbv.end(), lb.pre);
+  }
+  if (!up_al) {
+    std::copy(ap.tbl_idx.begin(), ap.tbl_idx.end(), al.tbl);
+    std::copy(ap.ids.begin(), ap.ids.end(), al.ids);
+  }
+  if (up_a || up_b || up_al) {
+    Staging::Slot *slot = nullptr;
+    CUDA_TRY(p->staging.get(up, &slot));
+    uint8_t *h = static_cast<uint8_t *>(slot->host);
+    uint8_t *dws = static_cast<uint8_t *>(workspace);
+    size_t off = 0;
+    auto put = [&](const void *src, size_t n) {
+      if (n) std::memcpy(h + off, src, n);
+      const size_t o = off;
+      off += align256(std::max<size_t>(n, 4));
+      return dws + o;
+    };
+    if (up_a) {
+      la.ptr = reinterpret_cast<const AppendReq *>(put(ra.data(), sizeof(AppendReq) * ra.size()));
+      la.pre_ptr = reinterpret_cast<const int32_t *>(put(pa.data(), 4 * pa.size()));
+    }
+    if (up_b) {
+      lb.ptr = reinterpret_cast<const AppendReq *>(put(rb.data(), sizeof(AppendReq) * rb.size()));
+      lb.pre_ptr = reinterpret_cast<const int32_t *>(put(pbv.data(), 4 * pbv.size()));
+    }
+    if (up_al) {
+      al.tbl_ptr = reinterpret_cast<const int32_t *>(put(ap.tbl_idx.data(), 4 * ap.tbl_idx.size()));
+      al.ids_ptr = reinterpret_cast<const int32_t *>(put(ap.ids.data(), 4 * ap.ids.size()));
+    }
+    CUDA_TRY(p->staging.upload(slot, workspace, off, s));
+  }
+  CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, al, s));
+  if (!rb.empty()) {  // fork after the table update, before the decode-class append
+    CUDA_TRY(cudaEventRecord(p->ev_afork, s));
+    CUDA_TRY(cudaStreamWaitEvent(p->aux_lo, p->ev_afork, 0));
+  }
   CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
                          stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
                          static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                         b->max_blocks, d_reqs, d_qi, b->num_reqs, ap.total_q, s));
+                         b->max_blocks, la, pa.back(), s));
+  if (!rb.empty()) {
+    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
+                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
+                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
+                           b->max_blocks, lb, pbv.back(), p->aux_lo));
+    CUDA_TRY(cudaEventRecord(p->ev_app, p->aux_lo));
+    CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_app, 0));  // the tile kernel's stream
+    p->app_pending = true;
+  }
   // commit host state: free mirror + caller's host table mirror
   p->free_host.swap(fh);
   p->n_free -= ap.need;
@@ -437,6 +514,7 @@ struct kva_plan {
   // by ev_up0); a kernel that reads uploaded arrays on `stream` first waits ev_up1
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
   bool uploaded = false;
+  kva_pool *pool = nullptr;  // for the side-stream append event (the pool outlives its plans)
   ~kva_plan() {
     if (ev_up0) cudaEventDestroy(ev_up0);
     if (ev_up1) cudaEventDestroy(ev_up1);
@@ -735,6 +813,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->tile_tc = tile_use_tc();
   pl->tile_impl = tile_impl_for(b);
   pl->aux = p->aux;
+  pl->pool = p;
   pl->ev_fork = p->ev_fork;
   pl->ev_join = p->ev_join;
   {
@@ -842,8 +921,15 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (needed && pl->uploaded) CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_up1, 0));
     return KVA_OK;
   };
+  // rows appended on the side stream are read only by the tile kernel: on `s` it waits for them
+  // (on the side stream it is ordered after them already)
+  auto wait_append = [&]() -> kva_status {
+    if (pl->pool->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, pl->pool->ev_app, 0));
+    return KVA_OK;
+  };
   auto run_tile = [&]() -> kva_status {
     if (ts == s && wait_upload(true) != KVA_OK) return KVA_ERR_CUDA;
+    if (ts == s && wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
     if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
@@ -880,6 +966,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (wait_upload(pl->mrg.ptr != nullptr) != KVA_OK) return KVA_ERR_CUDA;
     CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
   }
+  // a full run leaves `s` ordered after every side-stream write of this step
+  if ((phases & KVA_PHASE_ALL) == KVA_PHASE_ALL && wait_append() != KVA_OK) return KVA_ERR_CUDA;
   return KVA_OK;
 }
 
@@ -924,6 +1012,7 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
   }
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));  // released blocks' writes
   // ids travel as kernel parameters (<= kReleaseBatch per launch): no device scratch,
   // no host<->device copy, stream-ordered like every other call
   for (int64_t off = 0; off < n; off += kReleaseBatch) {

@@ -55,7 +55,7 @@ class PlanStats(ctypes.Structure):
 
 
 EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_create", "kv_pool_destroy",
-           "kv_pool_free_count", "kv_pool_resync", "kv_append_workspace_size", "kv_append",
+           "kv_pool_free_count", "kv_pool_resync", "kv_pool_sync", "kv_append_workspace_size", "kv_append",
            "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
            "kva_plan_destroy",
@@ -89,6 +89,7 @@ def load(build_if_missing: bool = True):
         "kv_pool_destroy": ([P], ctypes.c_int),
         "kv_pool_free_count": ([P, P], ctypes.c_int),
         "kv_pool_resync": ([P], ctypes.c_int),
+        "kv_pool_sync": ([P, P], ctypes.c_int),
         "kv_append_workspace_size": ([P, P], ctypes.c_int),
         "kv_append": ([P, P, P, P, i64, P, P, sz, P], ctypes.c_int),
         "hybrid_attention_workspace_size": ([P, P], ctypes.c_int),
@@ -154,6 +155,10 @@ class Pool:
 
     def resync(self):
         _check(load().kv_pool_resync(self.handle))
+
+    def sync(self, stream=None):
+        """kv_pool_sync: order `stream` after the pool's side-stream kv_append writes."""
+        _check(load().kv_pool_sync(self.handle, _stream(stream)))
 
     def close(self):
         if self.handle:

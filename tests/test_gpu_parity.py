@@ -231,3 +231,25 @@ def test_full_size_sampled(name):
     o = gg["out"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
     l = gg["lse"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
     assert_attention_close(o, l, ref, ref_lse)
+
+
+def test_append_side_stream_ordering():
+    """kv_append writes the tile-path rows on the pool's side stream (include/kvattn.h
+    "Ordering"): after kv_pool_sync, work on the caller's stream sees the complete pool,
+    bit-identical to the oracle's kv_append (reading #13)."""
+    import paper_2504_03651_b200 as K
+    wl = W.make_workload("tiny")
+    dev = "cuda"
+    kp, vp = wl.k_pool.to(dev), wl.v_pool.to(dev)
+    pool = K.Pool(kp, vp, K.free_bits_tensor(wl.free_bits, dev))
+    batch = K.Batch(wl.batch, dev)
+    k_new, v_new = wl.k_new.to(dev), wl.v_new.to(dev)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        K.kv_append(pool, batch, k_new, v_new, stream=s)
+        pool.sync(s)
+        kc, vc = kp.clone(), vp.clone()
+    s.synchronize()
+    r = oracle_step(wl)
+    assert np.array_equal(bits16(kc), r["k_pool"]) and np.array_equal(bits16(vc), r["v_pool"])
