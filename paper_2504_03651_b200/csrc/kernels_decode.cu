@@ -17,7 +17,9 @@
 #include <cuda.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "internal.h"
@@ -288,6 +290,322 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// v2 (default): keys along the MMA M dimension.  For decode the rows (q_len x g <= 16) are few,
+// so S^T = K Q^T (M = 16 keys, N = 8 rows, K = d) and O^T = V^T P^T (M = 16 dims, N = 8 rows,
+// K = 16 keys) waste at most the N padding instead of 15/16 of M: half the MMAs of v1 and half
+// its accumulator registers.  P^T goes from the S^T accumulator layout to the B-operand layout
+// with two movmatrix transposes.  The running max is updated lazily (only when it grows by more
+// than 2^8 for some row of the warp, FA4-style), so the O rescale is skipped on almost every
+// block; masking runs only on blocks that reach the causal diagonal or the split end.  Fewer
+// instructions per byte let fewer SMs saturate HBM, which is what the co-scheduled tile
+// kernel needs (it runs on the remaining SMs).
+template <int D, int NR, int NST, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    decode_kt_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
+                     const __grid_constant__ CUtensorMap tmv, const __grid_constant__ ReqList<DecodeReq> L,
+                     int n_units) {
+  constexpr int HALVES = D / 64;
+  constexpr int KBYTES = 16 * D * 2;  // K (or V) of one block for one head
+  constexpr int STAGE = 2 * KBYTES;
+  constexpr int KT = D / 16;          // k-steps of S^T = K Q^T
+  constexpr int MT = D / 16;          // m-tiles (dims) of O^T
+  constexpr int SROW = D + 4;         // padded fp32 row of the output staging tile
+  static_assert(NST * STAGE >= NR * 8 * SROW * 4, "staging tile must fit the ring");
+  constexpr float kLazy = 8.f;        // rescale only when the max grows by > 2^8
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[4][NST];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * 4 + warp;  // (item, kv head), head fastest
+  if (unit >= n_units) return;             // no CTA-wide barrier below
+  const int item = unit / p.Hkv, kv_head = unit - item * p.Hkv;
+  const DecodeReq *reqs = L.ptr ? L.ptr : L.req;
+  const int32_t *pre = L.ptr ? L.pre_ptr : L.pre;
+  int lo = 0, hi = L.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  const DecodeReq rq = reqs[lo];
+  const int split = item - pre[lo];
+  const int q_row0 = rq.q_row0, n_tok = rq.n_tok;
+  const int k0 = rq.kb + split * kSplitKeys;
+  const int k1 = min(rq.ctx, k0 + kSplitKeys);
+  const int pos0 = rq.ctx - rq.n_tok;
+  const int slot = rq.slot < 0 ? -1 : rq.slot + (kv_head * rq.nsplit + split) * (n_tok * p.g);
+  uint8_t *sbase = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  uint8_t *ws = sbase + warp * NST * STAGE;
+  uint64_t *bar = bars[warp];
+  const int g = p.g;
+  const int n_rows = n_tok * g;
+
+  if (lane == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int b0 = k0 / kBlock;
+  const int nblk = (k1 + kBlock - 1) / kBlock - b0;  // <= 32
+  const int32_t *trow = p.block_table + (int64_t)rq.table_row * p.max_blocks + b0;
+  const int my_id = lane < nblk ? __ldg(trow + lane) : 0;
+  const int row_base = kv_head * kBlock;
+
+  auto issue = [&](int st, int id) {  // lane 0 only
+    uint64_t *b = &bar[st];
+    mbar_arrive_expect_tx(b, STAGE);
+    const int row = id * p.Hkv * kBlock + row_base;
+    uint8_t *dst = ws + st * STAGE;
+#pragma unroll
+    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
+#pragma unroll
+    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
+  };
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int id = __shfl_sync(0xffffffffu, my_id, s);
+    if (lane == 0 && s < nblk) issue(s, id);
+  }
+
+  // Q^T as the B operand: n = row (nt*8 + lane/4), k = dims (lane%4)*2 (+1, +8, +9)
+  const int cq = (lane & 3) * 2;
+  uint32_t qb[NR][KT][2];
+#pragma unroll
+  for (int nt = 0; nt < NR; ++nt) {
+    const int r = nt * 8 + (lane >> 2);
+    const uint32_t *qp = nullptr;
+    if (r < n_rows)
+      qp = reinterpret_cast<const uint32_t *>(p.q + (int64_t)(q_row0 + r / g) * p.q_stride_tok +
+                                              (int64_t)(kv_head * g + r % g) * p.q_stride_head);
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      qb[nt][kk][0] = qp ? __ldg(qp + (kk * 16 + cq) / 2) : 0u;
+      qb[nt][kk][1] = qp ? __ldg(qp + (kk * 16 + cq + 8) / 2) : 0u;
+    }
+  }
+  // this thread's rows (accumulator columns): nt*8 + cq + {0, 1}
+  float m[NR][2], l[NR][2];
+  float o[MT][NR][4];
+#pragma unroll
+  for (int nt = 0; nt < NR; ++nt) {
+    m[nt][0] = m[nt][1] = -CUDART_INF_F;
+    l[nt][0] = l[nt][1] = 0.f;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) o[mt][nt][0] = o[mt][nt][1] = o[mt][nt][2] = o[mt][nt][3] = 0.f;
+  }
+  const float sl2 = p.scale_log2;
+  // ldmatrix lane addresses: K as A (row = key, col = dim), V^T as A via .trans
+  const int ka_key = (lane & 7) + ((lane >> 3) & 1) * 8, ka_col = (lane >> 4) * 8;
+  const int va_key = (lane & 7) + (lane >> 4) * 8, va_col = ((lane >> 3) & 1) * 8;
+
+  int st = 0;
+  uint32_t ph = 0;
+  for (int j = 0; j < nblk; ++j) {
+    const int next_id = __shfl_sync(0xffffffffu, my_id, (j + NST) & 31);
+    mbar_wait(&bar[st], ph);
+    const uint32_t kb = smem_u32(ws + st * STAGE), vb = kb + KBYTES;
+    const int key0 = (b0 + j) * kBlock;
+    if (key0 + kBlock > k1) {
+      // never-written slots of the last block are NaN-poisoned: zero those V rows
+      const int vr = k1 - key0;
+      uint8_t *vp = ws + st * STAGE + KBYTES;
+      for (int c = lane; c < (16 - vr) * HALVES * 8; c += 32) {
+        const int h = c / ((16 - vr) * 8), rem = c % ((16 - vr) * 8);
+        const int row = vr + rem / 8, ch = rem % 8;
+        *reinterpret_cast<uint4 *>(vp + h * 2048 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    // S^T = K Q^T: 16 keys x 8*NR rows; even / odd k-steps in independent accumulators
+    float s[NR][4], s2[NR][4];
+#pragma unroll
+    for (int nt = 0; nt < NR; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[nt][e] = s2[nt][e] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KT; ++kk) {
+      const int col = kk * 16 + ka_col;
+      uint32_t a[4];
+      ldsm_x4(kb + (col >> 6) * 2048 + sw128(ka_key, col & 63), a[0], a[1], a[2], a[3]);
+#pragma unroll
+      for (int nt = 0; nt < NR; ++nt) {
+        if (kk & 1) mma_bf16(s2[nt], a, qb[nt][kk][0], qb[nt][kk][1]);
+        else mma_bf16(s[nt], a, qb[nt][kk][0], qb[nt][kk][1]);
+      }
+    }
+    // scale (log2 domain) + mask only where a key can be invisible: the split end or the
+    // causal diagonal of multi-token rows
+    const bool need_mask = key0 + kBlock > k1 || key0 + kBlock - 1 > pos0;
+#pragma unroll
+    for (int nt = 0; nt < NR; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[nt][e] = (s[nt][e] + s2[nt][e]) * sl2;
+    if (need_mask) {
+#pragma unroll
+      for (int nt = 0; nt < NR; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = key0 + (lane >> 2) + (e >> 1) * 8;
+          const int r = nt * 8 + cq + (e & 1);
+          const bool ok = key < k1 && key <= pos0 + r / g;
+          s[nt][e] = ok ? s[nt][e] : -CUDART_INF_F;
+        }
+    }
+    float mx[NR][2];
+    bool grow = false;
+#pragma unroll
+    for (int nt = 0; nt < NR; ++nt) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v = fmaxf(s[nt][c], s[nt][c + 2]);
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+        mx[nt][c] = v;
+        grow |= v > m[nt][c] + kLazy;
+      }
+    }
+    if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+      for (int nt = 0; nt < NR; ++nt) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float mn = fmaxf(m[nt][c], mx[nt][c]);
+          const float a = m[nt][c] == -CUDART_INF_F ? 0.f : fast_exp2(m[nt][c] - mn);
+          m[nt][c] = mn;
+          l[nt][c] *= a;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            o[mt][nt][c] *= a;
+            o[mt][nt][c + 2] *= a;
+          }
+        }
+      }
+    }
+    uint32_t pb[NR][2];
+#pragma unroll
+    for (int nt = 0; nt < NR; ++nt) {
+      const float bA = m[nt][0] == -CUDART_INF_F ? 0.f : m[nt][0];
+      const float bB = m[nt][1] == -CUDART_INF_F ? 0.f : m[nt][1];
+      const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bB);
+      const float p2 = fast_exp2(s[nt][2] - bA), p3 = fast_exp2(s[nt][3] - bB);
+      l[nt][0] += p0 + p2;
+      l[nt][1] += p1 + p3;
+      pb[nt][0] = movmatrix_t(pack_bf16(p0, p1));  // keys 0-7
+      pb[nt][1] = movmatrix_t(pack_bf16(p2, p3));  // keys 8-15
+    }
+    // O^T += V^T P^T
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int col = mt * 16 + va_col;
+      uint32_t a[4];
+      ldsm_x4_t(vb + (col >> 6) * 2048 + sw128(va_key, col & 63), a[0], a[1], a[2], a[3]);
+#pragma unroll
+      for (int nt = 0; nt < NR; ++nt) mma_bf16(o[mt][nt], a, pb[nt][0], pb[nt][1]);
+    }
+    __syncwarp();
+    if (lane == 0 && j + NST < nblk) {
+      fence_proxy_async();
+      issue(st, next_id);
+    }
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  // row sums over the 8 key-lanes
+#pragma unroll
+  for (int nt = 0; nt < NR; ++nt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v = l[nt][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      l[nt][c] = v;
+    }
+  // normalised O through a padded fp32 staging tile (the ring is idle: every issued stage
+  // was consumed), then row-contiguous stores
+  float *stg = reinterpret_cast<float *>(ws);
+  __syncwarp();
+#pragma unroll
+  for (int nt = 0; nt < NR; ++nt) {
+    const float iA = l[nt][0] > 0.f ? 1.f / l[nt][0] : 0.f;
+    const float iB = l[nt][1] > 0.f ? 1.f / l[nt][1] : 0.f;
+    const int rA = nt * 8 + cq;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int dm = mt * 16 + (lane >> 2);
+      stg[rA * SROW + dm] = o[mt][nt][0] * iA;
+      stg[(rA + 1) * SROW + dm] = o[mt][nt][1] * iB;
+      stg[rA * SROW + dm + 8] = o[mt][nt][2] * iA;
+      stg[(rA + 1) * SROW + dm + 8] = o[mt][nt][3] * iB;
+    }
+  }
+  constexpr float kLn2 = 0.6931471805599453f;
+  if (lane < 4) {
+#pragma unroll
+    for (int nt = 0; nt < NR; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int r = nt * 8 + cq + c;
+        if (r >= n_rows) continue;
+        const float lse = l[nt][c] > 0.f ? (m[nt][c] + __log2f(l[nt][c])) * kLn2 : -CUDART_INF_F;
+        if (slot < 0) {
+          if (p.lse) p.lse[(int64_t)(q_row0 + r / g) * p.Hq + kv_head * g + r % g] = lse;
+        } else {
+          p.part_lse[slot + r] = lse;
+        }
+      }
+  }
+  __syncwarp();
+  constexpr int V = D / 32;  // values per lane per row
+  for (int r = 0; r < n_rows; ++r) {
+    const float *src = stg + r * SROW + lane * V;
+    float v[V];
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const float2 t = *reinterpret_cast<const float2 *>(src + i);
+      v[i] = t.x;
+      v[i + 1] = t.y;
+    }
+    if (slot < 0) {
+      const int64_t qrow = q_row0 + r / g;
+      const int hq = kv_head * g + r % g;
+      if (p.out_f32) {
+        float *dst = reinterpret_cast<float *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+#pragma unroll
+        for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
+      } else {
+        uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+#pragma unroll
+        for (int i = 0; i < V; i += 2) *reinterpret_cast<uint32_t *>(dst + i) = pack_bf16(v[i], v[i + 1]);
+      }
+    } else {
+      float *dst = p.part_o + (int64_t)(slot + r) * D + lane * V;
+#pragma unroll
+      for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
+    }
+  }
+}
+
+template <int D, int NR, int NST, int MINB>
+static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const void *tmv,
+                                   const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
+  const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;
+  auto kern = decode_kt_kernel<D, NR, NST, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
+  const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
+  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, L, n);
+  return cudaGetLastError();
+}
+
 template <int D, int NST, int PF>
 static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const void *tmv,
                                    const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
@@ -307,6 +625,33 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
                           const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  // KVA_DECODE_IMPL=v1: the M = rows kernel (cross-check); default v2 (keys along M).
+  // KVA_DECODE_CFG: 0 = 3 stages x 2 CTAs/SM (default), 1 = 2 stages x 3 CTAs/SM.
+  static const int impl = [] {
+    const char *e = getenv("KVA_DECODE_IMPL");
+    return e && std::string(e) == "v1" ? 1 : 2;
+  }();
+  static const int cfg = [] {
+    const char *e = getenv("KVA_DECODE_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  if (impl == 2) {
+    int max_rows = 0;
+    const DecodeReq *reqs = L.ptr ? nullptr : L.req;
+    if (reqs)
+      for (int i = 0; i < L.n; ++i) max_rows = std::max(max_rows, reqs[i].n_tok * p.g);
+    else
+      max_rows = kDecodeRows;
+    const bool nr1 = max_rows <= 8;
+    if (p.d == 128) {
+      if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s)
+                               : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s);
+      return nr1 ? launch_decode_kt<128, 1, 3, 2>(p, tmk, tmv, L, n, s)
+                 : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s);
+    }
+    return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s)
+               : launch_decode_kt<64, 2, 4, 2>(p, tmk, tmv, L, n, s);
+  }
   static const int pf = [] {
     const char *e = getenv("KVA_DECODE_PF");
     return e ? atoi(e) : 0;  // L2 prefetch measured counter-productive

@@ -1,7 +1,8 @@
 """GPU parity of the alternative tile-kernel implementations and launch modes, each in a fresh
 process (the implementation is chosen once per process from KVA_TILE_IMPL / KVA_OVERLAP /
 KVA_TILE_CTAS): legacy mma.sync (64-row tiles), tcgen05 one-Q-tile, tcgen05 two-Q-tile
-(default), tcgen05 CTA-pair (cta_group::2), and overlapped vs sequential scheduling."""
+(default), tcgen05 CTA-pair (cta_group::2), and overlapped vs sequential scheduling; the two
+decode kernels (v1: rows along M, v2: keys along M) and v2's two occupancy configurations."""
 import os
 import subprocess
 import sys
@@ -20,6 +21,7 @@ from gpu_util import gpu_step, oracle_step, assert_attention_close
 reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 600 + 300, 300, 0), W.ReqSpec(W.OFFLINE_PREFILL, 600 + 173, 173, 0),
         W.ReqSpec(W.ONLINE_DECODE, 2000, 1), W.ReqSpec(W.ONLINE_DECODE, 77, 1)]
 reqs += [W.ReqSpec(W.OFFLINE_DECODE, 600 + 5 + i, 1, 0) for i in range(20)]
+reqs += [W.ReqSpec(W.OFFLINE_DECODE, 1100, 2), W.ReqSpec(W.OFFLINE_DECODE, 730, 2, 0)]
 for d, Hq, Hkv in [(128, 16, 2), (64, 8, 4)]:
     wl = W.make_workload(W.custom_config("v", Hq, Hkv, d, 7, reqs, [600 // 16]))
     g = gpu_step(wl)
@@ -50,3 +52,8 @@ def test_overlap_modes_bitexact(tmp_path):
     b = _run({"KVA_OVERLAP": "0"}, "seq", tmp_path)
     for d in (128, 64):
         assert np.array_equal(np.load(a + f"_{d}.npy"), np.load(b + f"_{d}.npy"))
+
+
+@pytest.mark.parametrize("env", [{"KVA_DECODE_IMPL": "v1"}, {"KVA_DECODE_CFG": "1"}])
+def test_decode_impl_parity(env, tmp_path):
+    _run(env, "dec_" + "_".join(env.values()), tmp_path)
