@@ -20,6 +20,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -133,7 +134,8 @@ __device__ __forceinline__ ItemGeom geom(const TileItem &it, int g) {
 
 }  // namespace tc2
 
-template <int D>
+// PP = column pairs (of every 16) whose exp2 runs as a polynomial on the FMA pipe
+template <int D, int PP>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     tile_tc2_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv, const TileItem *__restrict__ items,
@@ -378,9 +380,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           float m8[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) m8[i] = -CUDART_INF_F;
-          if (full) {
+          if (full) {  // 3-input max: half the instructions
 #pragma unroll
-            for (int i = 0; i < N; ++i) m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(u[i]));
+            for (int i = 0; i < N; i += 2) m8[(i >> 1) & 7] = fmax3(m8[(i >> 1) & 7], __uint_as_float(u[i]), __uint_as_float(u[i + 1]));
           } else {
 #pragma unroll
             for (int i = 0; i < N; ++i) m8[i & 7] = fmaxf(m8[i & 7], i < lim ? __uint_as_float(u[i]) : -CUDART_INF_F);
@@ -399,29 +401,42 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         const float nbase = m_used == -CUDART_INF_F ? 0.f : -m_used;
         // pass 2 (reload): P = exp2(s * scale - m), 4 independent row-sum chains, bf16 pairs
         // stored over S columns already read (P chunk c -> columns [16c, 16c+16))
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-        {
-          uint32_t u[N];
-          load_all(u);
+        // paired fp32 ops (FFMA2/FADD2); kPolyPairs of every 16 column pairs take exp2 on the
+        // FMA pipe (polynomial), the rest on MUFU, balancing the two units (PP of 16)
+        float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sc = make_float2(sl2, sl2), nb = make_float2(nbase, nbase);
 #pragma unroll
-          for (int c = 0; c < N / 32; ++c) {
+        for (int hb = 0; hb < 2; ++hb) {  // 64-column halves: fewer live registers (no spills)
+          uint32_t u[N];
+#pragma unroll
+          for (int c = 2 * hb; c < 2 * hb + 2; ++c)
+            ld32(t_row + COL_S[t] + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
+          wait_ld();
+#pragma unroll
+          for (int c = 2 * hb; c < 2 * hb + 2; ++c) {
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int i0 = c * 32 + 2 * i, i1 = i0 + 1;
-              float e0 = fast_exp2(fmaf(__uint_as_float(u[i0]), sl2, nbase));
-              float e1 = fast_exp2(fmaf(__uint_as_float(u[i1]), sl2, nbase));
-              if (!full) {
-                e0 = i0 < lim ? e0 : 0.f;
-                e1 = i1 < lim ? e1 : 0.f;
+              const float2 x = ffma2(make_float2(__uint_as_float(u[i0]), __uint_as_float(u[i1])), sc, nb);
+              float2 e;
+              if (i < PP) {
+                e = exp2_poly2(x);
+              } else {
+                e.x = fast_exp2(x.x);
+                e.y = fast_exp2(x.y);
               }
-              s4[i & 3] += e0 + e1;
-              pk[i] = pack_bf16(e0, e1);
+              if (!full) {
+                e.x = i0 < lim ? e.x : 0.f;
+                e.y = i1 < lim ? e.y : 0.f;
+              }
+              s2[i & 1] = fadd2(s2[i & 1], e);
+              pk[i] = pack_bf16(e.x, e.y);
             }
             st16(t_row + COL_S[t] + c * 16, pk);
           }
         }
-        const float ps = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        const float ps = (s2[0].x + s2[0].y) + (s2[1].x + s2[1].y);
         l = l * alpha + ps;
         if (__any_sync(0xffffffffu, rescale) && j >= 1) {  // warp-collective TMEM access
 #pragma unroll
@@ -488,11 +503,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
-template <int D>
+template <int D, int PP>
 static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const void *tmv,
                                      const TileItem *items, int n, int max_ctas, cudaStream_t s) {
   const size_t smem = 2 * (size_t)tc2::M * D * 2 + 4 * (size_t)tc2::N * D * 2 + 1024;
-  auto kern = tile_tc2_kernel<D>;
+  auto kern = tile_tc2_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
@@ -510,8 +525,20 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tmv,
                             const TileItem *items, int n, int max_ctas, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  if (p.d == 128) return launch_tile_tc2_t<128>(p, tmk, tmv, items, n, max_ctas, s);
-  return launch_tile_tc2_t<64>(p, tmk, tmv, items, n, max_ctas, s);
+  // KVA_POLY: column pairs (of 16) with exp2 on the FMA pipe: 0 (default), 4 or 6.  Measured
+  // (profiles/poly.sh): 0 is fastest — this softmax is issue/latency-bound, not MUFU-bound
+  // (llama7b tile 102 / 109 / 116 us, llama70b 962 / 887 / 856 TFLOP/s for 0 / 4 / 6).
+  static const int pp = [] {
+    const char *e = getenv("KVA_POLY");
+    return e ? atoi(e) : 0;
+  }();
+  if (p.d == 128) {
+    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, n, max_ctas, s);
+    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, n, max_ctas, s);
+    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, n, max_ctas, s);
+  }
+  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, n, max_ctas, s);
+  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, n, max_ctas, s);
 }
 
 }  // namespace kva

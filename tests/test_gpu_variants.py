@@ -2,7 +2,8 @@
 process (the implementation is chosen once per process from KVA_TILE_IMPL / KVA_OVERLAP /
 KVA_TILE_CTAS): legacy mma.sync (64-row tiles), tcgen05 one-Q-tile, tcgen05 two-Q-tile
 (default), tcgen05 CTA-pair (cta_group::2), and overlapped vs sequential scheduling; the two
-decode kernels (v1: rows along M, v2: keys along M) and v2's two occupancy configurations."""
+decode kernels (v1: rows along M, v2: keys along M) and v2's two occupancy configurations; the
+tile kernel's exp2 split between MUFU and the FMA-pipe polynomial (KVA_POLY pairs of 16)."""
 import os
 import subprocess
 import sys
@@ -54,6 +55,7 @@ def test_overlap_modes_bitexact(tmp_path):
         assert np.array_equal(np.load(a + f"_{d}.npy"), np.load(b + f"_{d}.npy"))
 
 
-@pytest.mark.parametrize("env", [{"KVA_DECODE_IMPL": "v1"}, {"KVA_DECODE_CFG": "1"}])
+@pytest.mark.parametrize("env", [{"KVA_DECODE_IMPL": "v1"}, {"KVA_DECODE_CFG": "1"},
+                                 {"KVA_POLY": "0"}, {"KVA_POLY": "4"}])
 def test_decode_impl_parity(env, tmp_path):
     _run(env, "dec_" + "_".join(env.values()), tmp_path)
