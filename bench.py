@@ -25,6 +25,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+WORKLOAD_NAMES = {"llama7b": "llama7b (BASELINE.json configs[1])", "tiny": "tiny (BASELINE.json configs[0])",
+                  "qwen14b": "qwen14b (BASELINE.json configs[2])", "llama70b": "llama70b (BASELINE.json configs[4])",
+                  "qwen14b-p": "qwen14b-p (configs[2] variant: shared-prefix prefill, SURVEY NEXT-4)"}
 METRIC = "mixed-batch attention tokens/s and HBM GB/s (% of B200 roofline) at 1/2/4/8 GPUs"
 UNIT = "tokens/s"
 
@@ -132,14 +135,25 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel="decode_kernel"):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def measured_tensor_peak():
+    """dense bf16 TFLOP/s: the SUSTAINED figure (the tile kernel is timed inside a long step)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if "bf16_tflops_sustained" in d:
+            return d["bf16_tflops_sustained"], "measured (MEASURED_PEAKS.json bf16_tflops_sustained, cuBLAS 8192^3)"
+    return 1440.6, "fallback (B200_PROFILING.md sustained bf16)"
+
+
+def ncu_traffic(config, kernel):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary
+    (profiles/ncu_summary.json, written by profiles/ncu_summarize.py; keyed config -> kernel)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -402,7 +416,7 @@ def run_ours(args, rank, world, local):
         "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE.json configs[1])" if args.config == "llama7b" else args.config,
+        "config": {"workload": WORKLOAD_NAMES.get(args.config, args.config),
                    "q_tokens": tokens, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "head_dim": cfg.d,
                    "requests": len(cfg.reqs), "parallelism": f"kv-head shard x{world}",
                    "kv_bytes_algorithmic_per_rank": stats["kv_bytes_algorithmic"],
@@ -415,11 +429,22 @@ def run_ours(args, rank, world, local):
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
                    "overlap": "tile (tcgen05) on a side stream concurrent with decode; eviction selection on a third stream concurrent with the attention"},
-        "roofline": {"bound": "hbm", "kernel": "decode_kernel (split-KV)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "decode_kt_kernel (split-KV)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(), "bytes_per_launch": dec_bytes, "peak_source": peak_src},
+                     "traffic": ncu_traffic(args.config, "decode_kt_kernel"), "bytes_per_launch": dec_bytes,
+                     "peak_source": peak_src},
         "clocks": ck, "gpu_launches": gpu_launches,
     }
+    tile_avg = statistics.mean(tile_ms) if tile_ms else 0.0
+    if tile_avg > (dec_avg if dec_ms else 0.0):
+        # tensor-bound batch (long prefill chunks): the dominant kernel is the tcgen05 tile kernel
+        tp, tp_src = measured_tensor_peak()
+        ach = stats["tile_flops"] / (tile_avg * 1e-3) / 1e12
+        res["roofline"] = {"bound": "tensor", "kernel": "tile_tc2_kernel (tcgen05)", "achieved": ach,
+                           "peak": tp, "unit": "TFLOP/s", "frac": ach / tp,
+                           "traffic": ncu_traffic(args.config, "tile_tc2_kernel"),
+                           "flops_per_launch": stats["tile_flops"], "peak_source": tp_src,
+                           "decode_hbm": {"achieved_GBps": achieved, "frac": achieved / peak}}
     if dec_alone:
         a = dec_bytes / (dec_alone * 1e-3) / 1e9
         res["config"]["decode_kernel_standalone"] = {"ms": dec_alone, "GBps": a, "frac_of_peak": a / peak,

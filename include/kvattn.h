@@ -243,6 +243,12 @@ kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out
                         int64_t *n_selected, int32_t apply, kva_pool *pool, void *workspace,
                         size_t workspace_bytes, kva_stream_t stream);
 
+/* ---- diagnostics (not part of the hot path) ----
+ * kva_diag_occupy: enqueue n_ctas CTAs that each hold smem_bytes of shared memory and spin
+ * for ns nanoseconds on `stream`; a kernel launched right after on another stream then runs on
+ * the remaining SMs (profiles/decode_sm_curve.py: decode bandwidth vs SM count). */
+kva_status kva_diag_occupy(int32_t n_ctas, int32_t smem_bytes, int64_t ns, kva_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

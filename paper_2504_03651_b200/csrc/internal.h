@@ -93,8 +93,16 @@ cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tma
                         const TileItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
+// Tile items of the tcgen05 kernel: kernel parameter when n <= kInlineTiles (no upload, so the
+// tile kernel is not ordered behind a host->device copy and claims its SMs first), else uploaded.
+constexpr int kInlineTiles = 560;
+struct TileList {
+  int32_t n;
+  const TileItem *ptr;
+  TileItem item[kInlineTiles];
+};
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
+                            const TileList &items, int max_ctas, cudaStream_t s);
 cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);

@@ -2,6 +2,7 @@
 // coalesced KV-append block scatter (a2).
 #include <math_constants.h>
 
+#include "kvattn.h"
 #include "common.cuh"
 #include "internal.h"
 
@@ -187,3 +188,28 @@ cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t 
 }
 
 }  // namespace kva
+
+// ------------------------------------------------------------------------------------------
+// Diagnostics only (kva_diag_occupy): n_ctas CTAs that each hold `smem` bytes of shared
+// memory and spin for `ns` nanoseconds, so a kernel launched next on another stream runs on
+// the remaining SMs (measures a kernel's throughput as a function of the SMs it gets).
+namespace kva {
+__global__ void diag_occupy_kernel(unsigned long long ns) {
+  extern __shared__ uint8_t sm_pad[];
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (threadIdx.x == 0) sm_pad[0] = 0;
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+}  // namespace kva
+
+extern "C" kva_status kva_diag_occupy(int32_t n_ctas, int32_t smem_bytes, int64_t ns, kva_stream_t stream) {
+  if (n_ctas <= 0) return KVA_OK;
+  if (cudaFuncSetAttribute(kva::diag_occupy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
+    return KVA_ERR_CUDA;
+  kva::diag_occupy_kernel<<<n_ctas, 32, smem_bytes, reinterpret_cast<cudaStream_t>(stream)>>>((unsigned long long)ns);
+  return cudaGetLastError() == cudaSuccess ? KVA_OK : KVA_ERR_CUDA;
+}

@@ -138,8 +138,9 @@ __device__ __forceinline__ ItemGeom geom(const TileItem &it, int g) {
 template <int D, int PP>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     tile_tc2_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv, const TileItem *__restrict__ items,
-                    int n_items) {
+                    const __grid_constant__ CUtensorMap tmv, const __grid_constant__ TileList L) {
+  const TileItem *items = L.ptr ? L.ptr : L.item;
+  const int n_items = L.n;
   using namespace tc2;
   constexpr int HALVES = D / 64;
   constexpr int KBYTES = 16 * D * 2;  // one paged block, one head (K or V)
@@ -505,7 +506,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
 
 template <int D, int PP>
 static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const void *tmv,
-                                     const TileItem *items, int n, int max_ctas, cudaStream_t s) {
+                                     const TileList &L, int max_ctas, cudaStream_t s) {
+  const int n = L.n;
   const size_t smem = 2 * (size_t)tc2::M * D * 2 + 4 * (size_t)tc2::N * D * 2 + 1024;
   auto kern = tile_tc2_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -518,13 +520,13 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::max(1, std::min(n, max_ctas > 0 ? max_ctas : nsm));
   kern<<<grid, tc2::THREADS, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
-                                        *reinterpret_cast<const CUtensorMap *>(tmv), items, n);
+                                        *reinterpret_cast<const CUtensorMap *>(tmv), L);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tmv,
-                            const TileItem *items, int n, int max_ctas, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
+                            const TileList &items, int max_ctas, cudaStream_t s) {
+  if (items.n <= 0) return cudaSuccess;
   // KVA_POLY: column pairs (of 16) with exp2 on the FMA pipe: 0 (default), 4 or 6.  Measured
   // (profiles/poly.sh): 0 is fastest — this softmax is issue/latency-bound, not MUFU-bound
   // (llama7b tile 102 / 109 / 116 us, llama70b 962 / 887 / 856 TFLOP/s for 0 / 4 / 6).
@@ -533,12 +535,12 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tm
     return e ? atoi(e) : 0;
   }();
   if (p.d == 128) {
-    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, n, max_ctas, s);
-    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, n, max_ctas, s);
-    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, n, max_ctas, s);
+    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, max_ctas, s);
+    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, max_ctas, s);
+    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, max_ctas, s);
   }
-  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, n, max_ctas, s);
-  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, n, max_ctas, s);
+  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, max_ctas, s);
+  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, max_ctas, s);
 }
 
 }  // namespace kva

@@ -509,6 +509,7 @@ struct kva_plan {
   ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
   ReqList<MergeReq> mrg;                   // merged requests (idem)
   const TileItem *d_tile = nullptr;
+  TileList tiles;                          // tcgen05 tile items (inline kernel parameter or uploaded)
   int n_dec = 0, n_tile = 0, n_mrows = 0;  // work units: decode (split, head), tiles, merge (row, head)
   // the plan arrays are uploaded on the pool's side stream (ordered after `stream`'s prior work
   // by ev_up0); a kernel that reads uploaded arrays on `stream` first waits ev_up1
@@ -769,7 +770,12 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     std::copy(pb.mrg.begin(), pb.mrg.end(), pl->mrg.req);
     std::copy(pb.mrg_pre.begin(), pb.mrg_pre.end(), pl->mrg.pre);
   }
-  const bool need_upload = !pb.tile.empty() || !dec_inline || !mrg_inline;
+  const int impl = tile_impl_for(b);
+  const bool tile_inline = impl == 2 && pb.tile.size() <= (size_t)kInlineTiles;
+  pl->tiles.n = (int32_t)pb.tile.size();
+  pl->tiles.ptr = nullptr;
+  if (tile_inline) std::copy(pb.tile.begin(), pb.tile.end(), pl->tiles.item);
+  const bool need_upload = (!pb.tile.empty() && !tile_inline) || !pb.row_list.empty() || !dec_inline || !mrg_inline;
   if (need_upload) {
     Staging::Slot *slot = nullptr;
     cudaError_t e = p->staging.get(arrays, &slot);
@@ -785,7 +791,8 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       off += align256(std::max<size_t>(n, 4));
       return dws + o;
     };
-    pl->d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), sizeof(TileItem) * pb.tile.size()));
+    pl->d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), tile_inline ? 0 : sizeof(TileItem) * pb.tile.size()));
+    if (!tile_inline) pl->tiles.ptr = pl->d_tile;
     pl->p.row_list = reinterpret_cast<const int32_t *>(put(pb.row_list.data(), 4 * pb.row_list.size()));
     if (!dec_inline) {
       pl->dec.ptr = reinterpret_cast<const DecodeReq *>(put(pb.dec.data(), sizeof(DecodeReq) * pb.dec.size()));
@@ -933,7 +940,7 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
     if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
-    else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
+    else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles,
                                                           fork ? pl->tile_ctas : 0, ts));
     else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                   fork ? pl->tile_ctas : 0, ts));
@@ -943,6 +950,9 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   };
   auto run_decode = [&]() -> kva_status {
     if (wait_upload(pl->dec.ptr != nullptr) != KVA_OK) return KVA_ERR_CUDA;
+    // overlapped: the decode kernel also waits for the side-stream append, so it does not
+    // become ready before the tile kernel (launched first, high priority) and fill every SM
+    if (fork && wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
     CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));

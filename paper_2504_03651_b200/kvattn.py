@@ -60,7 +60,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
-           "evict_select_workspace_size", "evict_select"]
+           "evict_select_workspace_size", "evict_select", "kva_diag_occupy"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
 
 _lib = None
@@ -105,6 +105,7 @@ def load(build_if_missing: bool = True):
         "evict_keys": ([P, P, P, P, i64, P, P], ctypes.c_int),
         "evict_select_workspace_size": ([i64, i64, P], ctypes.c_int),
         "evict_select": ([P, i64, i64, P, P, i32, P, P, sz, P], ctypes.c_int),
+        "kva_diag_occupy": ([i32, i32, i64, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -373,3 +374,8 @@ def evict_select(keys: torch.Tensor, k: int, out_ids: torch.Tensor | None = None
 def free_bits_tensor(free_bits_np: np.ndarray, device) -> torch.Tensor:
     """uint32 numpy bitmap -> int32 device tensor with the same bits."""
     return torch.from_numpy(np.ascontiguousarray(free_bits_np, np.uint32).view(np.int32).copy()).to(device)
+
+
+def diag_occupy(n_ctas: int, smem_bytes: int, ns: int, stream=None):
+    """Diagnostics: hold n_ctas SMs (smem_bytes each) for ns nanoseconds on `stream`."""
+    _check(load().kva_diag_occupy(n_ctas, smem_bytes, ns, _stream(stream)))

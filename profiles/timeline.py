@@ -26,7 +26,7 @@ def main():
         if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0:
             evs.append((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)))
     evs.sort()
-    mine = [x for x in evs if any(k in x[2] for k in ("kva::", "decode_kernel", "tile_", "merge_kernel",
+    mine = [x for x in evs if any(k in x[2] for k in ("kva::", "decode_", "tile_", "merge_kernel",
                                                       "append_kernel", "alloc_write", "evict_", "release_ids",
                                                       "Memcpy", "Memset", "elementwise", "copy"))]
     # last step = kernels after the last append_kernel's preceding evict_keys

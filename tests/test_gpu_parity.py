@@ -211,7 +211,20 @@ def test_d64_chunks_and_cascade():
     assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
 
 
-@pytest.mark.parametrize("name", ["llama7b", "qwen14b", "llama70b"])
+def test_shared_prefix_prefill_members():
+    """NEXT-4 (qwen14b variant 3b, scaled down): many offline tasks PREFILL private suffixes
+    of ragged lengths under one shared prefix (GQA g=5), next to online decodes."""
+    rng = np.random.default_rng(47)
+    reqs = [W.ReqSpec(W.ONLINE_DECODE, 700, 1) for _ in range(3)]
+    reqs += [W.ReqSpec(W.OFFLINE_PREFILL, 32 * 16 + int(s), int(s), 0) for s in rng.integers(1, 90, 24)]
+    wl = W.make_workload(W.custom_config("qp", 10, 2, 128, 47, reqs, [32]))
+    gg = gpu_step(wl)
+    r = oracle_step(wl)
+    _check_append(gg, r)
+    assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
+
+
+@pytest.mark.parametrize("name", ["llama7b", "qwen14b", "llama70b", "qwen14b-p"])
 def test_full_size_sampled(name):
     """BASELINE configs at full size, in the bench's launch configuration; sampled rows."""
     wl = W.make_workload(name, device="cuda")

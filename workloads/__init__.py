@@ -80,6 +80,18 @@ def _cfg_qwen14b(shared=True):
                   [128] if shared else [])
 
 
+def _cfg_qwen14b_prefill(shared=True):
+    # SURVEY §8(f) NEXT-4, variant 3b of BASELINE config 3: the same 256 offline tasks, each
+    # PREFILLING its private suffix U{32..256} (q_len = suffix) under the shared 2k prompt
+    # prefix (Table 1: a shared document, private question), + 32 online decodes.
+    # The cascade part is tensor-bound here (every member's suffix rows x the 2k prefix).
+    suffix = torch.randint(32, 257, (256,), generator=torch.Generator("cpu").manual_seed(2))
+    reqs = [ReqSpec(ONLINE_DECODE, 2048, 1) for _ in range(32)]
+    reqs += [ReqSpec(OFFLINE_PREFILL, 2048 + int(s), int(s), 0 if shared else -1) for s in suffix]
+    return Config("qwen14b-p" if shared else "qwen14b-pu", 40, 8, 128, 2, reqs,
+                  [128] if shared else [])
+
+
 def _cfg_llama70b():
     # BASELINE config 5: 64/8 x d128; 32 online decodes ctx 32k + 2 offline 8k chunks at
     # [8192, 16384) sharing an 8k prefix (reading #29).
@@ -95,6 +107,8 @@ CONFIGS = {
     "qwen14b": lambda: _cfg_qwen14b(True),
     "qwen14b-u": lambda: _cfg_qwen14b(False),
     "llama70b": _cfg_llama70b,
+    "qwen14b-p": lambda: _cfg_qwen14b_prefill(True),
+    "qwen14b-pu": lambda: _cfg_qwen14b_prefill(False),
 }
 
 
