@@ -61,10 +61,15 @@ def _load():
                                                 dbl, P, P, P, P, P, i64, P, P, ctypes.c_int]
             _lib.orc_kv_append.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, i32,
                                            P, P, P, P, P, P]
+            _lib.orc_kv_append_t.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, i32,
+                                             P, P, P, P, P, P, P, i64, i64]
+            _lib.orc_manager_step.argtypes = [P, P, P, P, i64, ctypes.c_uint32, i32, P, P, P,
+                                              i32, P, P, P, P]
             _lib.orc_evict_keys.argtypes = [P, P, P, P, i64, P]
             _lib.orc_evict_select.argtypes = [P, i64, i64, P, P]
             _lib.orc_validate.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32]
-            for f in ("orc_attention", "orc_attention_rows", "orc_kv_append",
+            for f in ("orc_attention", "orc_attention_rows", "orc_kv_append", "orc_kv_append_t",
+                      "orc_manager_step",
                       "orc_evict_keys", "orc_evict_select", "orc_validate"):
                 getattr(_lib, f).restype = ctypes.c_int
     return _lib
@@ -143,13 +148,29 @@ def attention_rows(b: dict, k_pool, v_pool, q, rows, heads, nthreads: int = 0):
     return st, out, lse
 
 
-def kv_append(b: dict, k_pool, v_pool, free_bits, k_new, v_new):
-    """KV append + smallest-free-id allocation (Eq.(5)).
+def kv_append(b: dict, k_pool, v_pool, free_bits, k_new, v_new, active_blocks=0, threshold_blocks=-1):
+    """KV append + smallest-free-id allocation (Eq.(5)), with the
+    optional burst-reserve threshold (offline allocations may not push
+    the active classes over threshold_blocks, online ones may use the reserve).
 
     Works on copies; returns (status, deficit, k_pool', v_pool', block_table', free_bits')
     with the pools as uint16 bit arrays.
     """
     lib = _load()
+    if threshold_blocks >= 0:
+        R, qi, ctx, bt, gof, gpb = _batch_args(b)
+        bt = bt.copy()
+        Hkv, d = b["num_kv_heads"], b["head_dim"]
+        kp, vp = _bits16(k_pool).copy(), _bits16(v_pool).copy()
+        fb = _c(free_bits, np.uint32).copy()
+        kn, vn = _bits16(k_new), _bits16(v_new)
+        rt = _c(b["req_type"], np.int32)
+        deficit = np.zeros(1, np.int32)
+        st = lib.orc_kv_append_t(R, Hkv, d, _p(qi), _p(ctx), _p(bt), bt.shape[1], _p(gof),
+                                 len(gpb) if gpb is not None else 0, _p(gpb), b["num_blocks"],
+                                 _p(kp), _p(vp), _p(fb), _p(kn), _p(vn), _p(deficit), _p(rt),
+                                 int(active_blocks), int(threshold_blocks))
+        return st, int(deficit[0]), kp, vp, bt, fb
     R, qi, ctx, bt, gof, gpb = _batch_args(b)
     bt = bt.copy()
     Hkv, d = b["num_kv_heads"], b["head_dim"]
@@ -174,6 +195,34 @@ def evict_keys(state, rc, lat, depth=None):
     keys = np.zeros(n, np.uint64)
     s = lib.orc_evict_keys(_p(st_), _p(rc_), _p(lat_), _p(dep), n, _p(keys))
     return s, keys
+
+
+def manager_step(state, rc, lat, depth, now, chains, pool):
+    """The KV manager's per-iteration metadata pass:
+    class transitions (chains = [(state, ids), ...], in order, lat = now), rc recount from the
+    offline pool's chains (pool = [ids, ...]), active-class count, eviction keys.
+    Works on copies; returns (status, state', rc', lat', keys, n_active)."""
+    lib = _load()
+    st_ = _c(state, np.uint8).copy()
+    rc_ = np.zeros(len(st_), np.uint32)
+    lat_ = _c(lat, np.uint32).copy()
+    dep = _c(depth, np.uint16)
+    ci = np.zeros(len(chains) + 1, np.int32)
+    for j, (_, ids) in enumerate(chains):
+        ci[j + 1] = ci[j] + len(ids)
+    cids = np.concatenate([np.asarray(ids, np.int32) for _, ids in chains]) if chains else np.zeros(0, np.int32)
+    cst = np.array([s_ for s_, _ in chains], np.uint8)
+    pi = np.zeros(len(pool) + 1, np.int32)
+    for j, ids in enumerate(pool):
+        pi[j + 1] = pi[j] + len(ids)
+    pids = np.concatenate([np.asarray(ids, np.int32) for ids in pool]) if pool else np.zeros(0, np.int32)
+    n = len(st_)
+    keys = np.zeros(n, np.uint64)
+    nact = np.zeros(1, np.int64)
+    s = lib.orc_manager_step(_p(st_), _p(rc_), _p(lat_), _p(dep), n, int(now) & 0xFFFFFFFF,
+                             len(chains), _p(ci), _p(cids), _p(cst), len(pool), _p(pi), _p(pids),
+                             _p(keys), _p(nact))
+    return s, st_, rc_, lat_, keys, int(nact[0])
 
 
 def evict_select(keys, k: int):

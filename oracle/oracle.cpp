@@ -229,6 +229,15 @@ int orc_attention_rows(int32_t num_reqs, int32_t Hq, int32_t Hkv, int32_t d,
  * is returned and nothing changes ("on NeedsEviction, state
  * unchanged").  k_new/v_new: [total_q][Hkv][d]; free_bits: bit b of word
  * b/32 set = block b free. */
+int orc_kv_append_t(int32_t num_reqs, int32_t Hkv, int32_t d,
+                    const int32_t *q_indptr, const int32_t *ctx_len,
+                    int32_t *block_table, int32_t max_blocks,
+                    const int32_t *group_of, int32_t num_groups,
+                    const int32_t *group_prefix_blocks, int32_t num_blocks,
+                    uint16_t *k_pool, uint16_t *v_pool, uint32_t *free_bits,
+                    const uint16_t *k_new, const uint16_t *v_new, int32_t *deficit,
+                    const int32_t *req_type, int64_t active_blocks, int64_t threshold_blocks);
+
 int orc_kv_append(int32_t num_reqs, int32_t Hkv, int32_t d,
                   const int32_t *q_indptr, const int32_t *ctx_len,
                   int32_t *block_table, int32_t max_blocks,
@@ -236,6 +245,30 @@ int orc_kv_append(int32_t num_reqs, int32_t Hkv, int32_t d,
                   const int32_t *group_prefix_blocks, int32_t num_blocks,
                   uint16_t *k_pool, uint16_t *v_pool, uint32_t *free_bits,
                   const uint16_t *k_new, const uint16_t *v_new, int32_t *deficit) {
+  return orc_kv_append_t(num_reqs, Hkv, d, q_indptr, ctx_len, block_table, max_blocks, group_of,
+                         num_groups, group_prefix_blocks, num_blocks, k_pool, v_pool, free_bits,
+                         k_new, v_new, deficit, nullptr, 0, -1);
+}
+
+/* kv_append with the burst-reserve threshold ("set a threshold to limit the KV
+ * cache size for running online tasks and active offline tasks while leaving sufficient space
+ * for future bursty online tasks"; "allocation fails with NeedsEviction if it would
+ * push active-class tokens over threshold_tokens, even when free capacity exists ... incoming
+ * online allocations may use the reserve, offline may not").  req_type[i] in {0 online decode,
+ * 1 offline prefill, 2 offline decode, 3 online prefill}; active_blocks = blocks of the
+ * active classes before this step (the manager step's count); threshold_blocks < 0 = no
+ * threshold.  Checks, in order: capacity (need > free -> NEEDS_EVICTION, deficit = need -
+ * free); then, if any OFFLINE request needs a block: active + need > threshold ->
+ * NEEDS_EVICTION with deficit = active + need - threshold (reading R35).  Nothing changes on
+ * any error. */
+int orc_kv_append_t(int32_t num_reqs, int32_t Hkv, int32_t d,
+                    const int32_t *q_indptr, const int32_t *ctx_len,
+                    int32_t *block_table, int32_t max_blocks,
+                    const int32_t *group_of, int32_t num_groups,
+                    const int32_t *group_prefix_blocks, int32_t num_blocks,
+                    uint16_t *k_pool, uint16_t *v_pool, uint32_t *free_bits,
+                    const uint16_t *k_new, const uint16_t *v_new, int32_t *deficit,
+                    const int32_t *req_type, int64_t active_blocks, int64_t threshold_blocks) {
   Batch b = make_batch(num_reqs, Hkv, Hkv, d, q_indptr, ctx_len, block_table, max_blocks,
                        group_of, num_groups, group_prefix_blocks, num_blocks, 0.0);
   if (deficit) *deficit = 0;
@@ -243,8 +276,9 @@ int orc_kv_append(int32_t num_reqs, int32_t Hkv, int32_t d,
   if (st != ST_OK) return st;
   /* resident positions [0, ctx-q_len) must be allocated; new-position
    * entries must be -1 or a valid id */
-  int64_t need = 0;
+  int64_t need = 0, need_offline = 0;
   for (int i = 0; i < num_reqs; ++i) {
+    const int64_t need_before = need;
     int ctx = ctx_len[i], start = ctx - q_len_of(b, i);
     if ((ctx + BLOCK - 1) / BLOCK > num_blocks) return ST_CAPACITY;
     for (int blk = 0; blk < (start + BLOCK - 1) / BLOCK; ++blk) {
@@ -261,11 +295,16 @@ int orc_kv_append(int32_t num_reqs, int32_t Hkv, int32_t d,
         return ST_INVALID;
       }
     }
+    if (req_type && (req_type[i] == 1 || req_type[i] == 2)) need_offline += need - need_before;
   }
   int64_t free_count = 0;
   for (int blk = 0; blk < num_blocks; ++blk) free_count += (free_bits[blk / 32] >> (blk % 32)) & 1u;
   if (need > free_count) {
     if (deficit) *deficit = (int32_t)(need - free_count);
+    return ST_NEEDS_EVICTION;
+  }
+  if (threshold_blocks >= 0 && need_offline > 0 && active_blocks + need > threshold_blocks) {
+    if (deficit) *deficit = (int32_t)(active_blocks + need - threshold_blocks);
     return ST_NEEDS_EVICTION;
   }
   int scan = 0; /* smallest free id is found by a forward scan */
@@ -326,6 +365,59 @@ int orc_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat
 /* Eviction order ("first consider the priority ... then the last
  * access time"; P:440 free table = priority queue; tie-break by block id
  * S:200): sort evictable blocks by (key, id) ascending, take the first k. */
+/* The KV manager's per-iteration metadata pass (§4.2):
+ *  1. class transitions (S:161-168 release_request; reading #17 pins): for chain j in list
+ *     order, every block id of chain_ids[chain_indptr[j] .. chain_indptr[j+1]) gets
+ *     state = chain_state[j] and lat = now (a later chain overrides an earlier one);
+ *  2. reference recount (S:154-160 update_references; "how many offline requests
+ *     (including current running request) will reuse it"): rc[b] = number of offline-pool
+ *     chains p that list b (pool_ids[pool_indptr[p] .. pool_indptr[p+1]));
+ *  3. *n_active = blocks of the active classes ("tokens held by {RunningOnline,
+ *     ActiveOffline}"): running online or pinned, or rc > 0 in any resident class
+ *     (S:119 a finished block with rc > 0 is classed ActiveOffline; reading #15);
+ *  4. keys = orc_evict_keys(state, rc, lat, depth).
+ * Validation first (ids in [0, n), states <= 5, monotone indptr); INVALID = nothing changed. */
+int orc_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth, int64_t n,
+                     uint32_t now, int32_t n_chains, const int32_t *chain_indptr,
+                     const int32_t *chain_ids, const uint8_t *chain_state, int32_t n_pool,
+                     const int32_t *pool_indptr, const int32_t *pool_ids, uint64_t *keys,
+                     int64_t *n_active) {
+  if (n_chains < 0 || n_pool < 0) return ST_INVALID;
+  if (n_chains > 0 && chain_indptr[0] != 0) return ST_INVALID;
+  for (int32_t j = 0; j < n_chains; ++j) {
+    if (chain_indptr[j + 1] < chain_indptr[j] || chain_state[j] > BS_FINISHED_OFFLINE) return ST_INVALID;
+    for (int32_t e = chain_indptr[j]; e < chain_indptr[j + 1]; ++e)
+      if (chain_ids[e] < 0 || chain_ids[e] >= n) return ST_INVALID;
+  }
+  if (n_pool > 0 && pool_indptr[0] != 0) return ST_INVALID;
+  for (int32_t p = 0; p < n_pool; ++p) {
+    if (pool_indptr[p + 1] < pool_indptr[p]) return ST_INVALID;
+    for (int32_t e = pool_indptr[p]; e < pool_indptr[p + 1]; ++e)
+      if (pool_ids[e] < 0 || pool_ids[e] >= n) return ST_INVALID;
+  }
+  for (int64_t b = 0; b < n; ++b)
+    if (state[b] > BS_FINISHED_OFFLINE) return ST_INVALID;
+  /* 1 */
+  for (int32_t j = 0; j < n_chains; ++j)
+    for (int32_t e = chain_indptr[j]; e < chain_indptr[j + 1]; ++e) {
+      state[chain_ids[e]] = chain_state[j];
+      lat[chain_ids[e]] = now;
+    }
+  /* 2 */
+  for (int64_t b = 0; b < n; ++b) rc[b] = 0;
+  for (int32_t p = 0; p < n_pool; ++p)
+    for (int32_t e = pool_indptr[p]; e < pool_indptr[p + 1]; ++e) rc[pool_ids[e]] += 1;
+  /* 3 */
+  int64_t act = 0;
+  for (int64_t b = 0; b < n; ++b) {
+    if (state[b] == BS_FREE) continue;
+    if (state[b] == BS_RUNNING_ONLINE || state[b] == BS_PINNED || rc[b] > 0) ++act;
+  }
+  if (n_active) *n_active = act;
+  /* 4 */
+  return orc_evict_keys(state, rc, lat, depth, n, keys);
+}
+
 int orc_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                      int64_t *n_selected) {
   if (n < 0 || k < 0) return ST_INVALID;

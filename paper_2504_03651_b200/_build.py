@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         if (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(src)
                 and os.path.getmtime(obj) >= hdr_t):
             return obj
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("KVA_NVCC_DEFS", "").split(), "-c", src, "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

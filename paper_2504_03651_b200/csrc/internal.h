@@ -88,7 +88,7 @@ struct AttnParams {
 
 // launchers (kernels_*.cu)
 cudaError_t launch_decode(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                          const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s);
+                          const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s, bool pdl = false);
 cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                         const TileItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,

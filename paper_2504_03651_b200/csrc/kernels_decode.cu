@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(128, MINB)
 
 template <int D, int NR, int NST, int MINB>
 static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const void *tmv,
-                                   const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
+                                   const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;
   auto kern = decode_kt_kernel<D, NR, NST, MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -602,8 +602,23 @@ static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const 
   if (e != cudaSuccess) return e;
   const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
   const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
-  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, L, n);
-  return cudaGetLastError();
+  if (!pdl) {
+    kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, L, n);
+    return cudaGetLastError();
+  }
+  // dependent launch: may start while the preceding tile kernel runs (after all its CTAs are
+  // resident, griddepcontrol.launch_dependents); no data dependency between the two
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n + 3) / 4);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, mk, mv, L, n);
 }
 
 template <int D, int NST, int PF>
@@ -623,7 +638,7 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
 }
 
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
-                          const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
+                          const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl) {
   if (n <= 0) return cudaSuccess;
   // KVA_DECODE_IMPL=v1: the M = rows kernel (cross-check); default v2 (keys along M).
   // KVA_DECODE_CFG: 0 = 3 stages x 2 CTAs/SM (default), 1 = 2 stages x 3 CTAs/SM.
@@ -644,13 +659,13 @@ cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
       max_rows = kDecodeRows;
     const bool nr1 = max_rows <= 8;
     if (p.d == 128) {
-      if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s)
-                               : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s);
-      return nr1 ? launch_decode_kt<128, 1, 3, 2>(p, tmk, tmv, L, n, s)
-                 : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s);
+      if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s, pdl)
+                               : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s, pdl);
+      return nr1 ? launch_decode_kt<128, 1, 3, 2>(p, tmk, tmv, L, n, s, pdl)
+                 : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s, pdl);
     }
-    return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s)
-               : launch_decode_kt<64, 2, 4, 2>(p, tmk, tmv, L, n, s);
+    return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s, pdl)
+               : launch_decode_kt<64, 2, 4, 2>(p, tmk, tmv, L, n, s, pdl);
   }
   static const int pf = [] {
     const char *e = getenv("KVA_DECODE_PF");

@@ -195,6 +195,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base_s;
+  // programmatic dependent launch: once every CTA of this persistent grid is resident, the
+  // next kernel on the stream (the decode kernel, launched with the PDL attribute) may start
+  // on the remaining SMs — the tile kernel claims its SMs first (it reads nothing the
+  // dependent writes, and the dependent reads nothing this kernel writes)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------

@@ -840,11 +840,11 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       pl->overlap = false;
       pl->tile_ctas = nsm;
     } else {
-      // split the SMs: proportional to the standalone times, skewed 1.2x towards the tile
-      // kernel because the decode stream keeps HBM nearly saturated with fewer SMs than its
-      // standalone share (measured optimum on llama7b: 44 of 148 with the eviction selection
-      // co-running on 74); >= 1/4 of the SMs each
-      const double f = 1.2 * t_tile / (t_tile + t_dec);
+      // split the SMs: proportional to the standalone times, skewed 1.5x towards the tile
+      // kernel because the decode stream saturates HBM on ~94-104 SMs (profiles/r01b
+      // decode_sm_curve.log: 6.8 TB/s on 104, 6.3 on 74); llama7b: 54 of 148 (step 403 us vs
+      // 420 at 44 without the eviction selection co-running, equal with it); >= 1/4 each
+      const double f = 1.5 * t_tile / (t_tile + t_dec);
       pl->tile_ctas = std::max(nsm / 4, std::min(nsm - nsm / 4, (int)(nsm * f + 0.5)));
     }
   }
@@ -958,6 +958,26 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     return KVA_OK;
   };
+  // overlapped, PDL mode (default for the tcgen05 tile kernel + decode v2): both kernels on
+  // `s`; the persistent tile kernel launches first and, once all its CTAs are resident, lets
+  // the decode kernel (programmatic dependent launch) start on the remaining SMs.  This fixes
+  // the SM split: with two streams the decode kernel's 2-CTA/SM grid could be dispatched first
+  // and hold every SM until its first wave retired.  Timing events bracket the pair.
+  static const bool pdl_mode = [] {
+    const char *e = getenv("KVA_PDL");
+    return !(e && std::string(e) == "0");
+  }();
+  if (fork && pdl_mode && pl->tile_impl == 2) {
+    if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
+    if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
+    if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
+    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s));
+    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, /*pdl=*/true));
+    if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));
+    if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
+    if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
+    return KVA_OK;
+  }
   // sequential mode: decode first (its CTAs share SMs with a concurrently running eviction
   // selection on another stream), then the tile kernel on every SM
   kva_status rs = KVA_OK;

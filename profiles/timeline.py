@@ -19,7 +19,7 @@ def main():
     import bench
     from torch.profiler import ProfilerActivity, profile
     args = bench.parse()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         bench.run_ours(args, 0, 1, 0)
     evs = []
     for e in prof.events():
@@ -35,7 +35,17 @@ def main():
     t0 = last[0][0]
     rows = [{"kernel": n.split("(")[0][-40:], "stream": s, "start_us": round(a - t0, 1),
              "end_us": round(b - t0, 1), "dur_us": round(b - a, 1)} for a, b, n, s in last]
-    for r in rows:
+    # host-side runtime API calls of the same step (when each launch was ENQUEUED)
+    t_end = last[-1][1]
+    api = []
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CPU and e.name.startswith("cuda") and \
+                t0 - 200 <= e.time_range.start <= t_end:
+            api.append({"api": e.name, "start_us": round(e.time_range.start - t0, 1),
+                        "dur_us": round(e.time_range.elapsed_us(), 1)})
+    api.sort(key=lambda r: r["start_us"])
+    rows.append({"host_api": api})
+    for r in rows[:-1]:
         print(f"{r['kernel']:42s} stream={r['stream']:<4} {r['start_us']:9.1f} -> {r['end_us']:9.1f}  ({r['dur_us']:.1f} us)")
     if out:
         json.dump(rows, open(out, "w"), indent=1)
