@@ -184,11 +184,22 @@ def run_ours(args, rank, world, local):
 
     ev = None
     if not args.no_evict:
+        # the KV manager's per-iteration pass over the `evict` config's 2^20-block metadata
+        # (BASELINE configs[3]): class transitions + rc recount from the offline pool
+        # -> keys -> top-64k selection (a8)
         evw = W.make_evict()
         t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)
         ev = dict(state=t(evw.state, np.uint8), rc=t(evw.rc, np.int32), lat=t(evw.lat, np.int32),
                   depth=t(evw.depth, np.int16), k=evw.k, n=len(evw.state))
-        ev["keys"] = torch.empty(ev["n"], dtype=torch.int64, device=dev)
+        chains, mpool = W.make_manager_update(evw, now=1 << 20, seed=1)
+        ev["mgr"] = K.ManagerStep(ev["state"], ev["rc"], ev["lat"], ev["depth"])
+        ev["chains"] = K.ManagerStep.chains_csr(chains)
+        # incremental reference counts: each iteration 1% of the offline pool's requests leave
+        # (finished) and as many new requests with the same prompts join (steady state)
+        rng_p = np.random.default_rng(11)
+        moved = [mpool[i] for i in rng_p.choice(len(mpool), len(mpool) // 100, replace=False)]
+        ev["pool_ids"] = torch.from_numpy(np.concatenate(moved).astype(np.int32)).to(dev)
+        ev["del_ids"] = ev["pool_ids"].clone()
         ev["ids"] = torch.empty(ev["k"], dtype=torch.int32, device=dev)
         ev["ws"] = torch.empty(K.evict_select_workspace_size(ev["n"], ev["k"]), dtype=torch.uint8, device=dev)
 
@@ -208,7 +219,10 @@ def run_ours(args, rank, world, local):
     tim_used = []
 
     ev_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("KVA_BENCH_EVICT_PRIO", "0")))
-    ev_fork, ev_join = torch.cuda.Event(), torch.cuda.Event()
+    ev_fork, ev_join, ev_keys = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
+    # the attention pair is launched after the manager's key pass, so the cooperative eviction
+    # selection (next on its stream) is placed on the SMs before the decode kernel fills them
+    gate_attn = os.environ.get("KVA_BENCH_GATE", "1") == "1"
 
     def step(time_idx=None):
         n = 0
@@ -217,16 +231,20 @@ def run_ours(args, rank, world, local):
             # it runs on its own stream, concurrently (its CTAs leave room for decode CTAs)
             ev_fork.record(stream)
             ev_stream.wait_event(ev_fork)
-            K.evict_keys(ev["state"], ev["rc"], ev["lat"], ev["depth"], keys=ev["keys"], stream=ev_stream)
-            K.evict_select(ev["keys"], ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
+            keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
+                             stream=ev_stream)
+            ev_keys.record(ev_stream)
+            K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
                            sync=False)
             ev_join.record(ev_stream)
-            n += 2
+            n += 3
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
         batch.table_host[...] = pristine_host
         K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
         n += 2 + plan.launch_count()
+        if ev is not None and gate_attn:
+            stream.wait_event(ev_keys)
         if time_idx is not None:
             plan.set_timing_events(*tim[time_idx])
             tim_used.append(tim[time_idx])
@@ -291,11 +309,13 @@ def run_ours(args, rank, world, local):
         if ev is not None:
             ev_fork.record(stream)
             ev_stream.wait_event(ev_fork)
-            K.evict_keys(ev["state"], ev["rc"], ev["lat"], ev["depth"], keys=ev["keys"], stream=ev_stream)
-            K.evict_select(ev["keys"], ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
+            keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
+                             stream=ev_stream)
+            ev_keys.record(ev_stream)
+            K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
                            sync=False)
             ev_join.record(ev_stream)
-            n += 2
+            n += 3
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
         batch.table_host[...] = pristine_host
         stream.wait_event(ev_in[i % 2])
@@ -304,6 +324,8 @@ def run_ours(args, rank, world, local):
         K.kv_append(pool, batch, b["k"], b["v"], ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
         n += 2 + plan.launch_count()
+        if ev is not None and gate_attn:
+            stream.wait_event(ev_keys)
         plan.run(b["q"], b["out"], lse, stream=stream)
         res_t = b["out"]
         if world > 1:
@@ -422,7 +444,7 @@ def run_ours(args, rank, world, local):
                    "kv_bytes_algorithmic_per_rank": stats["kv_bytes_algorithmic"],
                    "flops_per_rank": stats["flops"],
                    "step": "kv_append+hybrid_attention(plan,tile,decode,merge)" +
-                           ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+evict_keys+evict_select(1M,k=64k)") +
+                           ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)") +
                            "+release",
                    "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,

@@ -243,6 +243,64 @@ kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out
                         int64_t *n_selected, int32_t apply, kva_pool *pool, void *workspace,
                         size_t workspace_bytes, kva_stream_t stream);
 
+/* ---- KV-manager step (§4.2 "Priority-based KV cache
+ * eviction" / "Threshold to limit the KV cache size for active requests") ----
+ * One device pass per iteration over the pool's block metadata, feeding evict_select:
+ *   1. class transitions (S:161-168 release_request: finished online -> FINISHED_ONLINE,
+ *      finished offline -> FINISHED_OFFLINE, preempted offline -> ACTIVE_OFFLINE; reading #17:
+ *      this iteration's batch -> RUNNING_ONLINE / PINNED): chain j of the HOST CSR
+ *      (chain_indptr, chain_ids) gets state chain_state[j] and lat = now; a block listed in
+ *      several chains takes the LAST chain's state (list order);
+ *   2. reference counts (S:154-160 update_references; "how may offline requests
+ *      (including current running request) will reuse it"), DEVICE id lists (chains
+ *      concatenated; order irrelevant):
+ *        recount != 0: rc[b] = number of offline-pool chains that list b (pool_ids[0, pool_len));
+ *        recount == 0: rc[b] += #chains in pool_ids that list b (requests that joined the
+ *                      pool) - #chains in del_ids[0, del_len) that list b (requests that left);
+ *                      the caller keeps the counts consistent (a negative count is not
+ *                      detected on the device; the oracle reports it as INVALID);
+ *   3. *n_active (device int64, nullable) = blocks of the active classes: running
+ *      online / pinned, or rc > 0 in any resident class (reading #15);
+ *   4. keys_out = evict_keys(state, rc, lat, depth).
+ * Host arrays are validated before anything is enqueued (ids in [0, n), states <= 5, indptr
+ * monotone from 0 -> else KVA_ERR_INVALID, nothing changed).  Device pool ids outside [0, n)
+ * are skipped (not detected).  workspace: kv_manager_step_workspace_size() bytes of device
+ * scratch (the deduplicated transition list is uploaded there). */
+typedef struct {
+  int64_t num_blocks;
+  uint8_t *state;          /* device [n] KVA_BLK_* */
+  uint32_t *rc;            /* device [n] (rewritten by the recount) */
+  uint32_t *lat;           /* device [n] logical ticks (reading #18) */
+  const uint16_t *depth;   /* device [n] chain depth (reading #19), nullable */
+} kva_block_meta;
+typedef struct {
+  uint32_t now;
+  int32_t n_chains;
+  const int32_t *chain_indptr;  /* host [n_chains + 1] */
+  const int32_t *chain_ids;     /* host [chain_indptr[n_chains]] */
+  const uint8_t *chain_state;   /* host [n_chains] */
+  int32_t recount;              /* 1: full recount from pool_ids; 0: incremental */
+  const int32_t *pool_ids;      /* device [pool_len] */
+  int64_t pool_len;
+  const int32_t *del_ids;       /* device [del_len] (incremental mode only) */
+  int64_t del_len;
+} kva_manager_update;
+kva_status kv_manager_step_workspace_size(const kva_block_meta *meta, const kva_manager_update *u,
+                                          size_t *bytes);
+kva_status kv_manager_step(const kva_block_meta *meta, const kva_manager_update *u,
+                           uint64_t *keys_out, int64_t *n_active, void *workspace,
+                           size_t workspace_bytes, kva_stream_t stream);
+/* Burst-reserve threshold for kv_append.  threshold_blocks
+ * < 0 disables it (default); 0 <= threshold <= num_blocks else KVA_ERR_INVALID.  With a
+ * threshold, kv_append first checks capacity (KVA_NEEDS_EVICTION, deficit = need - free),
+ * then, if any OFFLINE request (KVA_OFFLINE_PREFILL / KVA_OFFLINE_DECODE) needs a new block:
+ * active + need > threshold -> KVA_NEEDS_EVICTION with *deficit = active + need - threshold,
+ * nothing changed (online requests may allocate into the reserve; reading R35).  `active` is
+ * the last value given to kv_pool_set_active_blocks (e.g. the manager step's n_active) plus
+ * the blocks allocated by kv_append since. */
+kva_status kv_pool_set_threshold(kva_pool *pool, int64_t threshold_blocks);
+kva_status kv_pool_set_active_blocks(kva_pool *pool, int64_t active_blocks);
+
 /* ---- diagnostics (not part of the hot path) ----
  * kva_diag_occupy: enqueue n_ctas CTAs that each hold smem_bytes of shared memory and spin
  * for ns nanoseconds on `stream`; a kernel launched right after on another stream then runs on

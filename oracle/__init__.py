@@ -64,7 +64,7 @@ def _load():
             _lib.orc_kv_append_t.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, i32,
                                              P, P, P, P, P, P, P, i64, i64]
             _lib.orc_manager_step.argtypes = [P, P, P, P, i64, ctypes.c_uint32, i32, P, P, P,
-                                              i32, P, P, P, P]
+                                              i32, P, P, i32, i32, P, P, P, P]
             _lib.orc_evict_keys.argtypes = [P, P, P, P, i64, P]
             _lib.orc_evict_select.argtypes = [P, i64, i64, P, P]
             _lib.orc_validate.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32]
@@ -197,14 +197,23 @@ def evict_keys(state, rc, lat, depth=None):
     return s, keys
 
 
-def manager_step(state, rc, lat, depth, now, chains, pool):
+def _csr(chains):
+    ip = np.zeros(len(chains) + 1, np.int32)
+    for j, ids in enumerate(chains):
+        ip[j + 1] = ip[j] + len(ids)
+    flat = np.concatenate([np.asarray(ids, np.int32) for ids in chains]) if chains else np.zeros(0, np.int32)
+    return ip, flat
+
+
+def manager_step(state, rc, lat, depth, now, chains, pool, delete=None, recount=True):
     """The KV manager's per-iteration metadata pass:
-    class transitions (chains = [(state, ids), ...], in order, lat = now), rc recount from the
-    offline pool's chains (pool = [ids, ...]), active-class count, eviction keys.
+    class transitions (chains = [(state, ids), ...], in order, lat = now), reference counts
+    (recount=True: rc = #pool chains listing the block; recount=False: rc += #chains of `pool`
+    (joined) - #chains of `delete` (left)), active-class count, eviction keys.
     Works on copies; returns (status, state', rc', lat', keys, n_active)."""
     lib = _load()
     st_ = _c(state, np.uint8).copy()
-    rc_ = np.zeros(len(st_), np.uint32)
+    rc_ = np.zeros(len(st_), np.uint32) if rc is None else _c(rc, np.uint32).copy()
     lat_ = _c(lat, np.uint32).copy()
     dep = _c(depth, np.uint16)
     ci = np.zeros(len(chains) + 1, np.int32)
@@ -212,16 +221,15 @@ def manager_step(state, rc, lat, depth, now, chains, pool):
         ci[j + 1] = ci[j] + len(ids)
     cids = np.concatenate([np.asarray(ids, np.int32) for _, ids in chains]) if chains else np.zeros(0, np.int32)
     cst = np.array([s_ for s_, _ in chains], np.uint8)
-    pi = np.zeros(len(pool) + 1, np.int32)
-    for j, ids in enumerate(pool):
-        pi[j + 1] = pi[j] + len(ids)
-    pids = np.concatenate([np.asarray(ids, np.int32) for ids in pool]) if pool else np.zeros(0, np.int32)
+    pi, pids = _csr(pool)
+    delete = delete or []
+    di, dids = _csr(delete)
     n = len(st_)
     keys = np.zeros(n, np.uint64)
     nact = np.zeros(1, np.int64)
     s = lib.orc_manager_step(_p(st_), _p(rc_), _p(lat_), _p(dep), n, int(now) & 0xFFFFFFFF,
                              len(chains), _p(ci), _p(cids), _p(cst), len(pool), _p(pi), _p(pids),
-                             _p(keys), _p(nact))
+                             1 if recount else 0, len(delete), _p(di), _p(dids), _p(keys), _p(nact))
     return s, st_, rc_, lat_, keys, int(nact[0])
 
 

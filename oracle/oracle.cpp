@@ -369,9 +369,13 @@ int orc_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat
  *  1. class transitions (S:161-168 release_request; reading #17 pins): for chain j in list
  *     order, every block id of chain_ids[chain_indptr[j] .. chain_indptr[j+1]) gets
  *     state = chain_state[j] and lat = now (a later chain overrides an earlier one);
- *  2. reference recount (S:154-160 update_references; "how many offline requests
- *     (including current running request) will reuse it"): rc[b] = number of offline-pool
- *     chains p that list b (pool_ids[pool_indptr[p] .. pool_indptr[p+1]));
+ *  2. reference counts (S:154-160 update_references; "how many offline requests
+ *     (including current running request) will reuse it"):
+ *     recount != 0: rc[b] = number of offline-pool chains p that list b
+ *                   (pool_ids[pool_indptr[p] .. pool_indptr[p+1]));
+ *     recount == 0 (incremental): rc[b] += #chains of pool_ids that list b (requests that
+ *                   joined the pool) - #chains of del_ids that list b (requests that left it);
+ *                   a count that would go negative -> INVALID, nothing changed;
  *  3. *n_active = blocks of the active classes ("tokens held by {RunningOnline,
  *     ActiveOffline}"): running online or pinned, or rc > 0 in any resident class
  *     (S:119 a finished block with rc > 0 is classed ActiveOffline; reading #15);
@@ -380,8 +384,9 @@ int orc_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat
 int orc_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth, int64_t n,
                      uint32_t now, int32_t n_chains, const int32_t *chain_indptr,
                      const int32_t *chain_ids, const uint8_t *chain_state, int32_t n_pool,
-                     const int32_t *pool_indptr, const int32_t *pool_ids, uint64_t *keys,
-                     int64_t *n_active) {
+                     const int32_t *pool_indptr, const int32_t *pool_ids, int32_t recount,
+                     int32_t n_del, const int32_t *del_indptr, const int32_t *del_ids,
+                     uint64_t *keys, int64_t *n_active) {
   if (n_chains < 0 || n_pool < 0) return ST_INVALID;
   if (n_chains > 0 && chain_indptr[0] != 0) return ST_INVALID;
   for (int32_t j = 0; j < n_chains; ++j) {
@@ -395,8 +400,23 @@ int orc_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t
     for (int32_t e = pool_indptr[p]; e < pool_indptr[p + 1]; ++e)
       if (pool_ids[e] < 0 || pool_ids[e] >= n) return ST_INVALID;
   }
+  if (n_del < 0 || (recount && n_del > 0)) return ST_INVALID;
+  if (n_del > 0 && del_indptr[0] != 0) return ST_INVALID;
+  for (int32_t p = 0; p < n_del; ++p) {
+    if (del_indptr[p + 1] < del_indptr[p]) return ST_INVALID;
+    for (int32_t e = del_indptr[p]; e < del_indptr[p + 1]; ++e)
+      if (del_ids[e] < 0 || del_ids[e] >= n) return ST_INVALID;
+  }
   for (int64_t b = 0; b < n; ++b)
     if (state[b] > BS_FINISHED_OFFLINE) return ST_INVALID;
+  std::vector<int64_t> rc_new(n);
+  for (int64_t b = 0; b < n; ++b) rc_new[b] = recount ? 0 : (int64_t)rc[b];
+  for (int32_t p = 0; p < n_pool; ++p)
+    for (int32_t e = pool_indptr[p]; e < pool_indptr[p + 1]; ++e) rc_new[pool_ids[e]] += 1;
+  for (int32_t p = 0; p < n_del; ++p)
+    for (int32_t e = del_indptr[p]; e < del_indptr[p + 1]; ++e) rc_new[del_ids[e]] -= 1;
+  for (int64_t b = 0; b < n; ++b)
+    if (rc_new[b] < 0 || rc_new[b] > (int64_t)UINT32_MAX) return ST_INVALID;
   /* 1 */
   for (int32_t j = 0; j < n_chains; ++j)
     for (int32_t e = chain_indptr[j]; e < chain_indptr[j + 1]; ++e) {
@@ -404,9 +424,7 @@ int orc_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t
       lat[chain_ids[e]] = now;
     }
   /* 2 */
-  for (int64_t b = 0; b < n; ++b) rc[b] = 0;
-  for (int32_t p = 0; p < n_pool; ++p)
-    for (int32_t e = pool_indptr[p]; e < pool_indptr[p + 1]; ++e) rc[pool_ids[e]] += 1;
+  for (int64_t b = 0; b < n; ++b) rc[b] = (uint32_t)rc_new[b];
   /* 3 */
   int64_t act = 0;
   for (int64_t b = 0; b < n; ++b) {

@@ -122,6 +122,12 @@ cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t 
                           const ReqList<AppendReq> &reqs, int32_t total_new_tok, cudaStream_t s);
 cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
                               const uint16_t *depth, int64_t n, uint64_t *keys, cudaStream_t s);
+cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth,
+                                int64_t n, uint32_t now, const int32_t *tr_ids, int64_t n_tr,
+                                const int32_t *tr_indptr, const uint8_t *tr_state, int32_t n_chains,
+                                int32_t *win, bool recount, const int32_t *pool_ids, int64_t pool_len,
+                                const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
+                                cudaStream_t s);
 size_t evict_select_ws_bytes(int64_t n, int64_t k);
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t s);

@@ -661,7 +661,7 @@ cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
     if (p.d == 128) {
       if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s, pdl)
                                : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s, pdl);
-      return nr1 ? launch_decode_kt<128, 1, 3, 2>(p, tmk, tmv, L, n, s, pdl)
+      return nr1 ? launch_decode_kt<128, 1, 3, 4>(p, tmk, tmv, L, n, s, pdl)
                  : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s, pdl);
     }
     return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s, pdl)

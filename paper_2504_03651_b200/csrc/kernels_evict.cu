@@ -17,6 +17,7 @@
 // Grid-wide steps are separated by cooperative-groups grid barriers (select rounds + 2 + passes).
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -55,6 +56,110 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   evict_keys_kernel<<<grid, 256, 0, s>>>(state, rc, lat, depth, n, keys);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// KV-manager step.  Transitions arrive as the caller's raw chains (host
+// validated, uploaded unchanged); "last chain wins" is resolved on the device: every listed
+// block's winner slot is reset, then takes the max element index listing it (atomicMax), and
+// only that element applies its chain's state.  Then the reference counts (recount: zeroed
+// by the host + atomicAdd; incremental: atomicAdd / atomicSub), then keys + active count.
+__global__ void manager_win_init_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr; e += (int64_t)gridDim.x * blockDim.x)
+    win[tr_ids[e]] = -1;
+}
+__global__ void manager_win_max_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr; e += (int64_t)gridDim.x * blockDim.x)
+    atomicMax(&win[tr_ids[e]], (int32_t)e);
+}
+
+__global__ void manager_apply_kernel(uint8_t *__restrict__ state, uint32_t *__restrict__ rc,
+                                     uint32_t *__restrict__ lat, int64_t n, uint32_t now,
+                                     const int32_t *__restrict__ tr_ids, int64_t n_tr,
+                                     const int32_t *__restrict__ tr_indptr, const uint8_t *__restrict__ tr_state,
+                                     int32_t n_chains, const int32_t *__restrict__ win,
+                                     const int32_t *__restrict__ pool_ids, int64_t pool_len,
+                                     const int32_t *__restrict__ del_ids, int64_t del_len) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr + pool_len + del_len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < n_tr) {
+      const int32_t id = tr_ids[e];  // validated on the host
+      if (win[id] != (int32_t)e) continue;  // a later chain lists this block too
+      int lo = 0, hi = n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tr_indptr[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      state[id] = tr_state[lo];
+      lat[id] = now;
+    } else if (e < n_tr + pool_len) {
+      const int32_t id = pool_ids[e - n_tr];
+      if ((uint64_t)id < (uint64_t)n) atomicAdd(&rc[id], 1u);
+    } else {
+      const int32_t id = del_ids[e - n_tr - pool_len];
+      if ((uint64_t)id < (uint64_t)n) atomicSub(&rc[id], 1u);
+    }
+  }
+}
+
+__global__ void manager_keys_kernel(const uint8_t *__restrict__ state, const uint32_t *__restrict__ rc,
+                                    const uint32_t *__restrict__ lat, const uint16_t *__restrict__ depth,
+                                    int64_t n, uint64_t *__restrict__ keys,
+                                    unsigned long long *__restrict__ n_active) {
+  unsigned int act = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = state[b];
+    const uint32_t r = rc[b];
+    uint64_t key;
+    if (s == 0 || s == 1 || s == 2 || s > 5) {
+      key = kInf;
+    } else {
+      uint64_t code;
+      if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
+      else code = (s == 4) ? 1ull : 0ull;
+      const uint64_t dep = depth ? (uint64_t)depth[b] : 0ull;
+      key = (code << 48) | ((uint64_t)lat[b] << 16) | (0xFFFFull - dep);
+    }
+    keys[b] = key;
+    act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
+  }
+  if (n_active) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) act += __shfl_xor_sync(0xffffffffu, act, o);
+    if ((threadIdx.x & 31) == 0 && act) atomicAdd(n_active, (unsigned long long)act);
+  }
+}
+
+cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth,
+                                int64_t n, uint32_t now, const int32_t *tr_ids, int64_t n_tr,
+                                const int32_t *tr_indptr, const uint8_t *tr_state, int32_t n_chains,
+                                int32_t *win, bool recount, const int32_t *pool_ids, int64_t pool_len,
+                                const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
+                                cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  if (recount) e = cudaMemsetAsync(rc, 0, (size_t)n * sizeof(uint32_t), s);
+  if (e == cudaSuccess && n_active) e = cudaMemsetAsync(n_active, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
+  auto grid_for = [](int64_t m) { return (int)std::min<int64_t>((m + 255) / 256, 148 * 8); };
+  if (n_tr > 0) {
+    manager_win_init_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win);
+    manager_win_max_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  const int64_t m = n_tr + pool_len + del_len;
+  if (m > 0) {
+    manager_apply_kernel<<<grid_for(m), 256, 0, s>>>(state, rc, lat, n, now, tr_ids, n_tr, tr_indptr, tr_state,
+                                                     n_chains, win, pool_ids, pool_len, del_ids, del_len);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (n > 0) {
+    manager_keys_kernel<<<grid_for(n), 256, 0, s>>>(state, rc, lat, depth, n, keys,
+                                                    reinterpret_cast<unsigned long long *>(n_active));
+    e = cudaGetLastError();
+  }
+  return e;
 }
 
 // ---------------------------------------------------------------------------------------

@@ -164,6 +164,8 @@ struct kva_pool {
   cudaEvent_t ev_afork = nullptr, ev_app = nullptr;
   bool app_pending = false;
   cudaStream_t aux_lo = nullptr;  // least-priority side stream of those writes (yields to decode)
+  // burst-reserve threshold: < 0 = none
+  int64_t threshold_blocks = -1, active_blocks = 0;
 };
 
 static int64_t count_free(const std::vector<uint32_t> &w, int nb) {
@@ -373,8 +375,10 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       (stride_tok % 8))
     return fail(KVA_ERR_INVALID, "k_new/v_new must be 16-byte aligned with stride %% 8 == 0");
   AppendPlan ap;
+  int64_t need_offline = 0;
   // count needed blocks (entries == -1 among new positions' blocks), validate the rest
   for (int i = 0; i < b->num_reqs; ++i) {
+    const int64_t need_before = ap.need;
     const int ql = qlen(b, i), ctx = b->ctx_len[i], start = ctx - ql;
     if (cdiv(ctx, kBlock) > nb)
       return fail(KVA_ERR_CAPACITY, "request %d needs %d blocks > pool's %d", i, cdiv(ctx, kBlock), nb);
@@ -384,11 +388,20 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       else if (row[k] < 0 || row[k] >= nb)
         return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid", i, k, row[k]);
     }
+    const int32_t ty = b->req_type ? b->req_type[i] : KVA_ONLINE_DECODE;
+    if (ty == KVA_OFFLINE_PREFILL || ty == KVA_OFFLINE_DECODE) need_offline += ap.need - need_before;
   }
   if (ap.need > p->n_free) {
     if (deficit) *deficit = (int32_t)(ap.need - p->n_free);
     return fail(KVA_NEEDS_EVICTION, "kv_append needs %lld blocks, %lld free", (long long)ap.need,
                 (long long)p->n_free);
+  }
+  // burst reserve: offline allocations may not push the active classes over the threshold;
+  // online ones may use the reserve (reading R35)
+  if (p->threshold_blocks >= 0 && need_offline > 0 && p->active_blocks + ap.need > p->threshold_blocks) {
+    if (deficit) *deficit = (int32_t)(p->active_blocks + ap.need - p->threshold_blocks);
+    return fail(KVA_NEEDS_EVICTION, "kv_append: %lld active + %lld new blocks > threshold %lld",
+                (long long)p->active_blocks, (long long)ap.need, (long long)p->threshold_blocks);
   }
   const size_t up = append_upload_bytes(b->num_reqs, ap.need);
   if (!workspace || ws_bytes < up)
@@ -493,6 +506,7 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_app, 0));  // the tile kernel's stream
     p->app_pending = true;
   }
+  p->active_blocks += ap.need;  // every new block belongs to a running request
   // commit host state: free mirror + caller's host table mirror
   p->free_host.swap(fh);
   p->n_free -= ap.need;
@@ -1064,6 +1078,103 @@ extern "C" kva_status hybrid_attention(kva_pool *p, const kva_batch_desc *b, con
   st = hybrid_attention_run(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse, stream);
   kva_plan_destroy(pl);
   return st;
+}
+
+// ------------------------------------------------------------------------------------------
+// burst-reserve threshold + KV-manager step
+// ------------------------------------------------------------------------------------------
+extern "C" kva_status kv_pool_set_threshold(kva_pool *p, int64_t threshold_blocks) {
+  if (!p) return fail(KVA_ERR_INVALID, "null pool");
+  if (threshold_blocks > p->desc.num_blocks)
+    return fail(KVA_ERR_INVALID, "threshold %lld > num_blocks %d", (long long)threshold_blocks, p->desc.num_blocks);
+  p->threshold_blocks = threshold_blocks < 0 ? -1 : threshold_blocks;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_pool_set_active_blocks(kva_pool *p, int64_t active_blocks) {
+  if (!p) return fail(KVA_ERR_INVALID, "null pool");
+  if (active_blocks < 0 || active_blocks > p->desc.num_blocks)
+    return fail(KVA_ERR_INVALID, "active_blocks %lld out of [0, num_blocks]", (long long)active_blocks);
+  p->active_blocks = active_blocks;
+  return KVA_OK;
+}
+
+namespace {
+std::mutex g_mgr_mu;
+Staging g_mgr_staging;  // pinned upload ring of the manager step (process-wide, mutex-guarded)
+
+kva_status manager_validate(const kva_block_meta *m, const kva_manager_update *u, int64_t *tot_out) {
+  if (!m || !u) return fail(KVA_ERR_INVALID, "null argument");
+  const int64_t n = m->num_blocks;
+  *tot_out = 0;
+  if (n < 0 || n > INT32_MAX) return fail(KVA_ERR_INVALID, "num_blocks out of range");
+  if (n > 0 && (!m->state || !m->rc || !m->lat)) return fail(KVA_ERR_INVALID, "state, rc, lat required");
+  if (u->n_chains < 0 || u->pool_len < 0 || u->del_len < 0) return fail(KVA_ERR_INVALID, "negative counts");
+  if (u->pool_len > 0 && !u->pool_ids) return fail(KVA_ERR_INVALID, "pool_ids required");
+  if (u->del_len > 0 && (!u->del_ids || u->recount)) return fail(KVA_ERR_INVALID, "del_ids only in incremental mode");
+  if (u->n_chains > 0) {
+    if (!u->chain_indptr || !u->chain_state) return fail(KVA_ERR_INVALID, "chain arrays required");
+    if (u->chain_indptr[0] != 0) return fail(KVA_ERR_INVALID, "chain_indptr[0] != 0");
+    for (int32_t j = 0; j < u->n_chains; ++j) {
+      if (u->chain_indptr[j + 1] < u->chain_indptr[j]) return fail(KVA_ERR_INVALID, "chain_indptr not monotone");
+      if (u->chain_state[j] > KVA_BLK_FINISHED_OFFLINE) return fail(KVA_ERR_INVALID, "chain %d: bad state", j);
+    }
+    const int64_t tot = u->chain_indptr[u->n_chains];
+    if (tot > 0 && !u->chain_ids) return fail(KVA_ERR_INVALID, "chain_ids required");
+    const int32_t *cid = u->chain_ids;
+    uint32_t bad = 0;
+    for (int64_t e = 0; e < tot; ++e) bad |= (uint32_t)cid[e] >= (uint32_t)n;  // vectorised
+    if (bad) return fail(KVA_ERR_INVALID, "chain id out of range");
+    *tot_out = tot;
+  }
+  return KVA_OK;
+}
+
+size_t manager_ws_bytes(int64_t n, int64_t tot, int32_t nc) {
+  return align256((size_t)tot * 4) + align256((size_t)(nc + 1) * 4) + align256((size_t)nc + 1) +
+         (tot > 0 ? align256((size_t)n * 4) : 0) + 256;
+}
+}  // namespace
+
+extern "C" kva_status kv_manager_step_workspace_size(const kva_block_meta *m, const kva_manager_update *u,
+                                                     size_t *bytes) {
+  if (!m || !u || !bytes) return fail(KVA_ERR_INVALID, "null argument");
+  const int64_t tot = (u->n_chains > 0 && u->chain_indptr) ? u->chain_indptr[u->n_chains] : 0;
+  *bytes = manager_ws_bytes(m->num_blocks, tot, std::max(0, u->n_chains));
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys,
+                                      int64_t *n_active, void *ws, size_t ws_bytes, kva_stream_t stream) {
+  int64_t tot = 0;
+  kva_status st = manager_validate(m, u, &tot);
+  if (st != KVA_OK) return st;
+  if (m->num_blocks > 0 && !keys) return fail(KVA_ERR_INVALID, "keys_out required");
+  const int32_t nc = tot > 0 ? u->n_chains : 0;
+  const size_t need = manager_ws_bytes(m->num_blocks, tot, nc);
+  if (tot > 0 && (!ws || ws_bytes < need))
+    return fail(KVA_ERR_INVALID, "kv_manager_step workspace too small (%zu < %zu)", ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(KVA_ERR_INVALID, "workspace must be 256-B aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t *w = static_cast<uint8_t *>(ws);
+  const size_t o_ind = align256((size_t)tot * 4), o_st = o_ind + align256((size_t)(nc + 1) * 4);
+  const size_t o_win = o_st + align256((size_t)nc + 1);
+  if (tot > 0) {  // upload the raw chains (no per-element host work beyond validation)
+    std::lock_guard<std::mutex> lk(g_mgr_mu);
+    Staging::Slot *slot = nullptr;
+    CUDA_TRY(g_mgr_staging.get(o_win, &slot));
+    uint8_t *h = static_cast<uint8_t *>(slot->host);
+    std::memcpy(h, u->chain_ids, (size_t)tot * 4);
+    std::memcpy(h + o_ind, u->chain_indptr, (size_t)(nc + 1) * 4);
+    std::memcpy(h + o_st, u->chain_state, (size_t)nc);
+    CUDA_TRY(g_mgr_staging.upload(slot, ws, o_st + nc, s));
+  }
+  CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now,
+                               reinterpret_cast<const int32_t *>(w), tot,
+                               reinterpret_cast<const int32_t *>(w + o_ind), w + o_st, nc,
+                               reinterpret_cast<int32_t *>(w + o_win), u->recount != 0, u->pool_ids,
+                               u->pool_len, u->del_ids, u->del_len, keys, n_active, s));
+  return KVA_OK;
 }
 
 // ------------------------------------------------------------------------------------------

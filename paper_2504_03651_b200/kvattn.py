@@ -44,6 +44,18 @@ class BatchDesc(ctypes.Structure):
                 ("group_prefix_blocks", ctypes.c_void_p), ("sm_scale", ctypes.c_float)]
 
 
+class BlockMeta(ctypes.Structure):
+    _fields_ = [("num_blocks", ctypes.c_int64), ("state", ctypes.c_void_p), ("rc", ctypes.c_void_p),
+                ("lat", ctypes.c_void_p), ("depth", ctypes.c_void_p)]
+
+
+class ManagerUpdate(ctypes.Structure):
+    _fields_ = [("now", ctypes.c_uint32), ("n_chains", ctypes.c_int32), ("chain_indptr", ctypes.c_void_p),
+                ("chain_ids", ctypes.c_void_p), ("chain_state", ctypes.c_void_p), ("recount", ctypes.c_int32),
+                ("pool_ids", ctypes.c_void_p), ("pool_len", ctypes.c_int64), ("del_ids", ctypes.c_void_p),
+                ("del_len", ctypes.c_int64)]
+
+
 class PlanStats(ctypes.Structure):
     _fields_ = [("n_decode_items", ctypes.c_int64), ("n_tile_items", ctypes.c_int64),
                 ("n_cascade_items", ctypes.c_int64), ("n_merge_rows", ctypes.c_int64),
@@ -60,7 +72,8 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
-           "evict_select_workspace_size", "evict_select", "kva_diag_occupy"]
+           "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
+           "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
 
 _lib = None
@@ -106,6 +119,10 @@ def load(build_if_missing: bool = True):
         "evict_select_workspace_size": ([i64, i64, P], ctypes.c_int),
         "evict_select": ([P, i64, i64, P, P, i32, P, P, sz, P], ctypes.c_int),
         "kva_diag_occupy": ([i32, i32, i64, P], ctypes.c_int),
+        "kv_pool_set_threshold": ([P, i64], ctypes.c_int),
+        "kv_pool_set_active_blocks": ([P, i64], ctypes.c_int),
+        "kv_manager_step_workspace_size": ([P, P, P], ctypes.c_int),
+        "kv_manager_step": ([P, P, P, P, P, sz, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -160,6 +177,14 @@ class Pool:
     def sync(self, stream=None):
         """kv_pool_sync: order `stream` after the pool's side-stream kv_append writes."""
         _check(load().kv_pool_sync(self.handle, _stream(stream)))
+
+    def set_threshold(self, threshold_blocks: int):
+        """kv_pool_set_threshold: burst reserve for kv_append (< 0 disables)."""
+        _check(load().kv_pool_set_threshold(self.handle, int(threshold_blocks)))
+
+    def set_active_blocks(self, n: int):
+        """kv_pool_set_active_blocks: active-class block count (e.g. the manager step's)."""
+        _check(load().kv_pool_set_active_blocks(self.handle, int(n)))
 
     def close(self):
         if self.handle:
@@ -337,6 +362,50 @@ def evict_keys(state, rc, lat, depth=None, keys=None, stream=None):
         keys = torch.empty(n, dtype=torch.int64, device=state.device)
     _check(L.evict_keys(_ptr(state), _ptr(rc), _ptr(lat), _ptr(depth), n, _ptr(keys), _stream(stream)))
     return keys
+
+
+class ManagerStep:
+    """kv_manager_step: class transitions (host chains, list order, last wins),
+    rc recount from the offline pool's chains (device ids), active-class count, eviction keys.
+    The host arrays are marshalled once per call; every step of the pass runs in the library."""
+
+    def __init__(self, state, rc, lat, depth=None):
+        self.state, self.rc, self.lat, self.depth = state, rc, lat, depth
+        self.meta = BlockMeta(state.numel(), _ptr(state), _ptr(rc), _ptr(lat), _ptr(depth))
+        self.keys = torch.empty(state.numel(), dtype=torch.int64, device=state.device)
+        self.n_active = torch.zeros(1, dtype=torch.int64, device=state.device)
+        self.ws = torch.empty(256, dtype=torch.uint8, device=state.device)
+
+    @staticmethod
+    def chains_csr(chains):
+        """[(state, ids-array), ...] -> host CSR (indptr, ids, states) for __call__."""
+        ci = np.zeros(len(chains) + 1, np.int32)
+        for j, (_, ids) in enumerate(chains):
+            ci[j + 1] = ci[j] + len(ids)
+        cids = (np.concatenate([np.asarray(ids, np.int32) for _, ids in chains]) if chains
+                else np.zeros(1, np.int32))
+        cst = np.array([s_ for s_, _ in chains] or [0], np.uint8)
+        return ci, cids, cst
+
+    def __call__(self, now: int, chains, pool_ids: torch.Tensor | None, del_ids: torch.Tensor | None = None,
+                 recount: bool = True, stream=None):
+        """chains: [(state, ids-array), ...] or a chains_csr() tuple (host); pool_ids: device
+        int32 (recount: every pool chain; incremental: the chains that joined), del_ids: device
+        int32 (incremental: the chains that left)."""
+        ci, cids, cst = chains if isinstance(chains, tuple) else self.chains_csr(chains)
+        plen = pool_ids.numel() if pool_ids is not None else 0
+        dlen = del_ids.numel() if del_ids is not None else 0
+        u = ManagerUpdate(int(now) & 0xFFFFFFFF, len(ci) - 1, ci.ctypes.data, cids.ctypes.data,
+                          cst.ctypes.data, 1 if recount else 0, _ptr(pool_ids) if plen else None, plen,
+                          _ptr(del_ids) if dlen else None, dlen)
+        need = ctypes.c_size_t()
+        L = load()
+        _check(L.kv_manager_step_workspace_size(ctypes.byref(self.meta), ctypes.byref(u), ctypes.byref(need)))
+        if self.ws.numel() < need.value:
+            self.ws = torch.empty(need.value, dtype=torch.uint8, device=self.state.device)
+        _check(L.kv_manager_step(ctypes.byref(self.meta), ctypes.byref(u), _ptr(self.keys), _ptr(self.n_active),
+                                 _ptr(self.ws), self.ws.numel(), _stream(stream)))
+        return self.keys
 
 
 def evict_select_workspace_size(n: int, k: int) -> int:

@@ -30,7 +30,7 @@ def main():
                                                       "append_kernel", "alloc_write", "evict_", "release_ids",
                                                       "Memcpy", "Memset", "elementwise", "copy"))]
     # last step = kernels after the last append_kernel's preceding evict_keys
-    starts = [i for i, x in enumerate(mine) if "evict_keys" in x[2]] or [0]
+    starts = [i for i, x in enumerate(mine) if "manager_apply" in x[2]] or [0]
     last = mine[starts[-1]:]
     t0 = last[0][0]
     rows = [{"kernel": n.split("(")[0][-40:], "stream": s, "start_us": round(a - t0, 1),

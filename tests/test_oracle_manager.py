@@ -189,3 +189,27 @@ def test_threshold_examples():
     st, deficit = oracle.kv_append(b, wl.k_pool, wl.v_pool, fb_small, wl.k_new, wl.v_new,
                                    active_blocks=0, threshold_blocks=nb)[:2]
     assert st == oracle.NEEDS_EVICTION and deficit == 3
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_incremental_counts_equal_recount(seed):
+    """Incremental mode (requests joining / leaving the offline pool) must equal a full recount
+    of the new pool ("request finishes and leaves pool -> rc decremented")."""
+    rng = np.random.default_rng(77 + seed)
+    n = int(rng.integers(30, 300))
+    state = rng.integers(0, 6, n).astype(np.uint8)
+    lat = rng.integers(0, 9, n).astype(np.uint32)
+    pool = [list(rng.choice(n, int(rng.integers(1, 20)), replace=False)) for _ in range(int(rng.integers(1, 25)))]
+    st, s1, rc1, l1, _, _ = oracle.manager_step(state, None, lat, None, 3, [], pool)
+    leave = sorted(set(rng.choice(len(pool), int(rng.integers(0, len(pool) + 1)), replace=False).tolist()))
+    join = [list(rng.choice(n, int(rng.integers(1, 20)), replace=False)) for _ in range(int(rng.integers(0, 10)))]
+    new_pool = [p for i, p in enumerate(pool) if i not in leave] + join
+    st_a, sa, rca, la, ka, na = oracle.manager_step(s1, rc1, l1, None, 4, [], join,
+                                                    delete=[pool[i] for i in leave], recount=False)
+    st_b, sb, rcb, lb, kb, nb = oracle.manager_step(s1, rc1, l1, None, 4, [], new_pool)
+    assert st_a == st_b == oracle.OK
+    assert np.array_equal(rca, rcb) and np.array_equal(ka, kb) and na == nb
+    # a count would go negative -> INVALID, nothing changed
+    st_c, sc, rcc, _, _, _ = oracle.manager_step(s1, np.zeros(n, np.uint32), l1, None, 4, [], [],
+                                                 delete=[pool[0]], recount=False)
+    assert st_c == oracle.INVALID and not rcc.any()

@@ -329,3 +329,33 @@ def retouch(ev: EvictWorkload, now: int, frac: float = 0.05, seed: int = 0):
     ends = np.concatenate([ev.run_start[1:], [len(ev.order)]])
     for r in pick:
         ev.lat[ev.order[ev.run_start[r]:ends[r]]] = now
+
+
+def make_manager_update(ev: EvictWorkload, now: int, seed: int = 0, touch_frac: float = 0.05,
+                        finish_frac: float = 0.01):
+    """One KV-manager iteration over the `evict` metadata: returns
+    (chains, pool) with chains = [(state, ids)] (host) and pool = [ids] (the offline pool's
+    prompt chains).  The pool reproduces the drawn rc exactly: an active-offline run with
+    rc = r is the prefix chain of r pool requests ("how many offline requests ... will
+    reuse it").  Transitions: a random touch_frac of runs keep their class with lat = now
+    (LRU refresh); finish_frac of runs change class (running online -> finished online,
+    pinned -> finished offline).  No method arithmetic here: only seeded choices."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    nr = len(ev.run_start)
+    ends = np.concatenate([ev.run_start[1:], [len(ev.order)]])
+    runs = [ev.order[ev.run_start[r]:ends[r]] for r in range(nr)]
+    pool = []
+    for r in range(nr):
+        b0 = runs[r][0]
+        if ev.state[b0] == EV_ACTIVE_OFFLINE:
+            pool.extend([runs[r]] * int(ev.rc[b0]))
+    chains = []
+    for r in rng.choice(nr, size=max(1, int(touch_frac * nr)), replace=False):
+        chains.append((int(ev.state[runs[r][0]]), runs[r]))
+    for r in rng.choice(nr, size=max(1, int(finish_frac * nr)), replace=False):
+        s = int(ev.state[runs[r][0]])
+        if s == 1:
+            chains.append((4, runs[r]))
+        elif s == 2:
+            chains.append((5, runs[r]))
+    return chains, pool
