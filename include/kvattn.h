@@ -301,6 +301,39 @@ kva_status kv_manager_step(const kva_block_meta *meta, const kva_manager_update 
 kva_status kv_pool_set_threshold(kva_pool *pool, int64_t threshold_blocks);
 kva_status kv_pool_set_active_blocks(kva_pool *pool, int64_t active_blocks);
 
+/* ---- prefix index + batch grouping (host only) ----
+ * A block-granular radix index over token ids: one entry per cached block, keyed by (parent
+ * entry, the block's 16 token ids), so identical token prefixes map to the same physical
+ * blocks ("prefix caching").  Sub-block matches are misses.
+ *   kva_prefix_insert: register the whole blocks of tokens[0, n_tokens) with their block ids
+ *     (blocks already cached must carry the same id; a new id must not be indexed elsewhere;
+ *     else KVA_ERR_INVALID, nothing changed); LAT of the chain = now.
+ *   kva_prefix_lookup (S:125-133 lookup_prefix): the longest cached prefix of whole blocks;
+ *     *n_hit blocks, the first min(cap, n_hit) ids written to out_block_ids; their LAT = now.
+ *   kva_prefix_remove: drop evicted blocks and every entry below them (no dangling
+ *     entries S:109); unknown ids are ignored.
+ *   kva_group_batch: the batch descriptor's shared-prefix groups from the requests' token ids
+ *     (tokens[i][0, n_tokens[i]) = request i's context): usable_i = min(cached prefix blocks,
+ *     prefix_limit_blocks[i]) (nullable; pass floor((ctx - q_len)/16) so the queries lie after
+ *     the prefix, reading #8).  Requests with usable_i >= min_blocks whose first min_blocks
+ *     blocks are the same entries form a group if there are >= 2 of them; its prefix is the
+ *     deepest entry all members share, capped by every member's usable_i.  Groups are numbered
+ *     in order of their first member; group_of[i] = -1 for the rest.  group_prefix_blocks needs
+ *     room for R entries. */
+typedef struct kva_prefix_index kva_prefix_index;
+kva_status kva_prefix_index_create(kva_prefix_index **out);
+kva_status kva_prefix_index_destroy(kva_prefix_index *ix);
+kva_status kva_prefix_insert(kva_prefix_index *ix, const int32_t *tokens, int64_t n_tokens,
+                             const int32_t *block_ids, uint32_t now);
+kva_status kva_prefix_lookup(kva_prefix_index *ix, const int32_t *tokens, int64_t n_tokens,
+                             int32_t *out_block_ids, int64_t cap, int64_t *n_hit, uint32_t now);
+kva_status kva_prefix_remove(kva_prefix_index *ix, const int32_t *block_ids, int64_t n);
+kva_status kva_prefix_size(const kva_prefix_index *ix, int64_t *n_blocks);
+kva_status kva_group_batch(kva_prefix_index *ix, int32_t num_reqs, const int32_t *const *tokens,
+                           const int64_t *n_tokens, const int32_t *prefix_limit_blocks,
+                           int32_t min_blocks, int32_t *group_of, int32_t *group_prefix_blocks,
+                           int32_t *num_groups);
+
 /* ---- diagnostics (not part of the hot path) ----
  * kva_diag_occupy: enqueue n_ctas CTAs that each hold smem_bytes of shared memory and spin
  * for ns nanoseconds on `stream`; a kernel launched right after on another stream then runs on

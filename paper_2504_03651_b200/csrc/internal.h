@@ -6,7 +6,12 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/kvattn.h"
+
 namespace kva {
+
+// sets the thread-local kva_last_error() message (kvattn_host.cu) and returns st
+kva_status set_error(kva_status st, const char *msg);
 
 constexpr int kBlock = 16;        // tokens per KV block (reading #5)
 constexpr int kSplitKeys = 512;   // fixed split-KV length (depends only on ctx, H9)

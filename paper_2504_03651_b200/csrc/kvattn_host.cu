@@ -42,6 +42,12 @@ static kva_status fail(kva_status st, const char *fmt, ...) {
   } while (0)
 
 extern "C" const char *kva_last_error(void) { return g_err.c_str(); }
+namespace kva {
+kva_status set_error(kva_status st, const char *msg) {
+  g_err = msg;
+  return st;
+}
+}  // namespace kva
 extern "C" const char *kva_version(void) {
   return "kvattn 0.1 (sm_100a; decode split-KV TMA+mma.sync, tile attention, radix top-k)";
 }

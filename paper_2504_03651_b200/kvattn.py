@@ -73,7 +73,9 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
-           "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step"]
+           "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step",
+           "kva_prefix_index_create", "kva_prefix_index_destroy", "kva_prefix_insert", "kva_prefix_lookup",
+           "kva_prefix_remove", "kva_prefix_size", "kva_group_batch"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
 
 _lib = None
@@ -123,6 +125,13 @@ def load(build_if_missing: bool = True):
         "kv_pool_set_active_blocks": ([P, i64], ctypes.c_int),
         "kv_manager_step_workspace_size": ([P, P, P], ctypes.c_int),
         "kv_manager_step": ([P, P, P, P, P, sz, P], ctypes.c_int),
+        "kva_prefix_index_create": ([P], ctypes.c_int),
+        "kva_prefix_index_destroy": ([P], ctypes.c_int),
+        "kva_prefix_insert": ([P, P, i64, P, ctypes.c_uint32], ctypes.c_int),
+        "kva_prefix_lookup": ([P, P, i64, P, i64, P, ctypes.c_uint32], ctypes.c_int),
+        "kva_prefix_remove": ([P, P, i64], ctypes.c_int),
+        "kva_prefix_size": ([P, P], ctypes.c_int),
+        "kva_group_batch": ([P, i32, P, P, P, i32, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -448,3 +457,63 @@ def free_bits_tensor(free_bits_np: np.ndarray, device) -> torch.Tensor:
 def diag_occupy(n_ctas: int, smem_bytes: int, ns: int, stream=None):
     """Diagnostics: hold n_ctas SMs (smem_bytes each) for ns nanoseconds on `stream`."""
     _check(load().kva_diag_occupy(n_ctas, smem_bytes, ns, _stream(stream)))
+
+
+class PrefixIndex:
+    """Block-granular prefix index (host, C++): insert / lookup / remove chains of
+    whole 16-token blocks and build the batch descriptor's shared-prefix groups (group_batch)."""
+
+    def __init__(self):
+        self.handle = ctypes.c_void_p()
+        _check(load().kva_prefix_index_create(ctypes.byref(self.handle)))
+
+    @staticmethod
+    def _i32(a):
+        return np.ascontiguousarray(a, dtype=np.int32)
+
+    def insert(self, tokens, block_ids, now: int = 0):
+        t, b = self._i32(tokens), self._i32(block_ids)
+        _check(load().kva_prefix_insert(self.handle, t.ctypes.data, t.size, b.ctypes.data, int(now) & 0xFFFFFFFF))
+
+    def lookup(self, tokens, now: int = 0) -> np.ndarray:
+        t = self._i32(tokens)
+        out = np.zeros(max(1, t.size // 16), np.int32)
+        n = ctypes.c_int64()
+        _check(load().kva_prefix_lookup(self.handle, t.ctypes.data, t.size, out.ctypes.data, out.size,
+                                        ctypes.byref(n), int(now) & 0xFFFFFFFF))
+        return out[: n.value]
+
+    def remove(self, block_ids):
+        b = self._i32(block_ids)
+        _check(load().kva_prefix_remove(self.handle, b.ctypes.data, b.size))
+
+    def size(self) -> int:
+        n = ctypes.c_int64()
+        _check(load().kva_prefix_size(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def group_batch(self, token_lists, prefix_limit_blocks=None, min_blocks: int = 1):
+        """-> (group_of int32[R], group_prefix_blocks int32[G]) for the batch descriptor."""
+        arrs = [self._i32(t) for t in token_lists]
+        R = len(arrs)
+        ptrs = (ctypes.c_void_p * max(1, R))(*[a.ctypes.data for a in arrs])
+        lens = np.array([a.size for a in arrs] or [0], np.int64)
+        lim = None if prefix_limit_blocks is None else self._i32(prefix_limit_blocks)
+        gof = np.full(max(1, R), -1, np.int32)
+        gpb = np.zeros(max(1, R), np.int32)
+        G = ctypes.c_int32()
+        _check(load().kva_group_batch(self.handle, R, ptrs, lens.ctypes.data,
+                                      None if lim is None else lim.ctypes.data, int(min_blocks),
+                                      gof.ctypes.data, gpb.ctypes.data, ctypes.byref(G)))
+        return gof[:R], gpb[: G.value]
+
+    def close(self):
+        if self.handle:
+            load().kva_prefix_index_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

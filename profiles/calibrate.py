@@ -1,0 +1,127 @@
+"""Estimator calibration on B200: sweep hybrid_attention over
+pure-prefill, pure-decode and mixed batches (Llama-2-7B attention shape, one layer), time each
+with CUDA events (median of warm runs), fit Eq.(6)-(8) with paper_2504_03651_b200.estimator, and
+report fit residuals plus two questions the paper leaves open:
+  * is the mixed-batch time between max and sum (P:395 prose) or between min and max (Eq.(8) as
+    written)?  -> fraction of mixed samples in each interval;
+  * with fixed-length splits, does gamma (the max(L) term, load imbalance) vanish?
+
+python profiles/calibrate.py [outdir]   -> outdir/estimator_samples.jsonl, estimator_fit.json
+"""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2504_03651_b200 as K  # noqa: E402
+from paper_2504_03651_b200 import estimator as E  # noqa: E402
+import workloads as W  # noqa: E402
+
+HQ, HKV, D = 32, 32, 128
+
+
+def time_batch(reqs, seed):
+    cfg = W.custom_config("cal", HQ, HKV, D, seed, reqs, [])
+    wl = W.make_workload(cfg, device="cuda")
+    pool = K.Pool(wl.k_pool, wl.v_pool, K.free_bits_tensor(wl.free_bits, "cuda"))
+    batch = K.Batch(wl.batch, "cuda")
+    K.kv_append(pool, batch, wl.k_new, wl.v_new)
+    plan = K.Plan(pool, batch)
+    out = torch.empty(wl.q.shape, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream()
+    ts = []
+    for i in range(8):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        plan.run(wl.q, out)
+        b.record(s)
+        b.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b) * 1e-3)
+    plan.close()
+    pool.close()
+    return statistics.median(ts)
+
+
+def main():
+    outdir = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+    os.makedirs(outdir, exist_ok=True)
+    rng = np.random.default_rng(0)
+    samples = []
+
+    def add(prefill_spans, decode_lens, seed):
+        reqs = [W.ReqSpec(W.OFFLINE_PREFILL, e, e - s_) for s_, e in prefill_spans]
+        reqs += [W.ReqSpec(W.ONLINE_DECODE, l, 1) for l in decode_lens]
+        t = time_batch(reqs, seed)
+        samples.append({"prefill_spans": [list(x) for x in prefill_spans],
+                        "decode_lens": [int(x) for x in decode_lens], "time_s": t})
+
+    for l in [16, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192]:
+        add([(0, l)], [], l)
+    for s_, e in [(512, 1024), (1024, 2048), (2048, 4096), (4096, 8192), (1536, 2048)]:
+        add([(s_, e)], [], s_ + e)
+    for i in range(16):
+        n = int(rng.integers(4, 129))
+        L = rng.integers(64, 4096, n)
+        if i % 2:
+            L[0] = int(rng.integers(8192, 32768))
+        add([], L.tolist(), 100 + i)
+    for i in range(12):
+        l = int(rng.choice([256, 512, 1024, 2048]))
+        L = rng.integers(256, 4096, int(rng.integers(8, 65)))
+        add([(0, l)], L.tolist(), 200 + i)
+    with open(os.path.join(outdir, "estimator_samples.jsonl"), "w") as f:
+        for s_ in samples:
+            f.write(json.dumps(s_) + "\n")
+
+    p = E.calibrate(samples)
+    rel = [abs(E.estimate(s_, p) - s_["time_s"]) / s_["time_s"] for s_ in samples]
+    rel_prose = [abs(E.batch_time_prose(*E.sample_components(s_, p), p) - s_["time_s"]) / s_["time_s"]
+                 for s_ in samples if s_["decode_lens"] and s_["prefill_spans"]]
+    kinds = ["prefill" if not s_["decode_lens"] else "decode" if not s_["prefill_spans"] else "mixed"
+             for s_ in samples]
+    # the open question on Eq.(8): where do measured mixed times fall?
+    between_max_sum = between_min_max = 0
+    ratios = []
+    for s_, k in zip(samples, kinds):
+        if k != "mixed":
+            continue
+        tp = time_batch([W.ReqSpec(W.OFFLINE_PREFILL, e, e - a) for a, e in s_["prefill_spans"]], 900)
+        td = time_batch([W.ReqSpec(W.ONLINE_DECODE, l, 1) for l in s_["decode_lens"]], 901)
+        t = s_["time_s"]
+        between_max_sum += max(tp, td) <= t <= tp + td
+        between_min_max += min(tp, td) <= t <= max(tp, td)
+        ratios.append((t - max(tp, td)) / min(tp, td))
+    # extended decode model for this kernel: time vs total KV bytes (sum L) — fixed splits
+    dec = [s_ for s_, k in zip(samples, kinds) if k == "decode"]
+    A = np.stack([[max(s_["decode_lens"]) for s_ in dec], [sum(s_["decode_lens"]) for s_ in dec],
+                  [1.0] * len(dec)], 1)
+    tdv = np.array([s_["time_s"] for s_ in dec])
+    coef, *_ = np.linalg.lstsq(A / tdv[:, None], np.ones(len(dec)), rcond=None)
+    res = {
+        "params": p.as_dict(),
+        "median_rel_err": {k: float(np.median([r for r, kk in zip(rel, kinds) if kk == k]))
+                           for k in ("prefill", "decode", "mixed")},
+        "max_rel_err": {k: float(np.max([r for r, kk in zip(rel, kinds) if kk == k]))
+                        for k in ("prefill", "decode", "mixed")},
+        "mixed_median_rel_err_prose_form": float(np.median(rel_prose)),
+        "mixed_between_max_and_sum": f"{between_max_sum}/{len(ratios)}",
+        "mixed_between_min_and_max": f"{between_min_max}/{len(ratios)}",
+        "mixed_(t-max)/min": [round(x, 3) for x in ratios],
+        "decode_extended_fit_s": {"per_max_token": float(coef[0]), "per_total_token": float(coef[1]),
+                                  "const": float(coef[2]),
+                                  "note": "time = a*max(L) + b*sum(L) + c; b*2*HKV*D*2 bytes/token gives GB/s"},
+        "decode_GBps_from_fit": float(2 * HKV * D * 2 / coef[1] / 1e9) if coef[1] > 0 else None,
+        "shape": {"Hq": HQ, "Hkv": HKV, "d": D, "layers": 1},
+        "n_samples": len(samples),
+    }
+    json.dump(res, open(os.path.join(outdir, "estimator_fit.json"), "w"), indent=1)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
