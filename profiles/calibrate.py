@@ -64,16 +64,24 @@ def main():
         add([(0, l)], [], l)
     for s_, e in [(512, 1024), (1024, 2048), (2048, 4096), (4096, 8192), (1536, 2048)]:
         add([(s_, e)], [], s_ + e)
+    # Eq.(7) is a model of one batch size (it pools lengths, it has no n term): decode-only and
+    # the decode part of mixed batches use n = 64 requests (the llama7b decode count)
     for i in range(16):
-        n = int(rng.integers(4, 129))
-        L = rng.integers(64, 4096, n)
+        L = rng.integers(64, 4096, 64)
         if i % 2:
             L[0] = int(rng.integers(8192, 32768))
         add([], L.tolist(), 100 + i)
     for i in range(12):
         l = int(rng.choice([256, 512, 1024, 2048]))
-        L = rng.integers(256, 4096, int(rng.integers(8, 65)))
+        L = rng.integers(256, 4096, 64)
         add([(0, l)], L.tolist(), 200 + i)
+    # varying batch size (for the extended decode fit only; kept out of calibrate())
+    extra = []
+    for i in range(10):
+        n = int(rng.integers(4, 129))
+        L = rng.integers(64, 4096, n)
+        reqs = [W.ReqSpec(W.ONLINE_DECODE, int(x), 1) for x in L]
+        extra.append({"prefill_spans": [], "decode_lens": L.tolist(), "time_s": time_batch(reqs, 300 + i)})
     with open(os.path.join(outdir, "estimator_samples.jsonl"), "w") as f:
         for s_ in samples:
             f.write(json.dumps(s_) + "\n")
@@ -97,7 +105,7 @@ def main():
         between_min_max += min(tp, td) <= t <= max(tp, td)
         ratios.append((t - max(tp, td)) / min(tp, td))
     # extended decode model for this kernel: time vs total KV bytes (sum L) — fixed splits
-    dec = [s_ for s_, k in zip(samples, kinds) if k == "decode"]
+    dec = [s_ for s_, k in zip(samples, kinds) if k == "decode"] + extra
     A = np.stack([[max(s_["decode_lens"]) for s_ in dec], [sum(s_["decode_lens"]) for s_ in dec],
                   [1.0] * len(dec)], 1)
     tdv = np.array([s_["time_s"] for s_ in dec])
@@ -112,6 +120,7 @@ def main():
         "mixed_between_max_and_sum": f"{between_max_sum}/{len(ratios)}",
         "mixed_between_min_and_max": f"{between_min_max}/{len(ratios)}",
         "mixed_(t-max)/min": [round(x, 3) for x in ratios],
+        "mu_from_measured_components": float(np.median(ratios)) if ratios else None,
         "decode_extended_fit_s": {"per_max_token": float(coef[0]), "per_total_token": float(coef[1]),
                                   "const": float(coef[2]),
                                   "note": "time = a*max(L) + b*sum(L) + c; b*2*HKV*D*2 bytes/token gives GB/s"},
