@@ -18,8 +18,10 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "internal.h"
 
@@ -183,10 +185,191 @@ struct SortWs {
 };
 }  // namespace
 
+// ---------------------------------------------------------------------------------------
+// Sample-bucket path of evict_select (KVA_EVICT_IMPL=fast, n >= 2^16): sample -> splitters -> one bucketing pass
+// -> per-bucket sorts.  Three launches, no grid barrier; the exact cooperative kernel above is
+// the fallback (it runs only if a bucket overflows or the sample under-estimated the k-th key).
+//   1. one CTA sorts a strided sample of kSample (2048) keys and picks v_hi = the sample element at
+//      rank r + 4 sqrt(r) + 8 (r = k * kSample / n) and kBuckets - 1 splitters below it;
+//   2. every key < v_hi goes to its bucket (key range), positions reserved per CTA tile;
+//   3. bucket b's CTA checks that the candidates hold >= k keys (then they contain every key
+//      <= the k-th smallest, ties included), sorts its bucket by (key, id) in shared memory and
+//      writes the ranks < k of the global order.
+namespace {
+constexpr int kSample = 2048;
+constexpr int kBuckets = 64;
+constexpr int kCap = 8192;  // pairs per bucket (its shared-memory sort: 8192 x 12 B)
+struct FastWs {
+  unsigned long long split[kBuckets];  // split[b] = first key of bucket b + 1 (b < kBuckets - 1)
+  unsigned long long v_hi;             // candidates: key < v_hi (UINT64_MAX: every evictable key)
+  unsigned int cnt[kBuckets];
+  int overflow;
+  int run_fallback;
+};
+}  // namespace
+
+__device__ __forceinline__ bool pair_gt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
+  return ka > kb || (ka == kb && ia > ib);
+}
+
+// bitonic sort of N (power of two) (key, id) pairs in shared memory, ascending
+__device__ void smem_bitonic(uint64_t *k, int32_t *id, int N) {
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          if (pair_gt(k[i], id[i], k[j], id[j]) == up) {
+            const uint64_t tk = k[i]; k[i] = k[j]; k[j] = tk;
+            const int32_t ti = id[i]; id[i] = id[j]; id[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) sel_sample_kernel(const uint64_t *__restrict__ keys, int64_t n,
+                                                          int64_t k, FastWs *__restrict__ fw) {
+  __shared__ uint64_t sk[kSample];
+  __shared__ int32_t si[kSample];
+  __shared__ int s_ev;
+  const int tid = threadIdx.x;
+  if (tid < kBuckets) fw->cnt[tid] = 0u;
+  if (tid == 0) {
+    fw->overflow = 0;
+    fw->run_fallback = 0;
+    s_ev = 0;
+  }
+  __syncthreads();
+  int ev = 0;
+  for (int i = tid; i < kSample; i += blockDim.x) {
+    const uint64_t key = keys[(int64_t)(((__int128)i * n) / kSample)];
+    sk[i] = key;
+    si[i] = i;
+    ev += key != kInf;
+  }
+  atomicAdd(&s_ev, ev);
+  __syncthreads();
+  smem_bitonic(sk, si, kSample);
+  if (tid == 0) {
+    const double r = (double)k * kSample / (double)n;
+    const int64_t r_hi = (int64_t)ceil(r + 4.0 * sqrt(r) + 8.0);
+    const int evs = s_ev;
+    int top;  // sample ranks [0, top) are spread over the buckets
+    if (r_hi >= evs) {
+      fw->v_hi = kInf;  // the candidates may have to be every evictable key
+      top = evs;
+    } else {
+      fw->v_hi = sk[r_hi];
+      top = (int)r_hi;
+    }
+    for (int b = 0; b < kBuckets - 1; ++b) {
+      const int rk = (int)(((int64_t)top * (b + 1)) / kBuckets);
+      fw->split[b] = top > 0 ? sk[min(rk, kSample - 1)] : kInf;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sel_bucket_kernel(const uint64_t *__restrict__ keys, int64_t n,
+                                                         FastWs *__restrict__ fw, uint64_t *__restrict__ bkey,
+                                                         int32_t *__restrict__ bid) {
+  constexpr int PER = 16;  // keys per thread per tile
+  __shared__ uint64_t s_split[kBuckets];
+  __shared__ unsigned int s_cnt[kBuckets], s_base[kBuckets];
+  const int tid = threadIdx.x;
+  if (tid < kBuckets) s_split[tid] = fw->split[tid];
+  __syncthreads();
+  const uint64_t v_hi = fw->v_hi;
+  const int64_t tile = (int64_t)blockDim.x * PER;
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+    if (tid < kBuckets) s_cnt[tid] = 0u;
+    __syncthreads();
+    int8_t bk[PER];
+    unsigned int lp[PER];
+    uint64_t kv[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int64_t i = t0 + (int64_t)u * blockDim.x + tid;  // coalesced
+      bk[u] = -1;
+      if (i < n) {
+        const uint64_t key = keys[i];
+        kv[u] = key;
+        if (key < v_hi && key != kInf) {
+          int lo = 0, hi = kBuckets - 1;  // bucket = #splitters <= key
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_split[mid] <= key) lo = mid + 1;
+            else hi = mid;
+          }
+          bk[u] = (int8_t)lo;
+          lp[u] = atomicAdd(&s_cnt[lo], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < kBuckets) s_base[tid] = s_cnt[tid] ? atomicAdd(&fw->cnt[tid], s_cnt[tid]) : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (bk[u] < 0) continue;
+      const unsigned int pos = s_base[bk[u]] + lp[u];
+      if (pos < (unsigned)kCap) {
+        bkey[(int64_t)bk[u] * kCap + pos] = kv[u];
+        bid[(int64_t)bk[u] * kCap + pos] = (int32_t)(t0 + (int64_t)u * blockDim.x + tid);
+      } else {
+        fw->overflow = 1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) sel_sort_kernel(int64_t k, FastWs *__restrict__ fw,
+                                                        const uint64_t *__restrict__ bkey,
+                                                        const int32_t *__restrict__ bid,
+                                                        int32_t *__restrict__ out_ids, int64_t *__restrict__ d_count) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint64_t *sk = reinterpret_cast<uint64_t *>(sm);
+  int32_t *si = reinterpret_cast<int32_t *>(sm + (size_t)kCap * 8);
+  const int b = blockIdx.x, tid = threadIdx.x;
+  int64_t total = 0, off = 0;
+  for (int j = 0; j < kBuckets; ++j) {
+    const int64_t c = fw->cnt[j];
+    if (j < b) off += c;
+    total += c;
+  }
+  const bool inf_mode = fw->v_hi == kInf;
+  const bool valid = !fw->overflow && (inf_mode || total >= k);
+  if (b == 0 && tid == 0) {
+    fw->run_fallback = valid ? 0 : 1;
+    if (valid) *d_count = total < k ? total : k;
+  }
+  const int64_t cnt = fw->cnt[b];
+  if (!valid || off >= k || cnt == 0) return;
+  int N = 2;
+  while (N < cnt) N <<= 1;
+  for (int i = tid; i < N; i += blockDim.x) {
+    if (i < cnt) {
+      sk[i] = bkey[(int64_t)b * kCap + i];
+      si[i] = bid[(int64_t)b * kCap + i];
+    } else {
+      sk[i] = kInf;
+      si[i] = INT32_MAX;
+    }
+  }
+  __syncthreads();
+  smem_bitonic(sk, si, N);
+  for (int64_t i = tid; i < cnt && off + i < k; i += blockDim.x) out_ids[off + i] = si[i];
+}
+
 size_t evict_select_ws_bytes(int64_t n, int64_t k) {
   (void)n;
   const size_t pairs = (size_t)std::max<int64_t>(k, 1);
-  return sizeof(SelWs) + sizeof(SortWs) + 2 * pairs * (sizeof(uint64_t) + sizeof(int32_t)) + 256;
+  return sizeof(SelWs) + sizeof(SortWs) + 2 * pairs * (sizeof(uint64_t) + sizeof(int32_t)) + 256 +
+         ((sizeof(FastWs) + 255) & ~size_t(255)) + (size_t)kBuckets * kCap * (8 + 4) + 256;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -238,7 +421,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     evict_select_kernel(const uint64_t *__restrict__ keys, int64_t n, int64_t k,
                         int32_t *__restrict__ out_ids, int64_t *__restrict__ d_count,
                         SelWs *__restrict__ sw, SortWs *__restrict__ so, uint64_t *pk0,
-                        int32_t *pi0, uint64_t *pk1, int32_t *pi1, int cache_keys) {
+                        int32_t *pi0, uint64_t *pk1, int32_t *pi1, int cache_keys,
+                        const int *__restrict__ run_flag) {
+  // fallback of the sample-bucket fast path: every CTA leaves before any grid barrier when the
+  // fast path produced the result (run_flag == 0); run_flag == nullptr: always run
+  if (run_flag && *(volatile const int *)run_flag == 0) return;
   cg::grid_group grid = cg::this_grid();
   int tp = 0;
   auto stamp = [&]() {
@@ -717,11 +904,37 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   int32_t *pi0 = reinterpret_cast<int32_t *>(p); p += pairs * 4;
   int32_t *pi1 = reinterpret_cast<int32_t *>(p); p += pairs * 4;
   if ((size_t)(p - reinterpret_cast<uint8_t *>(ws)) > ws_bytes) return cudaErrorInvalidValue;
+  // fast path region after the cooperative kernel's scratch
+  p = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+  FastWs *fw = reinterpret_cast<FastWs *>(p);
+  p += (sizeof(FastWs) + 255) & ~size_t(255);
+  uint64_t *bkey = reinterpret_cast<uint64_t *>(p);
+  p += (size_t)kBuckets * kCap * 8;
+  int32_t *bid = reinterpret_cast<int32_t *>(p);
+  p += (size_t)kBuckets * kCap * 4;
+  if ((size_t)(p - reinterpret_cast<uint8_t *>(ws)) > ws_bytes) return cudaErrorInvalidValue;
+  // KVA_EVICT_IMPL=fast selects the sample-bucket path (read per call).  Default: the
+  // cooperative kernel alone — measured faster inside the bench step (its CTAs are resident
+  // from the start and co-run with the decode kernel; the fast path's 64 x 1024-thread sort
+  // CTAs queue behind it: 151 us alone vs 123, step 517 vs 455 us, profiles/r01b).
+  const char *impl_env = getenv("KVA_EVICT_IMPL");
+  const bool fast = impl_env && std::string(impl_env) == "fast" && n >= (1 << 16);
+  const int *run_flag = nullptr;
+  if (fast) {
+    sel_sample_kernel<<<1, 1024, 0, s>>>(keys, n, k, fw);
+    sel_bucket_kernel<<<std::max(1, std::min(nsm * 4, (int)((n + 4095) / 4096))), 256, 0, s>>>(keys, n, fw, bkey, bid);
+    static bool attr = (cudaFuncSetAttribute(sel_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kCap * 12), true);
+    (void)attr;
+    sel_sort_kernel<<<kBuckets, 1024, kCap * 12, s>>>(k, fw, bkey, bid, out_ids, d_count);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    run_flag = &fw->run_fallback;
+  }
   e = cudaMemsetAsync(sw, 0, sizeof(SelWs), s);
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&keys, (void *)&n, (void *)&k, (void *)&out_ids, (void *)&d_count,
                   (void *)&sw, (void *)&so, (void *)&pk0, (void *)&pi0, (void *)&pk1, (void *)&pi1,
-                  (void *)&cache};
+                  (void *)&cache, (void *)&run_flag};
   return cudaLaunchCooperativeKernel((void *)evict_select_kernel, dim3(C), dim3(kThreads), args, dyn, s);
 }
 

@@ -121,3 +121,38 @@ def test_evict_k_larger_than_evictable_and_zero():
     assert n == n_ev and np.array_equal(ids.cpu().numpy(), ref_ids)
     ids, n = K.evict_select(keys, 0)
     assert n == 0
+
+
+@pytest.mark.parametrize("impl", ["coop", "fast"])
+@pytest.mark.parametrize("case", ["all_equal", "two_values", "short", "k1", "k_all", "clustered", "few_ev"])
+def test_fast_path_adversarial(case, impl, monkeypatch):
+    """n = 2^17 (sample-bucket fast path + exact fallback): heavy ties, fewer evictable blocks
+    than k, k = 1, k = n, keys clustered in one bucket, very few evictable blocks."""
+    import paper_2504_03651_b200 as K
+    monkeypatch.setenv("KVA_EVICT_IMPL", impl)
+    n = 1 << 17
+    rng = np.random.default_rng(sum(map(ord, case)))
+    keys = rng.integers(0, 1 << 62, n, dtype=np.uint64)
+    k = 5000
+    if case == "all_equal":
+        keys[:] = np.uint64(12345)
+    elif case == "two_values":
+        keys = np.where(rng.random(n) < 0.5, np.uint64(7), np.uint64(9)).astype(np.uint64)
+    elif case == "short":
+        keys[rng.random(n) < 0.97] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        k = 10000
+    elif case == "k1":
+        k = 1
+    elif case == "k_all":
+        k = n
+    elif case == "clustered":
+        keys = (np.uint64(1 << 40) + rng.integers(0, 3000, n).astype(np.uint64)).astype(np.uint64)
+    elif case == "few_ev":
+        keys[:] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        keys[rng.choice(n, 37, replace=False)] = rng.integers(0, 100, 37).astype(np.uint64)
+        k = 20
+    d = torch.from_numpy(keys.view(np.int64)).cuda()
+    ids, nsel = K.evict_select(d, k)
+    s, ref = oracle.evict_select(keys, k)
+    assert nsel == len(ref)
+    assert np.array_equal(ids.cpu().numpy(), ref)

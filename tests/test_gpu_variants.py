@@ -59,3 +59,26 @@ def test_overlap_modes_bitexact(tmp_path):
                                  {"KVA_POLY": "0"}, {"KVA_POLY": "4"}, {"KVA_PDL": "0"}])
 def test_decode_impl_parity(env, tmp_path):
     _run(env, "dec_" + "_".join(env.values()), tmp_path)
+
+
+def test_evict_select_coop_only_matches_fast_path(tmp_path):
+    """The cooperative kernel (default) and the sample-bucket path (KVA_EVICT_IMPL=fast) give the
+    oracle's eviction order on the full-size `evict` config and its straddle variant."""
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, workloads as W, paper_2504_03651_b200 as K
+for straddle in (False, True):
+    ev = W.make_evict(straddle=straddle)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).cuda()
+    keys = K.evict_keys(t(ev.state, np.uint8), t(ev.rc, np.int32), t(ev.lat, np.int32), t(ev.depth, np.int16))
+    ids, n = K.evict_select(keys, ev.k)
+    _, rk = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    _, rids = oracle.evict_select(rk, ev.k)
+    assert np.array_equal(ids.cpu().numpy(), rids), straddle
+print("OK")
+""" % ROOT
+    for env in ({}, {"KVA_EVICT_IMPL": "fast"}):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
