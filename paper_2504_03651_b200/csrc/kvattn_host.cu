@@ -298,10 +298,13 @@ static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
       return fail(KVA_ERR_INVALID, "request %d: ctx %d > max_blocks*16", i, ctx);
     const int need_blocks = mode == 0 ? cdiv(ctx, kBlock) : cdiv(ctx - ql, kBlock);
     const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
-    for (int k = 0; k < need_blocks; ++k)
-      if (row[k] < 0 || row[k] >= nb)
-        return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid (num_blocks %d)", i, k,
-                    row[k], nb);
+    uint32_t bad = 0;  // branch-free (vectorised) range check; the slow path names the entry
+    for (int k = 0; k < need_blocks; ++k) bad |= (uint32_t)row[k] >= (uint32_t)nb;
+    if (bad)
+      for (int k = 0; k < need_blocks; ++k)
+        if (row[k] < 0 || row[k] >= nb)
+          return fail(KVA_ERR_INVALID, "request %d: block_table[%d] = %d invalid (num_blocks %d)", i, k,
+                      row[k], nb);
   }
   if (b->group_of) {
     if (b->num_groups > 0 && !b->group_prefix_blocks)
@@ -318,9 +321,11 @@ static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
       if (first[gi] < 0) first[gi] = i;
       const int32_t *a = b->block_table_host + (int64_t)i * b->max_blocks;
       const int32_t *c = b->block_table_host + (int64_t)first[gi] * b->max_blocks;
-      for (int k = 0; k < np; ++k)
-        if (a[k] != c[k] || a[k] < 0 || a[k] >= nb)
-          return fail(KVA_ERR_GROUP, "request %d: prefix block %d differs from group %d's", i, k, gi);
+      // (entries are in range: the prefix lies inside the resident part checked above)
+      if (std::memcmp(a, c, (size_t)np * sizeof(int32_t)) != 0)
+        for (int k = 0; k < np; ++k)
+          if (a[k] != c[k])
+            return fail(KVA_ERR_GROUP, "request %d: prefix block %d differs from group %d's", i, k, gi);
     }
   }
   return KVA_OK;
