@@ -102,7 +102,14 @@ kva_status kv_pool_sync(kva_pool *pool, kva_stream_t stream);
  * group_prefix_blocks[g] table entries must equal the group's blocks (those of its first
  * member) and every member's queries must lie after the prefix, else KVA_ERR_GROUP.
  * Grouping never changes results (reading #7); it changes how blocks are read.
+ * Nested groups (multi-level cascade; e.g. a system prompt shared by every
+ * offline task and a document shared by a subset): group_parent[g] = -1 or a group p < g with
+ * group_prefix_blocks[p] <= group_prefix_blocks[g] whose blocks are the first
+ * group_prefix_blocks[p] blocks of g; a request names its DEEPEST group.  Decode-class members
+ * then read each level's blocks once per (level, kv head), stacked over every member below it
+ * (at most KVA_MAX_CASCADE = 4 levels).  group_parent = NULL: every group is a root.
  * ------------------------------------------------------------------------------------ */
+enum { KVA_MAX_CASCADE = 4 };
 enum { KVA_ONLINE_DECODE = 0, KVA_OFFLINE_PREFILL = 1, KVA_OFFLINE_DECODE = 2,
        KVA_ONLINE_PREFILL = 3 };
 enum { KVA_OUT_BF16 = 0, KVA_OUT_F32 = 1 };
@@ -123,6 +130,7 @@ typedef struct {
   int32_t num_groups;
   const int32_t *group_prefix_blocks; /* host [num_groups] */
   float sm_scale;                   /* <= 0 -> 1/sqrt(head_dim) (reading #1) */
+  const int32_t *group_parent;      /* host [num_groups], -1 = root (nullable = all roots) */
 } kva_batch_desc;
 
 /* Host-only descriptor check (no device work): mode 0 = as hybrid_attention validates it

@@ -44,10 +44,14 @@ struct TileItem {
 };
 
 // One request whose partials are merged (a6): each of its rows r < rows is merged for every
-// kv head h (q head = h * g + r % g) from the cascade-prefix slot casc_slot + h*casc_hstride + r
-// (casc_slot < 0: none) and the split slots split_slot + (h * nsplit + s) * rows + r.
+// kv head h (q head = h * g + r % g) from the cascade-prefix slots casc_slot[l] +
+// h*casc_hstride[l] + r (l < n_casc, one per nested group level) and the split slots
+// split_slot + (h * nsplit + s) * rows + r.
+// Nested shared-prefix groups: one cascade partial per level (outermost first).
+constexpr int kMaxCascade = 4;
 struct MergeReq {
-  int32_t q_row0, rows, casc_slot, casc_hstride, split_slot, nsplit, pad0, pad1;
+  int32_t q_row0, rows, split_slot, nsplit, n_casc, pad0, pad1, pad2;
+  int32_t casc_slot[kMaxCascade], casc_hstride[kMaxCascade];
 };
 
 // Request list + exclusive prefix of work units (splits or rows) per request, handed to the

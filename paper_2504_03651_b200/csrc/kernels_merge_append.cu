@@ -13,7 +13,8 @@ using namespace dev;
 // a6: for each output (row, q-head) with partials {(O_j, lse_j)}:
 //   lse = ln sum_j e^{lse_j},  O = sum_j e^{lse_j - lse} O_j.
 // One warp per (request row, kv head); each lane owns D/32 contiguous channels (16-B / 8-B
-// vectors).  Partials in order: the cascade prefix slot (if any), then the key splits.
+// vectors).  Partials in order: the cascade prefix slots (one per nested level), then the key
+// splits.
 // ---------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
@@ -33,11 +34,12 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
   }
   const MergeReq mq = reqs[lo];
   const int r = m - pre[lo];
-  const bool casc = mq.casc_slot >= 0;
-  const int n = (int)casc + mq.nsplit;
-  const int casc_sl = mq.casc_slot + h * mq.casc_hstride + r;
+  const int nc = mq.n_casc;
+  const int n = nc + mq.nsplit;
   const int split0 = mq.split_slot + h * mq.nsplit * mq.rows + r;
-  auto slot_of = [&](int i) { return casc && i == 0 ? casc_sl : split0 + (i - (int)casc) * mq.rows; };
+  auto slot_of = [&](int i) {
+    return i < nc ? mq.casc_slot[i] + h * mq.casc_hstride[i] + r : split0 + (i - nc) * mq.rows;
+  };
   float L = -CUDART_INF_F;
   for (int i = lane; i < n; i += 32) L = fmaxf(L, p.part_lse[slot_of(i)]);
 #pragma unroll

@@ -307,25 +307,40 @@ static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
                       row[k], nb);
   }
   if (b->group_of) {
-    if (b->num_groups > 0 && !b->group_prefix_blocks)
+    const int G = std::max(b->num_groups, 0);
+    if (G > 0 && !b->group_prefix_blocks)
       return fail(KVA_ERR_INVALID, "group_prefix_blocks required");
-    std::vector<int> first(std::max(b->num_groups, 0), -1);
+    for (int gi = 0; gi < G; ++gi) {
+      if (b->group_prefix_blocks[gi] < 0) return fail(KVA_ERR_GROUP, "group %d: negative prefix", gi);
+      if (!b->group_parent) continue;
+      const int pa = b->group_parent[gi];
+      if (pa < -1 || pa >= gi) return fail(KVA_ERR_GROUP, "group %d: parent %d not an earlier group", gi, pa);
+      if (pa >= 0 && b->group_prefix_blocks[pa] > b->group_prefix_blocks[gi])
+        return fail(KVA_ERR_GROUP, "group %d: shorter prefix than its parent %d", gi, pa);
+      int depth = 1;
+      for (int x = pa; x >= 0; x = b->group_parent[x]) ++depth;
+      if (depth > kMaxCascade) return fail(KVA_ERR_UNSUPPORTED, "group %d: nesting deeper than %d", gi, kMaxCascade);
+    }
+    std::vector<int> first(G, -1);  // first request whose chain contains the group
     for (int i = 0; i < b->num_reqs; ++i) {
       const int gi = b->group_of[i];
       if (gi < 0) continue;
-      if (gi >= b->num_groups) return fail(KVA_ERR_GROUP, "request %d: group %d out of range", i, gi);
+      if (gi >= G) return fail(KVA_ERR_GROUP, "request %d: group %d out of range", i, gi);
       const int np = b->group_prefix_blocks[gi];
-      if (np < 0) return fail(KVA_ERR_GROUP, "group %d: negative prefix", gi);
       if (b->ctx_len[i] - qlen(b, i) < np * kBlock)
         return fail(KVA_ERR_GROUP, "request %d: queries/appends inside group %d's prefix", i, gi);
-      if (first[gi] < 0) first[gi] = i;
       const int32_t *a = b->block_table_host + (int64_t)i * b->max_blocks;
-      const int32_t *c = b->block_table_host + (int64_t)first[gi] * b->max_blocks;
+      // every level of the chain: the first n_l entries equal the level's blocks
       // (entries are in range: the prefix lies inside the resident part checked above)
-      if (std::memcmp(a, c, (size_t)np * sizeof(int32_t)) != 0)
-        for (int k = 0; k < np; ++k)
-          if (a[k] != c[k])
-            return fail(KVA_ERR_GROUP, "request %d: prefix block %d differs from group %d's", i, k, gi);
+      for (int l = gi; l >= 0; l = b->group_parent ? b->group_parent[l] : -1) {
+        if (first[l] < 0) first[l] = i;
+        const int32_t *c = b->block_table_host + (int64_t)first[l] * b->max_blocks;
+        const int nl = b->group_prefix_blocks[l];
+        if (std::memcmp(a, c, (size_t)nl * sizeof(int32_t)) != 0)
+          for (int k = 0; k < nl; ++k)
+            if (a[k] != c[k])
+              return fail(KVA_ERR_GROUP, "request %d: prefix block %d differs from group %d's", i, k, l);
+      }
     }
   }
   return KVA_OK;
@@ -597,37 +612,46 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
   auto grp = [&](int i) { return b->group_of ? b->group_of[i] : -1; };
   auto dec_class = [&](int i) { return qlen(b, i) * g <= kDecodeRows; };
-  // --- cascade tiles: decode-class members of each group, stacked along M ---
-  std::vector<int> member_idx(R, -1), first_member(G, -1);
-  std::vector<std::vector<int64_t>> casc_base(G);
+  // --- cascade tiles: decode-class members of each group, stacked along M; a nested group
+  // (level) covers keys [n_parent*16, n_g*16) and stacks every member at or below it ---
+  auto parent = [&](int gi) { return b->group_parent ? b->group_parent[gi] : -1; };
+  auto in_chain = [&](int i, int gi) {
+    for (int l = grp(i); l >= 0; l = parent(l))
+      if (l == gi) return true;
+    return false;
+  };
+  std::vector<int> first_member(G, -1);
+  std::vector<std::vector<int>> members(G);  // decode-class requests at or below the group
+  std::vector<std::vector<int>> member_off(G);  // their token offsets in the group's row list
+  std::vector<int64_t> casc_base(G, -1);
   std::vector<int> group_rows(G, 0), list_off(G, 0);
-  for (int i = 0; i < R; ++i) {
-    const int gi = grp(i);
-    if (gi < 0) continue;
-    if (first_member[gi] < 0) first_member[gi] = i;
-  }
+  for (int i = 0; i < R; ++i)
+    for (int l = grp(i); l >= 0; l = parent(l))
+      if (first_member[l] < 0) first_member[l] = i;
   for (int gi = 0; gi < G; ++gi) {
     list_off[gi] = (int)pb.row_list.size();
     for (int i = 0; i < R; ++i) {
-      if (grp(i) != gi || !dec_class(i)) continue;
-      member_idx[i] = (int)pb.row_list.size() - list_off[gi];
+      if (grp(i) < 0 || !dec_class(i) || !in_chain(i, gi)) continue;
+      members[gi].push_back(i);
+      member_off[gi].push_back((int)pb.row_list.size() - list_off[gi]);
       for (int j = 0; j < qlen(b, i); ++j) pb.row_list.push_back(b->q_indptr[i] + j);
     }
     const int ntok = (int)pb.row_list.size() - list_off[gi];
     group_rows[gi] = ntok * g;
     if (ntok == 0) continue;
     const int np = b->group_prefix_blocks[gi];
-    casc_base[gi].resize(Hkv);
+    const int kstart = parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] * kBlock : 0;
+    casc_base[gi] = pb.n_slots;
     for (int h = 0; h < Hkv; ++h) {
-      casc_base[gi][h] = pb.n_slots;
       for (int m0 = 0; m0 < group_rows[gi]; m0 += kTileM) {
+        if (np * kBlock <= kstart) break;  // a level with no blocks of its own: no tile
         TileItem t{};
         t.row_src = list_off[gi];
         t.r0 = m0;
         t.n_rows = std::min(kTileM, group_rows[gi] - m0);
         t.kv_head = h;
         t.table_row = first_member[gi];
-        t.k0 = 0;
+        t.k0 = kstart;
         t.k1 = np * kBlock;
         t.pos0 = 0;
         t.slot = (int32_t)(pb.n_slots + m0);
@@ -638,6 +662,11 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
       pb.n_slots += group_rows[gi];
     }
   }
+  // the merge lists a level only if it has a tile (blocks of its own)
+  auto level_has_tile = [&](int gi) {
+    const int kstart = parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] * kBlock : 0;
+    return b->group_prefix_blocks[gi] * kBlock > kstart;
+  };
   // --- per request ---
   {
     size_t nd = 0, nm = 0;
@@ -652,7 +681,8 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     pb.mrg_pre.reserve(nm + 1);
   }
   int64_t kv_tokens = 0, dec_keys = 0, dec_rows = 0;
-  for (int gi = 0; gi < G; ++gi) kv_tokens += (int64_t)b->group_prefix_blocks[gi] * kBlock;
+  for (int gi = 0; gi < G; ++gi)  // each level's own blocks once
+    kv_tokens += (int64_t)(b->group_prefix_blocks[gi] - (parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] : 0)) * kBlock;
   for (int i = 0; i < R; ++i) {
     const int ql = qlen(b, i), ctx = b->ctx_len[i], gi = grp(i), q0 = b->q_indptr[i];
     const int np = gi >= 0 ? b->group_prefix_blocks[gi] : 0;
@@ -660,7 +690,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     // sum_{j<ql} (ctx - ql + j + 1) visible keys per q-head
     pb.stats.flops += ((int64_t)ql * (ctx - ql + 1) + (int64_t)ql * (ql - 1) / 2) * Hq * 4 * d;
     if (dec_class(i)) {
-      const bool cascaded = gi >= 0 && member_idx[i] >= 0;
+      const bool cascaded = gi >= 0;
       const int kb = cascaded ? np * kBlock : 0;
       const int nsplit = cdiv(ctx - kb, kSplitKeys);
       const bool direct = !cascaded && nsplit == 1;
@@ -685,9 +715,16 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
         MergeReq mq{};
         mq.q_row0 = q0;
         mq.rows = rows;
-        // casc_base[gi][h] = casc_base[gi][0] + h * group_rows[gi]
-        mq.casc_slot = cascaded ? (int32_t)(casc_base[gi][0] + (int64_t)member_idx[i] * g) : -1;
-        mq.casc_hstride = cascaded ? group_rows[gi] : 0;
+        mq.n_casc = 0;
+        // level l's partial of (head h, row r): casc_base[l] + h * group_rows[l] + off * g + r
+        for (int l = cascaded ? gi : -1; l >= 0; l = parent(l)) {
+          if (!level_has_tile(l)) continue;
+          const auto &mv = members[l];
+          const size_t pos = std::lower_bound(mv.begin(), mv.end(), i) - mv.begin();
+          mq.casc_slot[mq.n_casc] = (int32_t)(casc_base[l] + (int64_t)member_off[l][pos] * g);
+          mq.casc_hstride[mq.n_casc] = group_rows[l];
+          ++mq.n_casc;
+        }
         mq.split_slot = (int32_t)base;
         mq.nsplit = nsplit;
         pb.mrg.push_back(mq);

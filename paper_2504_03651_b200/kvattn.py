@@ -41,7 +41,8 @@ class BatchDesc(ctypes.Structure):
                 ("ctx_len", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
                 ("block_table_host", ctypes.c_void_p), ("max_blocks", ctypes.c_int32),
                 ("group_of", ctypes.c_void_p), ("num_groups", ctypes.c_int32),
-                ("group_prefix_blocks", ctypes.c_void_p), ("sm_scale", ctypes.c_float)]
+                ("group_prefix_blocks", ctypes.c_void_p), ("sm_scale", ctypes.c_float),
+                ("group_parent", ctypes.c_void_p)]
 
 
 class BlockMeta(ctypes.Structure):
@@ -219,6 +220,8 @@ class Batch:
                          else np.ascontiguousarray(batch["group_of"], np.int32))
         gpb = batch.get("group_prefix_blocks")
         self.group_prefix_blocks = np.ascontiguousarray(gpb if gpb is not None else [], np.int32)
+        gpa = batch.get("group_parent")
+        self.group_parent = None if gpa is None else np.ascontiguousarray(gpa, np.int32)
         self.table_dev = (torch.from_numpy(self.table_host.copy()).to(device)
                           if device is not None else torch.from_numpy(self.table_host.copy()))
         self.num_reqs = len(self.ctx_len)
@@ -235,7 +238,7 @@ class Batch:
                       a(self.req_type), a(self.q_indptr), a(self.ctx_len), self.table_dev.data_ptr(),
                       a(self.table_host), self.table_host.shape[1], a(self.group_of),
                       len(self.group_prefix_blocks), a(self.group_prefix_blocks) if len(self.group_prefix_blocks) else None,
-                      self.sm_scale)
+                      self.sm_scale, a(self.group_parent) if self.group_parent is not None and len(self.group_parent) else None)
         self._desc = d  # keep alive
         return d
 

@@ -50,6 +50,7 @@ class Config:
     reqs: list = field(default_factory=list)
     group_prefix_blocks: list = field(default_factory=list)
     spiky: bool = False
+    group_parent: list = field(default_factory=list)  # nested groups: parent index or -1
 
 
 def _cfg_tiny():
@@ -116,8 +117,12 @@ def get_config(name: str) -> Config:
     return CONFIGS[name]()
 
 
-def custom_config(name, Hq, Hkv, d, seed, reqs, group_prefix_blocks, spiky=False) -> Config:
-    return Config(name, Hq, Hkv, d, seed, list(reqs), list(group_prefix_blocks), spiky)
+def custom_config(name, Hq, Hkv, d, seed, reqs, group_prefix_blocks, spiky=False, group_parent=None) -> Config:
+    return Config(name, Hq, Hkv, d, seed, list(reqs), list(group_prefix_blocks), spiky, list(group_parent or []))
+
+
+def _parent(cfg: Config, g: int) -> int:
+    return cfg.group_parent[g] if cfg.group_parent else -1
 
 
 @dataclass
@@ -140,7 +145,8 @@ class Workload:
 
 def _blocks_used(cfg: Config):
     """Blocks the step touches: prefixes + private blocks up to ctx (incl. appended)."""
-    n = sum(cfg.group_prefix_blocks)
+    n = sum(np_ - (cfg.group_prefix_blocks[_parent(cfg, g)] if _parent(cfg, g) >= 0 else 0)
+            for g, np_ in enumerate(cfg.group_prefix_blocks))
     for r in cfg.reqs:
         start = cfg.group_prefix_blocks[r.group] * BLOCK if r.group >= 0 else 0
         n += math.ceil(r.ctx / BLOCK) - start // BLOCK
@@ -184,9 +190,17 @@ def make_workload(cfg: Config | str, device="cpu", rank: int = 0, world: int = 1
     table = np.full((R, max_blocks), -1, np.int32)
     # group prefixes first
     gblocks = []
-    for np_ in cfg.group_prefix_blocks:
-        gblocks.append(perm[nxt:nxt + np_].copy())
-        nxt += np_
+    for g, np_ in enumerate(cfg.group_prefix_blocks):
+        p = _parent(cfg, g)
+        if p >= 0:  # nested group: the parent's blocks, then its own
+            if p >= g or cfg.group_prefix_blocks[p] > np_:
+                raise ValueError("group_parent must point to an earlier group with a shorter prefix")
+            npp = cfg.group_prefix_blocks[p]
+            gblocks.append(np.concatenate([gblocks[p][:npp], perm[nxt:nxt + np_ - npp]]))
+            nxt += np_ - npp
+        else:
+            gblocks.append(perm[nxt:nxt + np_].copy())
+            nxt += np_
     # resident private blocks per request (positions [start_private, ctx - q_len))
     for i, r in enumerate(cfg.reqs):
         npfx = cfg.group_prefix_blocks[r.group] if r.group >= 0 else 0
@@ -220,7 +234,9 @@ def make_workload(cfg: Config | str, device="cpu", rank: int = 0, world: int = 1
         return blks[ts // BLOCK], ts % BLOCK
 
     for gi, np_ in enumerate(cfg.group_prefix_blocks):
-        bi, oi = slots(gblocks[gi], np_ * BLOCK)
+        p = _parent(cfg, gi)
+        t0 = cfg.group_prefix_blocks[p] * BLOCK if p >= 0 else 0  # the parent filled its part
+        bi, oi = slots(gblocks[gi], np_ * BLOCK, t0)
         _fill(k_pool, bi, oi, gv, Hkv, d, device)
         _fill(v_pool, bi, oi, gv, Hkv, d, device)
     for i, r in enumerate(cfg.reqs):
@@ -255,6 +271,7 @@ def make_workload(cfg: Config | str, device="cpu", rank: int = 0, world: int = 1
         block_table=table,
         group_of=np.array([r.group for r in cfg.reqs], np.int32),
         group_prefix_blocks=np.array(cfg.group_prefix_blocks, np.int32),
+        group_parent=np.array(cfg.group_parent, np.int32) if cfg.group_parent else None,
         num_blocks=num_blocks,
         sm_scale=0.0,
     )
