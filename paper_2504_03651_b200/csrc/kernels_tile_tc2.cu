@@ -257,11 +257,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       auto qk = [&](int t, int j) {  // S_t = Q_t K_j^T
         const int KT = KT0 + j, s = KT & 1;
         if (lane == 0) {
+          if (!(p.debug_flags & 4)) {  // diagnostics: 4 = QK MMAs not issued (pipeline study)
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint64_t a = sdesc(q_base + t * QBYTES + (k >> 2) * (M * 128) + (k & 3) * 32, 16, 1024);
-            const uint64_t b = sdesc(k_base + s * TBYTES + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
-            umma_ss(tmem + COL_S[t], a, b, ID_QK, k > 0 ? 1u : 0u);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint64_t a = sdesc(q_base + t * QBYTES + (k >> 2) * (M * 128) + (k & 3) * 32, 16, 1024);
+              const uint64_t b = sdesc(k_base + s * TBYTES + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
+              umma_ss(tmem + COL_S[t], a, b, ID_QK, k > 0 ? 1u : 0u);
+            }
           }
           umma_commit(&bar_s[t]);
         }
@@ -290,10 +292,12 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         fence_after();
         if (lane == 0) {
+          if (!(p.debug_flags & 2)) {  // diagnostics: 2 = PV MMAs not issued (pipeline study)
 #pragma unroll
-          for (int k = 0; k < N / 16; ++k) {
-            const uint64_t b = sdesc(v_base + s * TBYTES + k * 2048, N * 128, 1024);
-            umma_ts(tmem + COL_O[t], tmem + COL_S[t] + k * 8, b, ID_PV, (j > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < N / 16; ++k) {
+              const uint64_t b = sdesc(v_base + s * TBYTES + k * 2048, N * 128, 1024);
+              umma_ts(tmem + COL_O[t], tmem + COL_S[t] + k * 8, b, ID_PV, (j > 0 || k > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&bar_o[t]);
         }
