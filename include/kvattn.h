@@ -341,6 +341,18 @@ kva_status kva_group_batch(kva_prefix_index *ix, int32_t num_reqs, const int32_t
                            const int64_t *n_tokens, const int32_t *prefix_limit_blocks,
                            int32_t min_blocks, int32_t *group_of, int32_t *group_prefix_blocks,
                            int32_t *num_groups);
+/* kva_group_batch_nested: nested groups for the multi-level cascade (group_parent of the batch
+ * descriptor).  Level l (thresholds level_min_blocks[] strictly increasing) groups requests whose
+ * first level_min_blocks[l] blocks are the same entries; a group's prefix is the deepest entry
+ * all its members share (capped by every usable_i); a group whose prefix does not extend its
+ * parent's is dropped (its members stay in the parent); group_parent[g] = the nearest kept group
+ * above (-1 at the top).  Groups are numbered level by level in order of first member (parents
+ * precede children); group_of[i] = request i's deepest group.  Output arrays need R entries. */
+kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t num_reqs, const int32_t *const *tokens,
+                                  const int64_t *n_tokens, const int32_t *prefix_limit_blocks,
+                                  int32_t n_levels, const int32_t *level_min_blocks,
+                                  int32_t *group_of, int32_t *group_prefix_blocks,
+                                  int32_t *group_parent, int32_t *num_groups);
 
 /* ---- diagnostics (not part of the hot path) ----
  * kva_diag_occupy: enqueue n_ctas CTAs that each hold smem_bytes of shared memory and spin

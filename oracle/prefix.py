@@ -76,3 +76,43 @@ def group_batch(index: BruteIndex, token_lists, prefix_limit_blocks=None, min_bl
             group_of[j] = len(prefixes)
         prefixes.append(depth)
     return group_of, prefixes
+
+
+def group_batch_nested(index: BruteIndex, token_lists, level_min_blocks, prefix_limit_blocks=None):
+    """Definition (include/kvattn.h kva_group_batch_nested) by brute force over token tuples."""
+    R = len(token_lists)
+    usable = []
+    for i, t in enumerate(token_lists):
+        u = len(index.lookup(list(t)))
+        if prefix_limit_blocks is not None:
+            u = min(u, max(0, int(prefix_limit_blocks[i])))
+        usable.append(u)
+    cur = [-1] * R
+    prefixes, parents = [], []
+    for m in level_min_blocks:
+        assign = []
+        done = set()
+        for i in range(R):
+            if i in done or usable[i] < m:
+                continue
+            head = tuple(token_lists[i][: m * B])
+            mem = [j for j in range(R) if usable[j] >= m and tuple(token_lists[j][: m * B]) == head]
+            done.update(mem)
+            if len(mem) < 2:
+                continue
+            depth = min(usable[j] for j in mem)
+            while depth > m:
+                ref = tuple(token_lists[mem[0]][: depth * B])
+                if all(tuple(token_lists[j][: depth * B]) == ref for j in mem):
+                    break
+                depth -= 1
+            par = cur[mem[0]]
+            if par >= 0 and depth <= prefixes[par]:
+                continue
+            g = len(prefixes)
+            prefixes.append(depth)
+            parents.append(par)
+            assign += [(j, g) for j in mem]
+        for j, g in assign:
+            cur[j] = g
+    return cur, prefixes, parents

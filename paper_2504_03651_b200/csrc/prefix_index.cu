@@ -237,3 +237,68 @@ extern "C" kva_status kva_group_batch(kva_prefix_index *ix, int32_t R, const int
   *num_groups = G;
   return KVA_OK;
 }
+
+// Nested grouping (multi-level cascade, NEXT-4): level l groups requests whose first
+// level_min_blocks[l] blocks are the same entries (thresholds strictly increasing); a level-l
+// group's prefix is the deepest entry all its members share (capped by every usable_i); a
+// group whose prefix does not extend its parent's is dropped (its members stay in the parent);
+// group_parent links each group to the nearest kept group above it.  Groups are numbered
+// level by level, in order of first member, so parents precede children.
+extern "C" kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t R, const int32_t *const *tokens,
+                                             const int64_t *n_tokens, const int32_t *prefix_limit_blocks,
+                                             int32_t n_levels, const int32_t *level_min_blocks,
+                                             int32_t *group_of, int32_t *group_prefix_blocks,
+                                             int32_t *group_parent, int32_t *num_groups) {
+  if (!ix || R < 0 || !group_of || !num_groups || n_levels < 1 || !level_min_blocks ||
+      (R > 0 && (!tokens || !n_tokens)))
+    return px_fail(KVA_ERR_INVALID, "bad argument");
+  for (int l = 0; l < n_levels; ++l)
+    if (level_min_blocks[l] < 1 || (l > 0 && level_min_blocks[l] <= level_min_blocks[l - 1]))
+      return px_fail(KVA_ERR_INVALID, "level_min_blocks must be >= 1 and strictly increasing");
+  std::vector<std::vector<int32_t>> paths(R);
+  std::vector<int64_t> usable(R, 0);
+  for (int32_t i = 0; i < R; ++i) {
+    if (n_tokens[i] < 0 || (n_tokens[i] > 0 && !tokens[i])) return px_fail(KVA_ERR_INVALID, "bad tokens");
+    ix->walk(tokens[i], n_tokens[i], paths[i]);
+    usable[i] = (int64_t)paths[i].size();
+    if (prefix_limit_blocks) usable[i] = std::min<int64_t>(usable[i], std::max(0, prefix_limit_blocks[i]));
+  }
+  std::vector<int32_t> cur(R, -1);  // deepest kept group of each request so far
+  int32_t G = 0;
+  for (int l = 0; l < n_levels; ++l) {
+    const int32_t m = level_min_blocks[l];
+    std::unordered_map<int32_t, std::vector<int32_t>> cls;
+    std::vector<int32_t> order;
+    for (int32_t i = 0; i < R; ++i) {
+      if (usable[i] < m) continue;
+      const int32_t key = paths[i][m - 1];
+      auto &v = cls[key];
+      if (v.empty()) order.push_back(key);
+      v.push_back(i);
+    }
+    std::vector<std::pair<int32_t, int32_t>> assign;  // (request, group) applied after the level
+    for (int32_t key : order) {
+      const auto &mem = cls[key];
+      if (mem.size() < 2) continue;
+      int64_t depth = m, lim = INT64_MAX;
+      for (int32_t i : mem) lim = std::min(lim, usable[i]);
+      while (depth < lim) {
+        const int32_t nd = paths[mem[0]][depth];
+        bool same = true;
+        for (int32_t i : mem) same = same && paths[i][depth] == nd;
+        if (!same) break;
+        ++depth;
+      }
+      const int32_t par = cur[mem[0]];  // every member shares the level above (identical prefix)
+      if (par >= 0 && group_prefix_blocks && depth <= group_prefix_blocks[par]) continue;  // no own blocks
+      if (group_prefix_blocks) group_prefix_blocks[G] = (int32_t)depth;
+      if (group_parent) group_parent[G] = par;
+      for (int32_t i : mem) assign.emplace_back(i, G);
+      ++G;
+    }
+    for (auto &a : assign) cur[a.first] = a.second;
+  }
+  for (int32_t i = 0; i < R; ++i) group_of[i] = cur[i];
+  *num_groups = G;
+  return KVA_OK;
+}

@@ -76,7 +76,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
            "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step",
            "kva_prefix_index_create", "kva_prefix_index_destroy", "kva_prefix_insert", "kva_prefix_lookup",
-           "kva_prefix_remove", "kva_prefix_size", "kva_group_batch"]
+           "kva_prefix_remove", "kva_prefix_size", "kva_group_batch", "kva_group_batch_nested"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
 
 _lib = None
@@ -133,6 +133,7 @@ def load(build_if_missing: bool = True):
         "kva_prefix_remove": ([P, P, i64], ctypes.c_int),
         "kva_prefix_size": ([P, P], ctypes.c_int),
         "kva_group_batch": ([P, i32, P, P, P, i32, P, P, P], ctypes.c_int),
+        "kva_group_batch_nested": ([P, i32, P, P, P, i32, P, P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -509,6 +510,23 @@ class PrefixIndex:
                                       None if lim is None else lim.ctypes.data, int(min_blocks),
                                       gof.ctypes.data, gpb.ctypes.data, ctypes.byref(G)))
         return gof[:R], gpb[: G.value]
+
+    def group_batch_nested(self, token_lists, level_min_blocks, prefix_limit_blocks=None):
+        """-> (group_of[R], group_prefix_blocks[G], group_parent[G]) for nested groups."""
+        arrs = [self._i32(t) for t in token_lists]
+        R = len(arrs)
+        ptrs = (ctypes.c_void_p * max(1, R))(*[a.ctypes.data for a in arrs])
+        lens = np.array([a.size for a in arrs] or [0], np.int64)
+        lim = None if prefix_limit_blocks is None else self._i32(prefix_limit_blocks)
+        lv = self._i32(level_min_blocks)
+        gof = np.full(max(1, R), -1, np.int32)
+        gpb = np.zeros(max(1, R), np.int32)
+        gpa = np.zeros(max(1, R), np.int32)
+        G = ctypes.c_int32()
+        _check(load().kva_group_batch_nested(self.handle, R, ptrs, lens.ctypes.data,
+                                             None if lim is None else lim.ctypes.data, lv.size, lv.ctypes.data,
+                                             gof.ctypes.data, gpb.ctypes.data, gpa.ctypes.data, ctypes.byref(G)))
+        return gof[:R], gpb[: G.value], gpa[: G.value]
 
     def close(self):
         if self.handle:

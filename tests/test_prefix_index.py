@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
-from oracle.prefix import BruteIndex, group_batch as brute_group
+from oracle.prefix import BruteIndex, group_batch as brute_group, group_batch_nested as oracle_nested
 import paper_2504_03651_b200 as K
 
 B = 16
@@ -129,3 +129,55 @@ def test_groups_satisfy_cascade_precondition():
              group_prefix_blocks=gpb.astype(np.int32), num_blocks=nid)
     assert oracle.validate(b) == oracle.OK
     assert list(gpb) == [5, 8] or list(gpb) == [8, 5]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_group_batch_nested_random(seed):
+    """Nested grouping (system prompt -> document -> section) equals the brute-force definition,
+    and the output satisfies the descriptor's nesting rules (parents first, longer prefixes)."""
+    rng = np.random.default_rng(700 + seed)
+    ix, ref = K.PrefixIndex(), BruteIndex()
+    system = rng.integers(0, 1000, 2 * B)
+    docs = [np.concatenate([system, rng.integers(1000, 9000, int(rng.integers(1, 4)) * B)]) for _ in range(3)]
+    secs = [np.concatenate([docs[int(rng.integers(0, 3))], rng.integers(9000, 9500, int(rng.integers(1, 3)) * B)])
+            for _ in range(4)]
+    nid = 0
+    for d in docs + secs:
+        hit = list(ix.lookup(d))
+        ids = hit + list(range(nid, nid + len(d) // B - len(hit)))
+        nid += len(d) // B - len(hit)
+        ix.insert(d, ids)
+        ref.insert(list(d), ids)
+    pool = docs + secs
+    reqs = [np.concatenate([pool[int(rng.integers(0, len(pool)))], rng.integers(9900, 9999, int(rng.integers(1, 30)))]).astype(np.int32)
+            for _ in range(int(rng.integers(4, 24)))]
+    for levels in ([1, 3], [2, 4, 6], [1]):
+        g1, p1, a1 = ix.group_batch_nested(reqs, levels)
+        g2, p2, a2 = oracle_nested(ref, [list(r) for r in reqs], levels)
+        assert list(g1) == g2 and list(p1) == p2 and list(a1) == a2
+        for g, (pp, par) in enumerate(zip(p1, a1)):
+            assert par < g and (par < 0 or p1[par] < pp)
+
+
+
+def test_nested_groups_from_token_ids_match_descriptor():
+    """NEXT-3 -> NEXT-4 end to end on the host: token ids of a nested-prefix batch (system prompt
+    -> documents) through the prefix index reproduce the descriptor's group_of /
+    group_prefix_blocks / group_parent that the GPU multi-level cascade consumes."""
+    import workloads as W
+    gpb, parent = [6, 14, 10], [-1, 0, 0]
+    reqs = []
+    for gi in range(3):
+        reqs += [W.ReqSpec(W.OFFLINE_DECODE, gpb[gi] * 16 + 5 + j, 1, gi) for j in range(4)]
+    wl = W.make_workload(W.custom_config("nest", 4, 2, 64, 5, reqs, gpb, group_parent=parent))
+    bt = wl.batch["block_table"]
+    tok = lambda blocks: np.repeat(np.asarray(blocks, np.int32) * 7 + 3, B)  # 16 token ids per block
+    ix = K.PrefixIndex()
+    for gi in range(3):  # the groups' prefix chains are resident (prefix cache)
+        first = next(i for i, r in enumerate(reqs) if r.group == gi)
+        ix.insert(tok(bt[first, : gpb[gi]]), bt[first, : gpb[gi]])
+    toks = [tok(bt[i, : (r.ctx - r.q_len) // B]) for i, r in enumerate(reqs)]
+    lim = [(r.ctx - r.q_len) // B for r in reqs]
+    gof, p, par = ix.group_batch_nested(toks, [1, 7], lim)
+    assert list(gof) == list(wl.batch["group_of"])
+    assert list(p) == gpb and list(par) == parent
