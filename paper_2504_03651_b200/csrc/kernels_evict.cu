@@ -110,27 +110,45 @@ __global__ void manager_keys_kernel(const uint8_t *__restrict__ state, const uin
                                     int64_t n, uint64_t *__restrict__ keys,
                                     unsigned long long *__restrict__ n_active) {
   unsigned int act = 0;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
-       b += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = state[b];
-    const uint32_t r = rc[b];
-    uint64_t key;
-    if (s == 0 || s == 1 || s == 2 || s > 5) {
-      key = kInf;
-    } else {
-      uint64_t code;
-      if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
-      else code = (s == 4) ? 1ull : 0ull;
-      const uint64_t dep = depth ? (uint64_t)depth[b] : 0ull;
-      key = (code << 48) | ((uint64_t)lat[b] << 16) | (0xFFFFull - dep);
-    }
-    keys[b] = key;
+  auto one = [&](uint32_t s, uint32_t r, uint32_t la, uint32_t dp) -> uint64_t {
     act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
+    if (s == 0 || s == 1 || s == 2 || s > 5) return kInf;
+    uint64_t code;
+    if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
+    else code = (s == 4) ? 1ull : 0ull;
+    return (code << 48) | ((uint64_t)la << 16) | (0xFFFFull - (uint64_t)dp);
+  };
+  // 4 blocks per thread with vector loads/stores when the arrays allow it (torch allocations
+  // are 256-B aligned), scalar tail
+  const bool vec = ((reinterpret_cast<uintptr_t>(state) | reinterpret_cast<uintptr_t>(rc) |
+                     reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(keys) |
+                     (depth ? reinterpret_cast<uintptr_t>(depth) : 0)) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s4 = reinterpret_cast<const uint32_t *>(state)[q];
+    const uint4 r4 = reinterpret_cast<const uint4 *>(rc)[q];
+    const uint4 l4 = reinterpret_cast<const uint4 *>(lat)[q];
+    uint2 d4 = make_uint2(0u, 0u);
+    if (depth) d4 = reinterpret_cast<const uint2 *>(depth)[q];
+    const uint64_t k0 = one(s4 & 0xFF, r4.x, l4.x, d4.x & 0xFFFF);
+    const uint64_t k1 = one((s4 >> 8) & 0xFF, r4.y, l4.y, d4.x >> 16);
+    const uint64_t k2 = one((s4 >> 16) & 0xFF, r4.z, l4.z, d4.y & 0xFFFF);
+    const uint64_t k3 = one(s4 >> 24, r4.w, l4.w, d4.y >> 16);
+    reinterpret_cast<ulonglong2 *>(keys)[2 * q] = make_ulonglong2(k0, k1);
+    reinterpret_cast<ulonglong2 *>(keys)[2 * q + 1] = make_ulonglong2(k2, k3);
   }
-  if (n_active) {
+  for (int64_t b = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
+       b += (int64_t)gridDim.x * blockDim.x)
+    keys[b] = one(state[b], rc[b], lat[b], depth ? depth[b] : 0u);
+  if (n_active) {  // one atomic per CTA (a per-warp atomic on one address serialises in L2)
+    __shared__ unsigned int s_act;
+    if (threadIdx.x == 0) s_act = 0u;
+    __syncthreads();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) act += __shfl_xor_sync(0xffffffffu, act, o);
-    if ((threadIdx.x & 31) == 0 && act) atomicAdd(n_active, (unsigned long long)act);
+    if ((threadIdx.x & 31) == 0 && act) atomicAdd(&s_act, act);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_act) atomicAdd(n_active, (unsigned long long)s_act);
   }
 }
 
