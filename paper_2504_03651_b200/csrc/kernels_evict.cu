@@ -725,6 +725,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int tbl = 256 * Sp;
   if (npass > 1)
     for (int e = c * kThreads + tid; e < tbl; e += C * kThreads) B[1][e] = 0u;
+  // pass 0 reads B[0] four columns at a time: zero its padding columns [S, Sp) (the sorters
+  // write columns < S below; the values are masked anyway — keeps initcheck clean)
+  for (int e = c * kThreads + tid; e < 256 * (Sp - S); e += C * kThreads)
+    B[0][(e / (Sp - S)) * Sp + S + e % (Sp - S)] = 0u;
   uint64_t *ka = pk0, *kb = pk1;
   int32_t *ia = pi0, *ib = pi1;
   if (sorter) {  // pass-0 digit counts of this sorter's range
