@@ -97,7 +97,8 @@ struct AttnParams {
 
 // launchers (kernels_*.cu)
 cudaError_t launch_decode(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                          const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s, bool pdl = false);
+                          const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s, bool pdl = false,
+                          const void *tmap_k3 = nullptr, const void *tmap_v3 = nullptr);
 cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                         const TileItem *items, int n_items, cudaStream_t s);
 cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
@@ -111,7 +112,8 @@ struct TileList {
   TileItem item[kInlineTiles];
 };
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                            const TileList &items, int max_ctas, cudaStream_t s);
+                            const TileList &items, int max_ctas, cudaStream_t s,
+                            const void *tmap_v3 = nullptr);
 cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(128, 2)
 // block; masking runs only on blocks that reach the causal diagonal or the split end.  Fewer
 // instructions per byte let fewer SMs saturate HBM, which is what the co-scheduled tile
 // kernel needs (it runs on the remaining SMs).
-template <int D, int NR, int NST, int MINB>
+template <int D, int NR, int NST, int MINB, bool T3>
 __global__ void __launch_bounds__(128, MINB)
     decode_kt_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
                      const __grid_constant__ CUtensorMap tmv, const __grid_constant__ ReqList<DecodeReq> L,
@@ -358,10 +358,15 @@ __global__ void __launch_bounds__(128, MINB)
     mbar_arrive_expect_tx(b, STAGE);
     const int row = id * p.Hkv * kBlock + row_base;
     uint8_t *dst = ws + st * STAGE;
+    if constexpr (T3) {  // 3-D maps: one box = the block-head's two halves, same smem layout
+      tma_load_3d(dst, &tmk, b, 0, row, 0);
+      tma_load_3d(dst + KBYTES, &tmv, b, 0, row, 0);
+    } else {
 #pragma unroll
-    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
+      for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
 #pragma unroll
-    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
+      for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
+    }
   };
 #pragma unroll
   for (int s = 0; s < NST; ++s) {
@@ -591,11 +596,11 @@ __global__ void __launch_bounds__(128, MINB)
   }
 }
 
-template <int D, int NR, int NST, int MINB>
+template <int D, int NR, int NST, int MINB, bool T3 = false>
 static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const void *tmv,
                                    const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;
-  auto kern = decode_kt_kernel<D, NR, NST, MINB>;
+  auto kern = decode_kt_kernel<D, NR, NST, MINB, T3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -638,7 +643,8 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
 }
 
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
-                          const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl) {
+                          const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl,
+                          const void *tmk3, const void *tmv3) {
   if (n <= 0) return cudaSuccess;
   // KVA_DECODE_IMPL=v1: the M = rows kernel (cross-check); default v2 (keys along M).
   // KVA_DECODE_CFG: 0 = 3 stages x 2 CTAs/SM (default), 1 = 2 stages x 3 CTAs/SM.
@@ -661,6 +667,9 @@ cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
     if (p.d == 128) {
       if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s, pdl)
                                : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s, pdl);
+      if (tmk3 && tmv3)  // one 3-D TMA box per block-head (half the TMA operations)
+        return nr1 ? launch_decode_kt<128, 1, 3, 4, true>(p, tmk3, tmv3, L, n, s, pdl)
+                   : launch_decode_kt<128, 2, 3, 2, true>(p, tmk3, tmv3, L, n, s, pdl);
       return nr1 ? launch_decode_kt<128, 1, 3, 4>(p, tmk, tmv, L, n, s, pdl)
                  : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s, pdl);
     }

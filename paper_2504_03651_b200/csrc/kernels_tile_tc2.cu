@@ -134,11 +134,14 @@ __device__ __forceinline__ ItemGeom geom(const TileItem &it, int g) {
 
 }  // namespace tc2
 
-// PP = column pairs (of every 16) whose exp2 runs as a polynomial on the FMA pipe
-template <int D, int PP>
+// PP = column pairs (of every 16) whose exp2 runs as a polynomial on the FMA pipe;
+// V3 = V tiles loaded with one 3-D box per block-head (d = 128): V tile layout
+// [block][half][16 keys][64] (PV reads it with LBO = 2 KB), else [half][128 keys][64]
+template <int D, int PP, bool V3>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     tile_tc2_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
-                    const __grid_constant__ CUtensorMap tmv, const __grid_constant__ TileList L) {
+                    const __grid_constant__ CUtensorMap tmv, const __grid_constant__ TileList L,
+                    const __grid_constant__ CUtensorMap tmv3) {
   const TileItem *items = L.ptr ? L.ptr : L.item;
   const int n_items = L.n;
   using namespace tc2;
@@ -229,12 +232,18 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (KT >= 2) mbar_wait(&bar_ve[s], ((KT >> 1) - 1) & 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&bar_vf[s], nb * KBYTES);
+          if constexpr (V3) {
 #pragma unroll
-          for (int q = 0; q < NBLK; ++q)
-            if (q < nb)
+            for (int q = 0; q < NBLK; ++q)
+              if (q < nb) tma_load_3d(sV + s * TBYTES + q * 4096, &tmv3, &bar_vf[s], 0, rows[q], 0);
+          } else {
 #pragma unroll
-              for (int h = 0; h < HALVES; ++h)
-                tma_load_2d(sV + s * TBYTES + h * (N * 128) + q * 2048, &tmv, &bar_vf[s], h * 64, rows[q]);
+            for (int q = 0; q < NBLK; ++q)
+              if (q < nb)
+#pragma unroll
+                for (int h = 0; h < HALVES; ++h)
+                  tma_load_2d(sV + s * TBYTES + h * (N * 128) + q * 2048, &tmv, &bar_vf[s], h * 64, rows[q]);
+          }
         }
         __syncwarp();
       }
@@ -283,8 +292,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
             const int vr = it.k1 - key0;
             for (int c = lane; c < (N - vr) * HALVES * 8; c += 32) {
               const int key = vr + c / (HALVES * 8), rem = c % (HALVES * 8);
-              *reinterpret_cast<uint4 *>(sV + s * TBYTES + (rem >> 3) * (N * 128) + (key >> 3) * 1024 +
-                                         (key & 7) * 128 + (rem & 7) * 16) = make_uint4(0, 0, 0, 0);
+              const uint32_t off = V3 ? (uint32_t)((key >> 4) * 4096 + (rem >> 3) * 2048 + ((key >> 3) & 1) * 1024)
+                                      : (uint32_t)((rem >> 3) * (N * 128) + (key >> 3) * 1024);
+              *reinterpret_cast<uint4 *>(sV + s * TBYTES + off + (key & 7) * 128 + (rem & 7) * 16) =
+                  make_uint4(0, 0, 0, 0);
             }
             fence_proxy_async();
             __syncwarp();
@@ -295,7 +306,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           if (!(p.debug_flags & 2)) {  // diagnostics: 2 = PV MMAs not issued (pipeline study)
 #pragma unroll
             for (int k = 0; k < N / 16; ++k) {
-              const uint64_t b = sdesc(v_base + s * TBYTES + k * 2048, N * 128, 1024);
+              const uint64_t b = V3 ? sdesc(v_base + s * TBYTES + k * 4096, 2048, 1024)
+                                    : sdesc(v_base + s * TBYTES + k * 2048, N * 128, 1024);
               umma_ts(tmem + COL_O[t], tmem + COL_S[t] + k * 8, b, ID_PV, (j > 0 || k > 0) ? 1u : 0u);
             }
           }
@@ -513,12 +525,12 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
-template <int D, int PP>
+template <int D, int PP, bool V3 = false>
 static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const void *tmv,
-                                     const TileList &L, int max_ctas, cudaStream_t s) {
+                                     const TileList &L, int max_ctas, cudaStream_t s, const void *tmv3) {
   const int n = L.n;
   const size_t smem = 2 * (size_t)tc2::M * D * 2 + 4 * (size_t)tc2::N * D * 2 + 1024;
-  auto kern = tile_tc2_kernel<D, PP>;
+  auto kern = tile_tc2_kernel<D, PP, V3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
@@ -529,12 +541,13 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::max(1, std::min(n, max_ctas > 0 ? max_ctas : nsm));
   kern<<<grid, tc2::THREADS, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
-                                        *reinterpret_cast<const CUtensorMap *>(tmv), L);
+                                        *reinterpret_cast<const CUtensorMap *>(tmv), L,
+                                        *reinterpret_cast<const CUtensorMap *>(V3 ? tmv3 : tmv));
   return cudaGetLastError();
 }
 
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tmv,
-                            const TileList &items, int max_ctas, cudaStream_t s) {
+                            const TileList &items, int max_ctas, cudaStream_t s, const void *tmv3) {
   if (items.n <= 0) return cudaSuccess;
   // KVA_POLY: column pairs (of 16) with exp2 on the FMA pipe: 0 (default), 4 or 6.  Measured
   // (profiles/poly.sh): 0 is fastest — this softmax is issue/latency-bound, not MUFU-bound
@@ -544,12 +557,13 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tm
     return e ? atoi(e) : 0;
   }();
   if (p.d == 128) {
-    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, max_ctas, s);
-    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, max_ctas, s);
-    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, max_ctas, s);
+    if (pp <= 0 && tmv3) return launch_tile_tc2_t<128, 0, true>(p, tmk, tmv, items, max_ctas, s, tmv3);
+    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
+    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, max_ctas, s, tmv3);
+    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, max_ctas, s, tmv3);
   }
-  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, max_ctas, s);
-  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, max_ctas, s);
+  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
+  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, max_ctas, s, tmv3);
 }
 
 }  // namespace kva

@@ -138,6 +138,25 @@ EncodeTiledFn encode_fn() {
 
 // 2-D view of a pool tensor: dim0 = head_dim (contiguous), dim1 = num_blocks*Hkv*16 rows;
 // box = 64 channels x 16 rows (one block-head half), 128-byte swizzle.
+// 3-D view {64 channels, rows, 2 halves} of a d = 128 pool: ONE box {64, 16, 2} moves a whole
+// block-head (4 KB) into shared memory as [half][16 rows][64] with the 128-B swizzle of each
+// half — exactly the layout of two 2-D boxes, in half the TMA operations (the K/V streams of the
+// decode and tile kernels are bounded by the TMA operation rate, profiles/r01b).
+kva_status make_pool_map_3d(CUtensorMap *m, void *base, int64_t rows, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (d != 128) return fail(KVA_ERR_UNSUPPORTED, "3-D pool map needs head_dim 128");
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, 128};
+  cuuint32_t box[3] = {64, 16, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+  return KVA_OK;
+}
+
 kva_status make_pool_map(CUtensorMap *m, void *base, int64_t rows, int d) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
@@ -160,6 +179,8 @@ struct kva_pool {
   std::vector<uint32_t> free_host;  // mirror of free_bits (library is the single writer)
   int64_t n_free = 0;
   CUtensorMap tmk, tmv;
+  CUtensorMap tmk3, tmv3;  // 3-D maps (d = 128): one TMA box per block-head
+  bool has3d = false;
   Staging staging;
   // side stream for the tensor-core tile kernel (runs concurrently with the HBM-bound
   // decode kernel on the caller's stream; fork/join by events)
@@ -222,6 +243,14 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
   const int64_t rows = (int64_t)d->num_blocks * d->num_kv_heads * kBlock;
   kva_status st = make_pool_map(&p->tmk, d->k_pool, rows, d->head_dim);
   if (st == KVA_OK) st = make_pool_map(&p->tmv, d->v_pool, rows, d->head_dim);
+  if (st == KVA_OK && d->head_dim == 128) {
+    const char *e3 = getenv("KVA_TMA3D");  // KVA_TMA3D=0: 2-D boxes only (cross-check)
+    if (!(e3 && std::string(e3) == "0")) {
+      st = make_pool_map_3d(&p->tmk3, d->k_pool, rows, d->head_dim);
+      if (st == KVA_OK) st = make_pool_map_3d(&p->tmv3, d->v_pool, rows, d->head_dim);
+      p->has3d = st == KVA_OK;
+    }
+  }
   if (st != KVA_OK) {
     delete p;
     return st;
@@ -546,6 +575,8 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
 struct kva_plan {
   AttnParams p;
   CUtensorMap tmk, tmv;
+  CUtensorMap tmk3, tmv3;
+  bool has3d = false;
   ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
   ReqList<MergeReq> mrg;                   // merged requests (idem)
   const TileItem *d_tile = nullptr;
@@ -817,6 +848,9 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->device = p->desc.device;
   pl->tmk = p->tmk;
   pl->tmv = p->tmv;
+  pl->tmk3 = p->tmk3;
+  pl->tmv3 = p->tmv3;
+  pl->has3d = p->has3d;
   pl->stats = pb.stats;
   uint8_t *dws = static_cast<uint8_t *>(ws);
   // request lists: kernel parameters when they fit, else uploaded with the tile items
@@ -1003,7 +1037,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                      fork ? pl->tile_ctas : 0, ts));
     else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles,
-                                                          fork ? pl->tile_ctas : 0, ts));
+                                                          fork ? pl->tile_ctas : 0, ts,
+                                                          pl->has3d ? &pl->tmv3 : nullptr));
     else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                   fork ? pl->tile_ctas : 0, ts));
     else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
@@ -1016,7 +1051,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     // become ready before the tile kernel (launched first, high priority) and fill every SM
     if (fork && wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
-    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s));
+    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, false, pl->has3d ? &pl->tmk3 : nullptr,
+                           pl->has3d ? &pl->tmv3 : nullptr));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     return KVA_OK;
   };
@@ -1033,8 +1069,9 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
-    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s));
-    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, /*pdl=*/true));
+    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s, pl->has3d ? &pl->tmv3 : nullptr));
+    CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, /*pdl=*/true,
+                           pl->has3d ? &pl->tmk3 : nullptr, pl->has3d ? &pl->tmv3 : nullptr));
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
