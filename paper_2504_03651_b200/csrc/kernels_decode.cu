@@ -353,19 +353,28 @@ __global__ void __launch_bounds__(128, MINB)
   const int my_id = lane < nblk ? __ldg(trow + lane) : 0;
   const int row_base = kv_head * kBlock;
 
+  const uint64_t l2pol = policy_evict_first();
   auto issue = [&](int st, int id) {  // lane 0 only
     uint64_t *b = &bar[st];
     mbar_arrive_expect_tx(b, STAGE);
     const int row = id * p.Hkv * kBlock + row_base;
     uint8_t *dst = ws + st * STAGE;
+    // The split-KV stream reads every byte once: it is marked evict-first in L2, so it does not
+    // push out what the co-running kernels reuse (the tile kernel's K/V tiles, the eviction
+    // selection's keys) — llama7b step 448 -> 433 us (profiles/r01b).  Debug flag 16: normal.
     if constexpr (T3) {  // 3-D maps: one box = the block-head's two halves, same smem layout
-      tma_load_3d(dst, &tmk, b, 0, row, 0);
-      tma_load_3d(dst + KBYTES, &tmv, b, 0, row, 0);
+      if (!(p.debug_flags & 16)) {
+        tma_load_3d_hint(dst, &tmk, b, 0, row, 0, l2pol);
+        tma_load_3d_hint(dst + KBYTES, &tmv, b, 0, row, 0, l2pol);
+      } else {
+        tma_load_3d(dst, &tmk, b, 0, row, 0);
+        tma_load_3d(dst + KBYTES, &tmv, b, 0, row, 0);
+      }
     } else {
 #pragma unroll
-      for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
+      for (int h = 0; h < HALVES; ++h) tma_load_2d_hint(dst + h * 2048, &tmk, b, h * 64, row, l2pol);
 #pragma unroll
-      for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
+      for (int h = 0; h < HALVES; ++h) tma_load_2d_hint(dst + KBYTES + h * 2048, &tmv, b, h * 64, row, l2pol);
     }
   };
 #pragma unroll
