@@ -13,6 +13,12 @@ namespace kva {
 // sets the thread-local kva_last_error() message (kvattn_host.cu) and returns st
 kva_status set_error(kva_status st, const char *msg);
 
+// cudaFuncSetAttribute(max dynamic smem = smem, carveout = max shared) once per (kernel,
+// device, smem) — the attribute calls cost microseconds per launch otherwise (kvattn_host.cu)
+cudaError_t smem_attrs_once(const void *kern, int smem);
+// multiprocessor count of the current device (cached)
+int sm_count();
+
 constexpr int kBlock = 16;        // tokens per KV block (reading #5)
 constexpr int kSplitKeys = 512;   // fixed split-KV length (depends only on ctx, H9)
 constexpr int kDecodeRows = 16;   // rows (q tokens x g heads) one decode warp handles

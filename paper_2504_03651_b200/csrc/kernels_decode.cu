@@ -610,9 +610,8 @@ static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const 
                                    const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;
   auto kern = decode_kt_kernel<D, NR, NST, MINB, T3>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(kern), (int)smem);
   if (e != cudaSuccess) return e;
   const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
   const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
@@ -640,10 +639,8 @@ static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const v
                                    const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
   const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;  // + alignment slack
   auto kern = decode_kernel<D, NST, PF>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(kern), (int)smem);
   if (e != cudaSuccess) return e;
   const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
   const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);

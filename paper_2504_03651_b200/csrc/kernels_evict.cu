@@ -891,11 +891,13 @@ cudaError_t launch_free_ids(uint32_t *free_bits, const int32_t *ids, const int64
 
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t s) {
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int nsm = sm_count();
+  static int max_smem = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
   // half the SMs: the selection is latency-bound, and runs concurrently with the attention
   // kernels (whose CTAs take the other SMs / share these)
   int C = std::max(1, std::min(nsm / 2, kMaxCtas));
@@ -910,10 +912,8 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   int cache = 0;
   if (const char *e = getenv("KVA_EVICT_CACHE")) cache = atoi(e) != 0;
   if (!cache || dyn + static_smem > (size_t)max_smem) { dyn = 0; cache = 0; }
-  cudaError_t e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (e != cudaSuccess) return e;
-  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
-  e = cudaFuncSetAttribute(evict_select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(evict_select_kernel), (int)dyn);
   if (e != cudaSuccess) return e;
   uint8_t *p = reinterpret_cast<uint8_t *>(ws);
   SelWs *sw = reinterpret_cast<SelWs *>(p);

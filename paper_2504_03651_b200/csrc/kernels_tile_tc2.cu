@@ -531,14 +531,10 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
   const int n = L.n;
   const size_t smem = 2 * (size_t)tc2::M * D * 2 + 4 * (size_t)tc2::N * D * 2 + 1024;
   auto kern = tile_tc2_kernel<D, PP, V3>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(kern), (int)smem);
   if (e != cudaSuccess) return e;
-  // full shared-memory carveout so CTAs of concurrently running kernels can share an SM
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = sm_count();
   const int grid = std::max(1, std::min(n, max_ctas > 0 ? max_ctas : nsm));
   kern<<<grid, tc2::THREADS, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
                                         *reinterpret_cast<const CUtensorMap *>(tmv), L,

@@ -47,6 +47,35 @@ kva_status set_error(kva_status st, const char *msg) {
   g_err = msg;
   return st;
 }
+cudaError_t smem_attrs_once(const void *kern, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void *, int>, int>> done;  // ((kernel, device), smem)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &d : done)
+      if (d.first.first == kern && d.first.second == dev && d.second >= smem) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    done.push_back({{kern, dev}, smem});
+  }
+  return e;
+}
+int sm_count() {
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
 }  // namespace kva
 extern "C" const char *kva_version(void) {
   return "kvattn 0.1 (sm_100a; decode split-KV TMA+mma.sync, tile attention, radix top-k)";
