@@ -119,7 +119,7 @@ struct TileList {
 };
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileList &items, int max_ctas, cudaStream_t s,
-                            const void *tmap_v3 = nullptr);
+                            const void *tmap_v3 = nullptr, const void *tmap_k3 = nullptr);
 cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "internal.h"
@@ -137,11 +138,11 @@ __device__ __forceinline__ ItemGeom geom(const TileItem &it, int g) {
 // PP = column pairs (of every 16) whose exp2 runs as a polynomial on the FMA pipe;
 // V3 = V tiles loaded with one 3-D box per block-head (d = 128): V tile layout
 // [block][half][16 keys][64] (PV reads it with LBO = 2 KB), else [half][128 keys][64]
-template <int D, int PP, bool V3>
+template <int D, int PP, bool V3, bool K3>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     tile_tc2_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
                     const __grid_constant__ CUtensorMap tmv, const __grid_constant__ TileList L,
-                    const __grid_constant__ CUtensorMap tmv3) {
+                    const __grid_constant__ CUtensorMap tmv3, const __grid_constant__ CUtensorMap tmk3) {
   const TileItem *items = L.ptr ? L.ptr : L.item;
   const int n_items = L.n;
   using namespace tc2;
@@ -222,12 +223,18 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (KT >= 2) mbar_wait(&bar_ke[s], ((KT >> 1) - 1) & 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&bar_kf[s], nb * KBYTES);
+          if constexpr (K3) {  // K tile [8-key group][half][8 keys][64]: one 4-D box per block
 #pragma unroll
-          for (int q = 0; q < NBLK; ++q)
-            if (q < nb)
+            for (int q = 0; q < NBLK; ++q)
+              if (q < nb) tma_load_4d(sK + s * TBYTES + q * 4096, &tmk3, &bar_kf[s], 0, 0, 0, rows[q] >> 3);
+          } else {
 #pragma unroll
-              for (int h = 0; h < HALVES; ++h)
-                tma_load_2d(sK + s * TBYTES + h * (N * 128) + q * 2048, &tmk, &bar_kf[s], h * 64, rows[q]);
+            for (int q = 0; q < NBLK; ++q)
+              if (q < nb)
+#pragma unroll
+                for (int h = 0; h < HALVES; ++h)
+                  tma_load_2d(sK + s * TBYTES + h * (N * 128) + q * 2048, &tmk, &bar_kf[s], h * 64, rows[q]);
+          }
         }
         if (KT >= 2) mbar_wait(&bar_ve[s], ((KT >> 1) - 1) & 1);
         if (lane == 0) {
@@ -267,11 +274,20 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         const int KT = KT0 + j, s = KT & 1;
         if (lane == 0) {
           if (!(p.debug_flags & 4)) {  // diagnostics: 4 = QK MMAs not issued (pipeline study)
+            if constexpr (K3) {  // 8-key groups of a half are 2 KB apart: SBO = 2048, N = 128
 #pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint64_t a = sdesc(q_base + t * QBYTES + (k >> 2) * (M * 128) + (k & 3) * 32, 16, 1024);
-              const uint64_t b = sdesc(k_base + s * TBYTES + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
-              umma_ss(tmem + COL_S[t], a, b, ID_QK, k > 0 ? 1u : 0u);
+              for (int k = 0; k < D / 16; ++k) {
+                const uint64_t a = sdesc(q_base + t * QBYTES + (k >> 2) * (M * 128) + (k & 3) * 32, 16, 1024);
+                const uint64_t b = sdesc(k_base + s * TBYTES + (k >> 2) * 1024 + (k & 3) * 32, 16, 2048);
+                umma_ss(tmem + COL_S[t], a, b, ID_QK, k > 0 ? 1u : 0u);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < D / 16; ++k) {
+                const uint64_t a = sdesc(q_base + t * QBYTES + (k >> 2) * (M * 128) + (k & 3) * 32, 16, 1024);
+                const uint64_t b = sdesc(k_base + s * TBYTES + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
+                umma_ss(tmem + COL_S[t], a, b, ID_QK, k > 0 ? 1u : 0u);
+              }
             }
           }
           umma_commit(&bar_s[t]);
@@ -525,12 +541,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
-template <int D, int PP, bool V3 = false>
+template <int D, int PP, bool V3 = false, bool K3 = false>
 static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const void *tmv,
-                                     const TileList &L, int max_ctas, cudaStream_t s, const void *tmv3) {
+                                     const TileList &L, int max_ctas, cudaStream_t s, const void *tmv3,
+                                     const void *tmk3 = nullptr) {
   const int n = L.n;
   const size_t smem = 2 * (size_t)tc2::M * D * 2 + 4 * (size_t)tc2::N * D * 2 + 1024;
-  auto kern = tile_tc2_kernel<D, PP, V3>;
+  auto kern = tile_tc2_kernel<D, PP, V3, K3>;
   // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
   cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(kern), (int)smem);
   if (e != cudaSuccess) return e;
@@ -538,12 +555,14 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
   const int grid = std::max(1, std::min(n, max_ctas > 0 ? max_ctas : nsm));
   kern<<<grid, tc2::THREADS, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
                                         *reinterpret_cast<const CUtensorMap *>(tmv), L,
-                                        *reinterpret_cast<const CUtensorMap *>(V3 ? tmv3 : tmv));
+                                        *reinterpret_cast<const CUtensorMap *>(V3 ? tmv3 : tmv),
+                                        *reinterpret_cast<const CUtensorMap *>(K3 ? tmk3 : tmk));
   return cudaGetLastError();
 }
 
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tmv,
-                            const TileList &items, int max_ctas, cudaStream_t s, const void *tmv3) {
+                            const TileList &items, int max_ctas, cudaStream_t s, const void *tmv3,
+                            const void *tmk3) {
   if (items.n <= 0) return cudaSuccess;
   // KVA_POLY: column pairs (of 16) with exp2 on the FMA pipe: 0 (default), 4 or 6.  Measured
   // (profiles/poly.sh): 0 is fastest — this softmax is issue/latency-bound, not MUFU-bound
@@ -553,6 +572,14 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tm
     return e ? atoi(e) : 0;
   }();
   if (p.d == 128) {
+    // K tiles by one 4-D box per block (N = 128 QK over a 2 KB group stride; default):
+    // llama70b 7.35 -> 7.21 ms, qwen14b-p 2.36 -> 2.25 ms.  KVA_TILE_K3=0: 2-D boxes.
+    static const bool k3 = [] {
+      const char *e = getenv("KVA_TILE_K3");
+      return !(e && std::string(e) == "0");
+    }();
+    if (pp <= 0 && tmv3 && tmk3 && k3)
+      return launch_tile_tc2_t<128, 0, true, true>(p, tmk, tmv, items, max_ctas, s, tmv3, tmk3);
     if (pp <= 0 && tmv3) return launch_tile_tc2_t<128, 0, true>(p, tmk, tmv, items, max_ctas, s, tmv3);
     if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
     if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, max_ctas, s, tmv3);

@@ -186,6 +186,25 @@ kva_status make_pool_map_3d(CUtensorMap *m, void *base, int64_t rows, int d) {
   return KVA_OK;
 }
 
+// 4-D view {64 channels, 8 rows, 2 halves, row groups} of a d = 128 pool: one box {64, 8, 2, 2}
+// is a whole block-head laid out [8-row group][half][8 rows][64] — for a K tile of 8 blocks
+// every 8-key group of one half is 2 KB apart, a uniform UMMA stride (SBO = 2048), so the QK
+// MMA keeps N = 128 while the K stream needs one TMA operation per block.
+kva_status make_pool_map_4d(CUtensorMap *m, void *base, int64_t rows, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if (d != 128 || rows % 8) return fail(KVA_ERR_UNSUPPORTED, "4-D pool map needs head_dim 128");
+  cuuint64_t dims[4] = {64, 8, 2, (cuuint64_t)(rows / 8)};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, 128, (cuuint64_t)d * 2 * 8};
+  cuuint32_t box[4] = {64, 8, 2, 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled (4-D) failed (%d)", (int)r);
+  return KVA_OK;
+}
+
 kva_status make_pool_map(CUtensorMap *m, void *base, int64_t rows, int d) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(KVA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
@@ -209,6 +228,7 @@ struct kva_pool {
   int64_t n_free = 0;
   CUtensorMap tmk, tmv;
   CUtensorMap tmk3, tmv3;  // 3-D maps (d = 128): one TMA box per block-head
+  CUtensorMap tmk4;        // 4-D K map for the tile kernel (N = 128 QK with one box per block)
   bool has3d = false;
   Staging staging;
   // side stream for the tensor-core tile kernel (runs concurrently with the HBM-bound
@@ -276,6 +296,7 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
     const char *e3 = getenv("KVA_TMA3D");  // KVA_TMA3D=0: 2-D boxes only (cross-check)
     if (!(e3 && std::string(e3) == "0")) {
       st = make_pool_map_3d(&p->tmk3, d->k_pool, rows, d->head_dim);
+      if (st == KVA_OK) st = make_pool_map_4d(&p->tmk4, d->k_pool, rows, d->head_dim);
       if (st == KVA_OK) st = make_pool_map_3d(&p->tmv3, d->v_pool, rows, d->head_dim);
       p->has3d = st == KVA_OK;
     }
@@ -604,7 +625,7 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
 struct kva_plan {
   AttnParams p;
   CUtensorMap tmk, tmv;
-  CUtensorMap tmk3, tmv3;
+  CUtensorMap tmk3, tmv3, tmk4;
   bool has3d = false;
   ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
   ReqList<MergeReq> mrg;                   // merged requests (idem)
@@ -878,6 +899,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->tmk = p->tmk;
   pl->tmv = p->tmv;
   pl->tmk3 = p->tmk3;
+  pl->tmk4 = p->tmk4;
   pl->tmv3 = p->tmv3;
   pl->has3d = p->has3d;
   pl->stats = pb.stats;
@@ -1067,7 +1089,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
                                                      fork ? pl->tile_ctas : 0, ts));
     else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles,
                                                           fork ? pl->tile_ctas : 0, ts,
-                                                          pl->has3d ? &pl->tmv3 : nullptr));
+                                                          pl->has3d ? &pl->tmv3 : nullptr,
+                                                          pl->has3d ? &pl->tmk4 : nullptr));
     else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
                                                   fork ? pl->tile_ctas : 0, ts));
     else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
@@ -1098,7 +1121,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
-    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s, pl->has3d ? &pl->tmv3 : nullptr));
+    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s, pl->has3d ? &pl->tmv3 : nullptr,
+                             pl->has3d ? &pl->tmk4 : nullptr));
     CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, /*pdl=*/true,
                            pl->has3d ? &pl->tmk3 : nullptr, pl->has3d ? &pl->tmv3 : nullptr));
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));

@@ -56,7 +56,8 @@ def test_overlap_modes_bitexact(tmp_path):
 
 
 @pytest.mark.parametrize("env", [{"KVA_DECODE_IMPL": "v1"}, {"KVA_DECODE_CFG": "1"},
-                                 {"KVA_POLY": "0"}, {"KVA_POLY": "4"}, {"KVA_PDL": "0"}, {"KVA_TMA3D": "0"}])
+                                 {"KVA_POLY": "0"}, {"KVA_POLY": "4"}, {"KVA_PDL": "0"}, {"KVA_TMA3D": "0"},
+                                 {"KVA_TILE_K3": "0"}])
 def test_decode_impl_parity(env, tmp_path):
     _run(env, "dec_" + "_".join(env.values()), tmp_path)
 
