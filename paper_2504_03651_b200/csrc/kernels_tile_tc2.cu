@@ -450,8 +450,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           for (int c = 2 * hb; c < 2 * hb + 2; ++c)
             ld32(t_row + COL_S[t] + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&u[c * 32]));
           wait_ld();
-#pragma unroll
-          for (int c = 2 * hb; c < 2 * hb + 2; ++c) {
+          // two explicit copies of the loop: a warp-uniform branch instead of a per-element
+          // compare + select that the compiler otherwise if-converts into every element
+          auto exp_chunk = [&](int c, bool masked) {
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
                 e.x = fast_exp2(x.x);
                 e.y = fast_exp2(x.y);
               }
-              if (!full) {
+              if (masked) {
                 e.x = i0 < lim ? e.x : 0.f;
                 e.y = i1 < lim ? e.y : 0.f;
               }
@@ -472,6 +473,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
               pk[i] = pack_bf16(e.x, e.y);
             }
             st16(t_row + COL_S[t] + c * 16, pk);
+          };
+          if (full) {
+#pragma unroll
+            for (int c = 2 * hb; c < 2 * hb + 2; ++c) exp_chunk(c, false);
+          } else {
+#pragma unroll
+            for (int c = 2 * hb; c < 2 * hb + 2; ++c) exp_chunk(c, true);
           }
         }
         const float ps = (s2[0].x + s2[0].y) + (s2[1].x + s2[1].y);
