@@ -366,10 +366,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const TileItem it = items[item];
       const ItemGeom G = geom(it, g);
-      if (G.rows_t[t] == 0) continue;
+      // this warp group's tile: selects, not a runtime-indexed (local-memory) array access
+      const int rows_t = t ? G.rows_t[1] : G.rows_t[0];
+      const int nt_t = t ? G.nt_t[1] : G.nt_t[0];
+      if (rows_t == 0) continue;
       const bool is_list = it.flags & kTileList, causal = it.flags & kTileCausal;
       const int r = it.r0 + t * M + row;
-      const bool valid = row < G.rows_t[t];
+      const bool valid = row < rows_t;
       int qrow = 0;
       if (valid) {
         const int tok = r / g;
@@ -386,10 +389,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       mbar_arrive(&bar_q[t]);
 
       const int pos = (causal && valid) ? it.pos0 + r / g : INT32_MAX;
-      const int k1 = G.k1_t[t];
+      const int k1 = t ? G.k1_t[1] : G.k1_t[0];
       const float sl2 = p.scale_log2;
       float m_used = -CUDART_INF_F, l = 0.f;
-      for (int j = 0; j < G.nt_t[t]; ++j, ++Gs) {
+      for (int j = 0; j < nt_t; ++j, ++Gs) {
         if (warp == 4 || warp == 8) ts(1 + t);
         mbar_wait(&bar_s[t], Gs & 1);  // QK_t(j) done; so is PV_t(j-1) (issued earlier)
         if (j >= 1) mbar_wait(&bar_o[t], (Gs - 1) & 1);  // observe that completion (no-op wait)
