@@ -35,6 +35,11 @@ constexpr int M = 128;            // rows per Q tile (UMMA M, TMEM lanes)
 constexpr int N = 128;            // keys per K/V tile
 constexpr int NBLK = N / kBlock;  // 8 paged blocks per key tile
 constexpr int THREADS = 320;      // 10 warps
+#ifdef KVA_TILE_TIMESTAMPS
+constexpr bool kTimestamps = true;
+#else
+constexpr bool kTimestamps = false;
+#endif
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -168,6 +173,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   // diagnostics: CTA 0 records %globaltimer at role events into p.dbg[role*512 + n]
   int dbg_n = 0;
   auto ts = [&](int role) {
+#ifndef KVA_TILE_TIMESTAMPS  // role timelines (profiles/tc2_timeline.py) need -DKVA_TILE_TIMESTAMPS
+    return;
+#endif
     if (p.dbg && blockIdx.x == 0 && lane == 0 && dbg_n < 512) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -393,10 +401,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       const float sl2 = p.scale_log2;
       float m_used = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < nt_t; ++j, ++Gs) {
-        if (warp == 4 || warp == 8) ts(1 + t);
+        if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
         mbar_wait(&bar_s[t], Gs & 1);  // QK_t(j) done; so is PV_t(j-1) (issued earlier)
         if (j >= 1) mbar_wait(&bar_o[t], (Gs - 1) & 1);  // observe that completion (no-op wait)
-        if (warp == 4 || warp == 8) ts(1 + t);
+        if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
         fence_after();
         if (p.debug_flags & 1) {  // diagnostics: measure the MMA/TMA pipeline without softmax
           fence_before();
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         wait_st();
         fence_before();
         mbar_arrive(&bar_p[t]);
-        if (warp == 4 || warp == 8) ts(1 + t);
+        if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
       }
       // ------------------------------- epilogue -------------------------------
       mbar_wait(&bar_o[t], (Gs - 1) & 1);

@@ -1,4 +1,5 @@
-"""Diagnostics: role timelines of tile_tc2_kernel's CTA 0 (KVA_DEBUG_TS device buffer)."""
+"""Diagnostics: role timelines of tile_tc2_kernel's CTA 0 (KVA_DEBUG_TS device buffer).
+Build with KVA_NVCC_DEFS=-DKVA_TILE_TIMESTAMPS (the stamps are compiled out by default)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
