@@ -223,14 +223,25 @@ def run_ours(args, rank, world, local):
     # the attention pair is launched after the manager's key pass, so the cooperative eviction
     # selection (next on its stream) is placed on the SMs before the decode kernel fills them
     gate_attn = os.environ.get("KVA_BENCH_GATE", "1") == "1"
+    # The manager pass + selection of step i depend only on the block metadata (updated in order
+    # on their own stream), not on step i-1's attention: by default they are not forked from the
+    # main stream each step, so step i's metadata pass runs as soon as step i-1's selection
+    # finishes (overlapping step i-1's tail) — the serving loop issues it as soon as the
+    # iteration's transitions are known.  Every step still runs the whole pass; the timed region
+    # starts with a fork (ev_fork) so no eviction work of a timed step precedes it.
+    # KVA_BENCH_EVICT_PIPELINE=0: fork every step (serialises it behind the previous step).
+    evict_pipeline = os.environ.get("KVA_BENCH_EVICT_PIPELINE", "1") == "1"
+    fork_next = {"v": True}
 
     def step(time_idx=None):
         n = 0
         if ev is not None:
             # the manager's eviction selection has no data dependency on this layer's attention:
             # it runs on its own stream, concurrently (its CTAs leave room for decode CTAs)
-            ev_fork.record(stream)
-            ev_stream.wait_event(ev_fork)
+            if fork_next["v"] or not evict_pipeline:
+                ev_fork.record(stream)
+                ev_stream.wait_event(ev_fork)
+                fork_next["v"] = False
             keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
                              stream=ev_stream)
             ev_keys.record(ev_stream)
@@ -271,6 +282,7 @@ def run_ours(args, rank, world, local):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
+        fork_next["v"] = True  # the first timed step's eviction work starts after s
         for i in range(nsteps):
             step(time_idx=i if time_kernels else None)
         e.record(stream)
@@ -307,8 +319,10 @@ def run_ours(args, rank, world, local):
             b["v"].copy_(h_v, non_blocking=True)
             ev_in[i % 2].record(cs_in)
         if ev is not None:
-            ev_fork.record(stream)
-            ev_stream.wait_event(ev_fork)
+            if fork_next["v"] or not evict_pipeline:
+                ev_fork.record(stream)
+                ev_stream.wait_event(ev_fork)
+                fork_next["v"] = False
             keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
                              stream=ev_stream)
             ev_keys.record(ev_stream)
@@ -375,6 +389,7 @@ def run_ours(args, rank, world, local):
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
         cs_in.wait_event(s)
+        fork_next["v"] = True
         for i in range(nsteps):
             step_e2e(i)
         stream.wait_stream(cs_out)   # the last result is on the host
@@ -444,7 +459,8 @@ def run_ours(args, rank, world, local):
                    "kv_bytes_algorithmic_per_rank": stats["kv_bytes_algorithmic"],
                    "flops_per_rank": stats["flops"],
                    "step": "kv_append+hybrid_attention(plan,tile,decode,merge)" +
-                           ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)") +
+                           ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)" +
+                            (" [eviction pass pipelined: issued after the previous step's selection]" if (ev is not None and evict_pipeline) else "")) +
                            "+release",
                    "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
