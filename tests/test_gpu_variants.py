@@ -83,3 +83,37 @@ print("OK")
         r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_pdl_merge_waits_for_the_tile_kernel(tmp_path):
+    """Under PDL the decode kernel may start (and finish) while the tile kernel still runs; the
+    merge after it reads cascade partials the TILE kernel writes.  Force the tile kernel to be
+    the long pole (1 persistent CTA, a long prefill chunk in the batch) with the workspace
+    NaN-filled: a merge that did not wait for it would produce NaN / wrong rows."""
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import workloads as W, paper_2504_03651_b200 as K
+from gpu_util import oracle_step, assert_attention_close
+reqs = [W.ReqSpec(W.OFFLINE_DECODE, 40 * 16 + 3 + i, 1, 0) for i in range(12)]
+reqs += [W.ReqSpec(W.OFFLINE_PREFILL, 40 * 16 + 1500, 1500, 0), W.ReqSpec(W.ONLINE_DECODE, 900, 1)]
+wl = W.make_workload(W.custom_config("pdl", 16, 2, 128, 61, reqs, [40]))
+dev = "cuda"
+pool = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), K.free_bits_tensor(wl.free_bits, dev))
+batch = K.Batch(wl.batch, dev)
+K.kv_append(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+ws = torch.full((K.hybrid_attention_workspace_size(batch) // 4 + 64,), float("nan"), device=dev).view(torch.uint8)
+plan = K.Plan(pool, batch, ws)
+assert plan.stats()["n_cascade_items"] > 0
+q = wl.q.to(dev)
+out = torch.empty(q.shape, dtype=torch.float32, device=dev)
+lse = torch.empty(q.shape[:2], dtype=torch.float32, device=dev)
+plan.run(q, out, lse)
+torch.cuda.synchronize()
+r = oracle_step(wl)
+assert_attention_close(out, lse, r["out"], r["lse"])
+print("OK")
+""" % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ, KVA_TILE_CTAS="1", KVA_OVERLAP="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
