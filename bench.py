@@ -211,12 +211,14 @@ def run_ours(args, rank, world, local):
 
     launches = {"n": 0}
 
-    tim = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    for e4 in tim:
-        for e in e4:
-            e.record(stream)   # materialise the cudaEvent_t handles
-    torch.cuda.synchronize()
-    tim_used = []
+    # per-kernel durations inside the timed steps from in-kernel %globaltimer spans (first CTA
+    # start -> last CTA end of the decode and tile kernels; kva_plan_set_span_buffer) — no stream
+    # operation between the kernels, so the programmatic-dependent-launch chain stays intact
+    # (CUDA events between them cost ~20 us per step)
+    spans = torch.zeros((args.steps, 4), dtype=torch.int64, device=dev)
+    spans[:, 0] = -1
+    spans[:, 2] = -1
+    span_used = []
 
     ev_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("KVA_BENCH_EVICT_PRIO", "0")))
     ev_fork, ev_join, ev_keys = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
@@ -251,14 +253,14 @@ def run_ours(args, rank, world, local):
             n += 3
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
         batch.table_host[...] = pristine_host
+        if ev is not None and gate_attn:  # before the append: the attention pair follows it directly
+            stream.wait_event(ev_keys)
         K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
         n += 2 + plan.launch_count()
-        if ev is not None and gate_attn:
-            stream.wait_event(ev_keys)
         if time_idx is not None:
-            plan.set_timing_events(*tim[time_idx])
-            tim_used.append(tim[time_idx])
+            plan.set_span_buffer(spans[time_idx])
+            span_used.append(time_idx)
         plan.run(q, out, lse, stream=stream)
         if world > 1:
             kdist.gather_outputs(out, gbuf)
@@ -335,11 +337,11 @@ def run_ours(args, rank, world, local):
         stream.wait_event(ev_in[i % 2])
         if i >= 2:
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done
+        if ev is not None and gate_attn:
+            stream.wait_event(ev_keys)
         K.kv_append(pool, batch, b["k"], b["v"], ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
         n += 2 + plan.launch_count()
-        if ev is not None and gate_attn:
-            stream.wait_event(ev_keys)
         plan.run(b["q"], b["out"], lse, stream=stream)
         res_t = b["out"]
         if world > 1:
@@ -417,8 +419,11 @@ def run_ours(args, rank, world, local):
     ms = timed(args.steps, time_kernels=True)
     gpu_launches = launches["n"]
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
-    dec_ms = [e4[2].elapsed_time(e4[3]) for e4 in tim_used if stats["n_decode_items"] > 0]
-    tile_ms = [e4[0].elapsed_time(e4[1]) for e4 in tim_used if stats["n_tile_items"] > 0]
+    sp = spans.cpu().numpy().view(np.uint64)
+    dec_ms = [float(sp[i, 1] - sp[i, 0]) * 1e-6 for i in span_used
+              if stats["n_decode_items"] > 0 and sp[i, 1] > 0 and sp[i, 1] >= sp[i, 0]]
+    tile_ms = [float(sp[i, 3] - sp[i, 2]) * 1e-6 for i in span_used
+               if stats["n_tile_items"] > 0 and sp[i, 3] > 0 and sp[i, 3] >= sp[i, 2]]
     # standalone decode-kernel timing (same plan, no co-running kernels): context for the
     # in-step roofline above, which is measured while the tile kernel shares the GPU
     dec_alone = None
@@ -468,6 +473,7 @@ def run_ours(args, rank, world, local):
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
                    "overlap": "tile (tcgen05) on a side stream concurrent with decode; eviction selection on a third stream concurrent with the attention"},
         "roofline": {"bound": "hbm", "kernel": "decode_kt_kernel (split-KV)", "achieved": achieved,
+                     "timing": "in-kernel %globaltimer span per timed step (first CTA start -> last CTA end)",
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, "decode_kt_kernel"), "bytes_per_launch": dec_bytes,
                      "peak_source": peak_src},

@@ -193,6 +193,12 @@ kva_status hybrid_attention_run_phases(const kva_plan *plan, const void *q, int6
 /* Instrumentation: cudaEvent_t handles (or NULL) recorded immediately before/after the tile
  * kernel launch (on the stream it runs on) and the decode kernel launch (on the caller's
  * stream) by every later run of this plan — per-kernel timing inside an overlapped step. */
+/* Instrumentation without stream operations: if dev_span (device, 4 x u64) is set, every later
+ * run of this plan records %globaltimer nanoseconds: [0] = min start and [1] = max end over the
+ * decode kernel's CTAs, [2] / [3] = the same for the tile kernel (atomicMin / atomicMax: the
+ * caller initialises [0], [2] to UINT64_MAX and [1], [3] to 0).  Unlike timing events this does
+ * not break the programmatic-dependent-launch chain of the run.  NULL disables it. */
+kva_status kva_plan_set_span_buffer(kva_plan *plan, unsigned long long *dev_span);
 kva_status kva_plan_set_timing_events(kva_plan *plan, void *tile_begin, void *tile_end,
                                       void *decode_begin, void *decode_end);
 /* Number of kernel launches hybrid_attention_run_phases(plan, phases) enqueues. */

@@ -98,6 +98,9 @@ struct AttnParams {
   float *part_lse;        // [slots]
   const int32_t *row_list;
   unsigned long long *dbg;  // optional timestamps (diagnostics; KVA_DEBUG_TS), nullable
+  // optional kernel spans (%globaltimer ns): [0] = min decode CTA start, [1] = max decode CTA
+  // end, [2] / [3] = the same for the tile kernel (kva_plan_set_span_buffer), nullable
+  unsigned long long *span;
   int32_t debug_flags;      // diagnostics only (KVA_DEBUG_FLAGS): 1 = tile softmax skipped
 };
 

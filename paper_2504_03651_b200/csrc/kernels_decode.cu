@@ -318,6 +318,16 @@ __global__ void __launch_bounds__(128, MINB)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * 4 + warp;  // (item, kv head), head fastest
+  __shared__ unsigned int s_done;
+  if (p.span) {  // instrumentation: CTA start (%globaltimer ns); the only CTA barrier
+    if (threadIdx.x == 0) {
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      atomicMin(&p.span[0], t0);
+      s_done = 0u;
+    }
+    __syncthreads();
+  }
   if (unit >= n_units) return;             // no CTA-wide barrier below
   const int item = unit / p.Hkv, kv_head = unit - item * p.Hkv;
   const DecodeReq *reqs = L.ptr ? L.ptr : L.req;
@@ -601,6 +611,15 @@ __global__ void __launch_bounds__(128, MINB)
       float *dst = p.part_o + (int64_t)(slot + r) * D + lane * V;
 #pragma unroll
       for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
+    }
+  }
+  if (p.span) {  // instrumentation: the CTA's last active warp records the end
+    __syncwarp();
+    const int active = min(4, n_units - (int)blockIdx.x * 4);
+    if (lane == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (atomicAdd(&s_done, 1u) == (unsigned)(active - 1)) atomicMax(&p.span[1], t1);
     }
   }
 }

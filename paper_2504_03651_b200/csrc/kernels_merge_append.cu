@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(256) append_kernel(
     uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
     const int32_t *__restrict__ block_table, int32_t max_blocks, const __grid_constant__ ReqList<AppendReq> L,
     int32_t total_new_tok) {
+  // the tile kernel launched right after this append (programmatic dependent launch) may
+  // become resident now; it waits (griddepcontrol.wait) before reading the pool
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const AppendReq *reqs = L.ptr ? L.ptr : L.req;
   const int32_t *tok_pre = L.ptr ? L.pre_ptr : L.pre;
   const int num_reqs = L.n;

@@ -212,9 +212,17 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   // on the remaining SMs — the tile kernel claims its SMs first (it reads nothing the
   // dependent writes, and the dependent reads nothing this kernel writes)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.span && threadIdx.x == 0) {  // instrumentation: CTA start
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    atomicMin(&p.span[2], t0);
+  }
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
+    // launched as a dependent of the kv_append kernel: the rows it writes must be complete
+    // (and visible) before the pool is read (a no-op for a normal launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     int KT = 0;  // K/V tiles loaded so far (ring position)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const TileItem it = items[item];
@@ -554,6 +562,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
   fence_before();
   __syncthreads();
+  if (p.span && threadIdx.x == 0) {  // instrumentation: CTA end (every role done)
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicMax(&p.span[3], t1);
+  }
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -572,11 +585,22 @@ static cudaError_t launch_tile_tc2_t(const AttnParams &p, const void *tmk, const
   if (e != cudaSuccess) return e;
   const int nsm = sm_count();
   const int grid = std::max(1, std::min(n, max_ctas > 0 ? max_ctas : nsm));
-  kern<<<grid, tc2::THREADS, smem, s>>>(p, *reinterpret_cast<const CUtensorMap *>(tmk),
-                                        *reinterpret_cast<const CUtensorMap *>(tmv), L,
-                                        *reinterpret_cast<const CUtensorMap *>(V3 ? tmv3 : tmv),
-                                        *reinterpret_cast<const CUtensorMap *>(K3 ? tmk3 : tmk));
-  return cudaGetLastError();
+  // programmatic dependent launch: may become resident while the preceding kernel on the
+  // stream (the kv_append of the tile-path rows) still runs; the producer waits for it
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tc2::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, *reinterpret_cast<const CUtensorMap *>(tmk),
+                            *reinterpret_cast<const CUtensorMap *>(tmv), L,
+                            *reinterpret_cast<const CUtensorMap *>(V3 ? tmv3 : tmv),
+                            *reinterpret_cast<const CUtensorMap *>(K3 ? tmk3 : tmk));
 }
 
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tmv,

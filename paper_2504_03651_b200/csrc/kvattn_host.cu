@@ -594,15 +594,35 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     CUDA_TRY(p->staging.upload(slot, workspace, off, s));
   }
   CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, al, s));
-  if (!rb.empty()) {  // fork after the table update, before the decode-class append
+  // Default: both appends on `stream` (decode-class rows first); the tile kernel, launched next
+  // with programmatic dependent launch, becomes resident while the tile-path rows are still
+  // being written and waits for them in-kernel, and the decode kernel (dependent of the tile
+  // kernel) starts meanwhile.  KVA_APPEND_SIDE=1: tile-path rows on a side stream instead.
+  static const bool side = [] {
+    const char *e = getenv("KVA_APPEND_SIDE");
+    return e && std::string(e) == "1";
+  }();
+  if (!side) {
+    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
+                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
+                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
+                           b->max_blocks, la, pa.back(), s));
+    if (!rb.empty())
+      CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
+                             stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
+                             static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
+                             b->max_blocks, lb, pbv.back(), s));
+  }
+  if (side && !rb.empty()) {  // fork after the table update, before the decode-class append
     CUDA_TRY(cudaEventRecord(p->ev_afork, s));
     CUDA_TRY(cudaStreamWaitEvent(p->aux_lo, p->ev_afork, 0));
   }
-  CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
-                         stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
-                         static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                         b->max_blocks, la, pa.back(), s));
-  if (!rb.empty()) {
+  if (side)
+    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
+                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
+                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
+                           b->max_blocks, la, pa.back(), s));
+  if (side && !rb.empty()) {
     CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
                            stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
                            static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
@@ -649,6 +669,7 @@ struct kva_plan {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t t_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events
+  unsigned long long *span = nullptr;                           // optional in-kernel spans
   kva_plan_stats stats{};
 };
 
@@ -1057,6 +1078,7 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.out_f32 = out_dtype == KVA_OUT_F32;
   p.lse = lse;
   p.dbg = nullptr;
+  p.span = pl->span;
   p.debug_flags = 0;
   if (const char *e = getenv("KVA_DEBUG_FLAGS")) p.debug_flags = atoi(e);
   if (const char *e = getenv("KVA_DEBUG_TS")) p.dbg = reinterpret_cast<unsigned long long *>(strtoull(e, nullptr, 0));
@@ -1158,6 +1180,12 @@ extern "C" kva_status hybrid_attention_run(const kva_plan *pl, const void *q, in
                                            int32_t out_dtype, float *lse, kva_stream_t stream) {
   return hybrid_attention_run_phases(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse,
                                      KVA_PHASE_ALL, stream);
+}
+
+extern "C" kva_status kva_plan_set_span_buffer(kva_plan *pl, unsigned long long *dev_span) {
+  if (!pl) return fail(KVA_ERR_INVALID, "null plan");
+  pl->span = dev_span;
+  return KVA_OK;
 }
 
 extern "C" kva_status kva_plan_set_timing_events(kva_plan *pl, void *tile_begin, void *tile_end,

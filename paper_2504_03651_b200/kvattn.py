@@ -71,6 +71,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "kv_pool_free_count", "kv_pool_resync", "kv_pool_sync", "kv_append_workspace_size", "kv_append",
            "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
+           "kva_plan_set_span_buffer",
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
@@ -114,6 +115,7 @@ def load(build_if_missing: bool = True):
         "hybrid_attention_run_phases": ([P, P, i64, i64, P, i64, i64, i32, P, i32, P], ctypes.c_int),
         "kva_plan_launch_count": ([P, i32, P], ctypes.c_int),
         "kva_plan_set_timing_events": ([P, P, P, P, P], ctypes.c_int),
+        "kva_plan_set_span_buffer": ([P, P], ctypes.c_int),
         "kv_release_blocks": ([P, P, i64, P], ctypes.c_int),
         "kva_plan_destroy": ([P], ctypes.c_int),
         "kva_plan_get_stats": ([P, P], ctypes.c_int),
@@ -326,6 +328,11 @@ class Plan:
         h = lambda e: None if e is None else ctypes.c_void_p(e.cuda_event)
         _check(load().kva_plan_set_timing_events(self.handle, h(tile_begin), h(tile_end),
                                                  h(decode_begin), h(decode_end)))
+
+    def set_span_buffer(self, span: torch.Tensor | None):
+        """kva_plan_set_span_buffer: int64 device tensor [4] (decode start/end, tile start/end ns;
+        initialise [0], [2] to -1 (= UINT64_MAX bits) and [1], [3] to 0)."""
+        _check(load().kva_plan_set_span_buffer(self.handle, _ptr(span) if span is not None else None))
 
     def launch_count(self, phases: int = PHASE_ALL) -> int:
         n = ctypes.c_int32()
