@@ -379,31 +379,52 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
     uint8_t *sQt = sQ + t * QBYTES;
     int Gs = 0;  // S/P/O uses of this tile group (barrier phases)
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    // Q_t of an item is staged by this warp group; the NEXT item's Q_t is staged right after
+    // the last softmax step of the current one (its last QK_t has completed, so sQ_t is free),
+    // before the epilogue: the MMA warp issues the next item's QKs while the epilogue drains O
+    auto next_item = [&](int item) {  // next item with rows of this tile group
+      for (; item < n_items; item += gridDim.x) {
+        const TileItem it = items[item];
+        const int n = it.n_rows - t * M;
+        if (n > 0) break;
+      }
+      return item;
+    };
+    auto load_q = [&](int item) {  // stage Q_t of `item` into sQt; returns this row's q row
       const TileItem it = items[item];
-      const ItemGeom G = geom(it, g);
-      // this warp group's tile: selects, not a runtime-indexed (local-memory) array access
-      const int rows_t = t ? G.rows_t[1] : G.rows_t[0];
-      const int nt_t = t ? G.nt_t[1] : G.nt_t[0];
-      if (rows_t == 0) continue;
-      const bool is_list = it.flags & kTileList, causal = it.flags & kTileCausal;
+      const int rows_t = min(M, it.n_rows - t * M);
       const int r = it.r0 + t * M + row;
-      const bool valid = row < rows_t;
       int qrow = 0;
-      if (valid) {
+      if (row < rows_t) {
         const int tok = r / g;
-        qrow = is_list ? __ldg(p.row_list + it.row_src + tok) : it.row_src + tok;
+        qrow = (it.flags & kTileList) ? __ldg(p.row_list + it.row_src + tok) : it.row_src + tok;
         const uint4 *src = reinterpret_cast<const uint4 *>(p.q + (int64_t)qrow * p.q_stride_tok +
                                                            (int64_t)(it.kv_head * g + r % g) * p.q_stride_head);
+        uint4 v[D / 8];
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4 *>(sQt + kmaj_off(row, c * 8, M)) = __ldg(src + c);
+        for (int c = 0; c < D / 8; ++c) v[c] = __ldg(src + c);
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4 *>(sQt + kmaj_off(row, c * 8, M)) = v[c];
       } else {
 #pragma unroll
         for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4 *>(sQt + kmaj_off(row, c * 8, M)) = make_uint4(0, 0, 0, 0);
       }
       fence_proxy_async();
       mbar_arrive(&bar_q[t]);
-
+      return qrow;
+    };
+    int item = next_item(blockIdx.x);
+    int qrow_next = item < n_items ? load_q(item) : 0;
+    for (; item < n_items;) {
+      const TileItem it = items[item];
+      const ItemGeom G = geom(it, g);
+      const int rows_t = t ? G.rows_t[1] : G.rows_t[0];
+      const int nt_t = t ? G.nt_t[1] : G.nt_t[0];
+      const bool causal = it.flags & kTileCausal;
+      const int r = it.r0 + t * M + row;
+      const bool valid = row < rows_t;
+      const int qrow = qrow_next;
+      const int nxt = next_item(item + gridDim.x);
       const int pos = (causal && valid) ? it.pos0 + r / g : INT32_MAX;
       const int k1 = t ? G.k1_t[1] : G.k1_t[0];
       const float sl2 = p.scale_log2;
@@ -519,6 +540,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         mbar_arrive(&bar_p[t]);
         if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
       }
+      if (nxt < n_items) qrow_next = load_q(nxt);
       // ------------------------------- epilogue -------------------------------
       mbar_wait(&bar_o[t], (Gs - 1) & 1);
       fence_after();
@@ -558,6 +580,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         else if (p.lse) p.lse[(int64_t)qrow * p.Hq + hq] = lse;
       }
       fence_before();  // O reads done before this group's next item overwrites O
+      item = nxt;
     }
   }
   fence_before();
