@@ -173,7 +173,15 @@ def run_ours(args, rank, world, local):
     batch = K.Batch(wl.batch, dev)
     pristine_dev = batch.table_dev.clone()
     pristine_host = batch.table_host.copy()
-    new_mask = pristine_host == -1
+    # the table entries kv_append fills (the -1 entries of each request's new positions): the
+    # per-step reset and the release touch only these, not the whole host table
+    _ql = np.diff(batch.q_indptr)
+    new_idx = np.array([i * pristine_host.shape[1] + kb
+                        for i in range(len(batch.ctx_len))
+                        for kb in range((int(batch.ctx_len[i]) - int(_ql[i])) // 16, (int(batch.ctx_len[i]) + 15) // 16)
+                        if pristine_host[i, kb] == -1], dtype=np.int64)
+    table_flat = batch.table_host.reshape(-1)
+    assert np.shares_memory(table_flat, batch.table_host)
     ws_app = torch.empty(K.kv_append_workspace_size(batch), dtype=torch.uint8, device=dev)
     ws_att = torch.empty(K.hybrid_attention_workspace_size(batch), dtype=torch.uint8, device=dev)
     q, k_new, v_new = wl.q, wl.k_new, wl.v_new
@@ -252,7 +260,7 @@ def run_ours(args, rank, world, local):
             ev_join.record(ev_stream)
             n += 3
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
-        batch.table_host[...] = pristine_host
+        table_flat[new_idx] = -1  # == pristine_host (only these entries change)
         if ev is not None and gate_attn:  # before the append: the attention pair follows it directly
             stream.wait_event(ev_keys)
         K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
@@ -266,7 +274,8 @@ def run_ours(args, rank, world, local):
             kdist.gather_outputs(out, gbuf)
         if ev is not None:
             stream.wait_event(ev_join)
-        allocated = batch.table_host[new_mask & (batch.table_host >= 0)]
+        allocated = table_flat[new_idx]
+        allocated = allocated[allocated >= 0]
         K.kv_release_blocks(pool, allocated, stream=stream)
         n += 1
         launches["n"] += n
@@ -333,7 +342,7 @@ def run_ours(args, rank, world, local):
             ev_join.record(ev_stream)
             n += 3
         batch.table_dev.copy_(pristine_dev, non_blocking=True)
-        batch.table_host[...] = pristine_host
+        table_flat[new_idx] = -1  # == pristine_host (only these entries change)
         stream.wait_event(ev_in[i % 2])
         if i >= 2:
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done
@@ -354,7 +363,8 @@ def run_ours(args, rank, world, local):
             ev_out[i % 2].record(cs_out)
         if ev is not None:
             stream.wait_event(ev_join)
-        allocated = batch.table_host[new_mask & (batch.table_host >= 0)]
+        allocated = table_flat[new_idx]
+        allocated = allocated[allocated >= 0]
         K.kv_release_blocks(pool, allocated, stream=stream)
         n += 1
         launches["n"] += n
@@ -408,6 +418,10 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         step()
     barrier()
+    # the partial reset restores the whole pristine host table (every step starts identically)
+    chk = batch.table_host.copy()
+    chk.reshape(-1)[new_idx] = -1
+    assert np.array_equal(chk, pristine_host), "kv_append changed table entries outside new_idx"
     plan0 = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
     stats = plan0.stats()
     plan0.close()

@@ -20,6 +20,52 @@
 using namespace kva;
 
 // ------------------------------------------------------------------------------------------
+// host-side section timer (diagnostics): KVA_HOST_PROF=1 accumulates steady-clock time per
+// labelled section and prints the per-call means at exit
+// ------------------------------------------------------------------------------------------
+namespace {
+struct HostProf {
+  bool on = false;
+  std::mutex mu;
+  std::vector<std::pair<std::string, std::vector<double>>> acc;
+  HostProf() {
+    const char *e = getenv("KVA_HOST_PROF");
+    on = e && e[0] == '1';
+  }
+  void add(const char *name, double us) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto &a : acc)
+      if (a.first == name) {
+        a.second.push_back(us);
+        return;
+      }
+    acc.push_back({name, {us}});
+  }
+  ~HostProf() {  // median and mean per label (first calls include lazy module loading)
+    if (!on) return;
+    for (auto &a : acc) {
+      std::vector<double> v = a.second;
+      std::sort(v.begin(), v.end());
+      double m = 0;
+      for (double x : v) m += x;
+      fprintf(stderr, "[kva host] %-28s median %8.2f us  mean %8.2f us  (%zu calls)\n", a.first.c_str(),
+              v[v.size() / 2], m / v.size(), v.size());
+    }
+  }
+};
+HostProf g_hprof;
+struct HSection {  // HSection t; ... t.lap("label");
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char *name) {
+    if (!g_hprof.on) return;
+    const auto n = std::chrono::steady_clock::now();
+    g_hprof.add(name, std::chrono::duration<double, std::micro>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
 // errors
 // ------------------------------------------------------------------------------------------
 static thread_local std::string g_err = "";
@@ -470,7 +516,9 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
                                 const void *v_new, int64_t stride_tok, int32_t *deficit,
                                 void *workspace, size_t ws_bytes, kva_stream_t stream) {
   if (deficit) *deficit = 0;
+  HSection hs;
   kva_status st = validate_desc(p, b, 1);
+  hs.lap("append.validate");
   if (st != KVA_OK) return st;
   if (b->num_reqs == 0) return KVA_OK;
   const int Hkv = b->num_kv_heads, d = b->head_dim, nb = p->desc.num_blocks;
@@ -512,6 +560,7 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
   if (!workspace || ws_bytes < up)
     return fail(KVA_ERR_INVALID, "kv_append workspace too small (%zu < %zu)", ws_bytes, up);
   // allocate: descriptor order, positions ascending, smallest free id first (reading #13)
+  hs.lap("append.count");
   std::vector<uint32_t> fh = p->free_host;  // commit only after everything is enqueued
   int scan = 0;
   for (int i = 0; i < b->num_reqs; ++i) {
@@ -525,8 +574,10 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
       ap.ids.push_back(scan);
     }
   }
+  hs.lap("append.alloc");
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  hs.lap("append.guard");
   // earlier side-stream appends may still read this workspace / write the pool
   if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));
   // Split by the kernel that reads the new rows: decode-class requests (served by the decode
@@ -593,7 +644,9 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     }
     CUDA_TRY(p->staging.upload(slot, workspace, off, s));
   }
+  hs.lap("append.lists");
   CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, al, s));
+  hs.lap("append.launch_alloc");
   // Default: both appends on `stream` (decode-class rows first); the tile kernel, launched next
   // with programmatic dependent launch, becomes resident while the tile-path rows are still
   // being written and waits for them in-kernel, and the decode kernel (dependent of the tile
@@ -631,11 +684,13 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_app, 0));  // the tile kernel's stream
     p->app_pending = true;
   }
+  hs.lap("append.launch_append");
   p->active_blocks += ap.need;  // every new block belongs to a running request
   // commit host state: free mirror + caller's host table mirror
   p->free_host.swap(fh);
   p->n_free -= ap.need;
   for (size_t j = 0; j < ap.ids.size(); ++j) b->block_table_host[ap.tbl_idx[j]] = ap.ids[j];
+  hs.lap("append.commit");
   return KVA_OK;
 }
 
@@ -902,12 +957,15 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
   *out = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
+  HSection hs;
   kva_status st = validate_desc(p, b, 0);
+  hs.lap("plan.validate");
   if (st != KVA_OK) return st;
   const auto t1 = std::chrono::steady_clock::now();
   PlanBuild pb;
   build_plan(b, pb);
   const auto t2 = std::chrono::steady_clock::now();
+  hs.lap("plan.build");
   size_t arrays = 0;
   const size_t need = plan_bytes(pb, b->head_dim, &arrays);
   if (!ws || ws_bytes < need)
@@ -915,7 +973,9 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(KVA_ERR_INVALID, "workspace must be 256-B aligned");
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  hs.lap("plan.guard");
   kva_plan *pl = new kva_plan();
+  hs.lap("plan.new");
   pl->device = p->desc.device;
   pl->tmk = p->tmk;
   pl->tmv = p->tmv;
@@ -944,6 +1004,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   pl->tiles.ptr = nullptr;
   if (tile_inline) std::copy(pb.tile.begin(), pb.tile.end(), pl->tiles.item);
   const bool need_upload = (!pb.tile.empty() && !tile_inline) || !pb.row_list.empty() || !dec_inline || !mrg_inline;
+  hs.lap("plan.inline_copy");
   if (need_upload) {
     Staging::Slot *slot = nullptr;
     cudaError_t e = p->staging.get(arrays, &slot);
@@ -985,6 +1046,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     }
     pl->uploaded = true;
   }
+  hs.lap("plan.upload");
   pl->tile_tc = tile_use_tc();
   pl->tile_impl = tile_impl_for(b);
   pl->aux = p->aux;
@@ -1017,6 +1079,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     }
   }
   const auto t3 = std::chrono::steady_clock::now();
+  hs.lap("plan.split");
   pl->stats.host_validate_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
   pl->stats.host_build_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
   pl->stats.host_total_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t3 - t0).count();
@@ -1066,6 +1129,7 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   const int vec = out_dtype == KVA_OUT_F32 ? 16 : 8;
   if ((reinterpret_cast<uintptr_t>(out) & (vec - 1)) || (o_st % 4) || (o_sh % 4))
     return fail(KVA_ERR_INVALID, "out must be %d-byte aligned with strides %% 4 == 0", vec);
+  HSection hs;
   DeviceGuard dg(pl->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   AttnParams p = pl->p;
@@ -1143,13 +1207,17 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
+    hs.lap("run.prep");
     CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, pl->tile_ctas, s, pl->has3d ? &pl->tmv3 : nullptr,
                              pl->has3d ? &pl->tmk4 : nullptr));
+    hs.lap("run.launch_tile");
     CUDA_TRY(launch_decode(p, &pl->tmk, &pl->tmv, pl->dec, pl->n_dec, s, /*pdl=*/true,
                            pl->has3d ? &pl->tmk3 : nullptr, pl->has3d ? &pl->tmv3 : nullptr));
+    hs.lap("run.launch_decode");
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
+    hs.lap("run.launch_merge");
     return KVA_OK;
   }
   // sequential mode: decode first (its CTAs share SMs with a concurrently running eviction
@@ -1212,6 +1280,7 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
                                         kva_stream_t stream) {
   if (!p || n < 0 || (n > 0 && !ids)) return fail(KVA_ERR_INVALID, "bad arguments");
   if (n == 0) return KVA_OK;
+  HSection hs;
   const int nb = p->desc.num_blocks;
   std::vector<uint8_t> seen(nb, 0);
   for (int64_t i = 0; i < n; ++i) {
@@ -1220,6 +1289,7 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
       return fail(KVA_ERR_INVALID, "block %d is already free", ids[i]);
     if (seen[ids[i]]++) return fail(KVA_ERR_INVALID, "block %d listed twice", ids[i]);
   }
+  hs.lap("release.check");
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));  // released blocks' writes
@@ -1229,6 +1299,7 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
     const int cnt = (int)std::min<int64_t>(kReleaseBatch, n - off);
     CUDA_TRY(launch_release_ids(p->desc.free_bits, ids + off, cnt, s));
   }
+  hs.lap("release.launch");
   for (int64_t i = 0; i < n; ++i) p->free_host[ids[i] >> 5] |= 1u << (ids[i] & 31);
   p->n_free += n;
   return KVA_OK;
@@ -1313,7 +1384,9 @@ extern "C" kva_status kv_manager_step_workspace_size(const kva_block_meta *m, co
 extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys,
                                       int64_t *n_active, void *ws, size_t ws_bytes, kva_stream_t stream) {
   int64_t tot = 0;
+  HSection hs;
   kva_status st = manager_validate(m, u, &tot);
+  hs.lap("manager.validate");
   if (st != KVA_OK) return st;
   if (m->num_blocks > 0 && !keys) return fail(KVA_ERR_INVALID, "keys_out required");
   const int32_t nc = tot > 0 ? u->n_chains : 0;
@@ -1335,11 +1408,13 @@ extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager
     std::memcpy(h + o_st, u->chain_state, (size_t)nc);
     CUDA_TRY(g_mgr_staging.upload(slot, ws, o_st + nc, s));
   }
+  hs.lap("manager.upload");
   CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now,
                                reinterpret_cast<const int32_t *>(w), tot,
                                reinterpret_cast<const int32_t *>(w + o_ind), w + o_st, nc,
                                reinterpret_cast<int32_t *>(w + o_win), u->recount != 0, u->pool_ids,
                                u->pool_len, u->del_ids, u->del_len, keys, n_active, s));
+  hs.lap("manager.launch");
   return KVA_OK;
 }
 
