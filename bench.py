@@ -294,9 +294,14 @@ def run_ours(args, rank, world, local):
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
         fork_next["v"] = True  # the first timed step's eviction work starts after s
+        host_t = []
         for i in range(nsteps):
+            t_h = time.perf_counter()
             step(time_idx=i if time_kernels else None)
+            host_t.append(time.perf_counter() - t_h)
         e.record(stream)
+        if os.environ.get("KVA_BENCH_HOST_TIMING") == "1":  # diagnostics: host enqueue time per step
+            sys.stderr.write(f"[bench host] step enqueue median {1e6 * sorted(host_t)[len(host_t) // 2]:.1f} us\n")
         barrier()
         ms = s.elapsed_time(e) / nsteps
         if world > 1:

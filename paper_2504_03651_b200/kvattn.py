@@ -235,7 +235,18 @@ class Batch:
         self.total_q = int(self.q_indptr[-1]) if len(self.q_indptr) else 0
         self._desc = None
 
+    def __setattr__(self, name, value):
+        # any rebinding (a new array / tensor object) invalidates the cached descriptor; in-place
+        # writes into the arrays keep their addresses and need no rebuild
+        if name != "_desc":
+            object.__setattr__(self, "_desc", None)
+        object.__setattr__(self, name, value)
+
     def desc(self):
+        """The C descriptor (cached: building it costs ~8 us of ctypes marshalling per call)."""
+        d = self._desc
+        if d is not None and d.block_table == self.table_dev.data_ptr():
+            return d
         a = lambda x: None if x is None else x.ctypes.data
         d = BatchDesc(self.num_reqs, self.num_q_heads, self.num_kv_heads, self.head_dim,
                       a(self.req_type), a(self.q_indptr), a(self.ctx_len), self.table_dev.data_ptr(),
