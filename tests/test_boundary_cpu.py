@@ -112,3 +112,22 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt, f
+
+
+def test_batch_descriptor_cache_follows_rebinding(K):
+    """Batch.desc() is cached (ctypes marshalling per call is host time on the hot path); a
+    rebound array is picked up, an in-place write needs no rebuild (same addresses), and the
+    validation result follows the data either way."""
+    wl = W.make_workload("tiny", preappended=True)
+    nb = wl.batch["num_blocks"]
+    b = _batch(K, wl)
+    d1 = b.desc()
+    assert b.desc() is d1 and K.validate_batch(b, nb, 0) == K.OK
+    row = b.table_host[0].copy()
+    b.table_host[0, 0] = -1                       # in place: same descriptor, new verdict
+    assert b.desc() is d1 and K.validate_batch(b, nb, 0) == K.ERR_INVALID
+    b.table_host[0] = row
+    b.ctx_len = b.ctx_len.copy()                  # rebinding: a new descriptor
+    d2 = b.desc()
+    assert d2 is not d1 and d2.ctx_len == b.ctx_len.ctypes.data
+    assert K.validate_batch(b, nb, 0) == K.OK
