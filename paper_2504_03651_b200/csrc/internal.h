@@ -139,7 +139,8 @@ cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const 
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
                           const int32_t *block_table, int32_t max_blocks,
-                          const ReqList<AppendReq> &reqs, int32_t total_new_tok, cudaStream_t s);
+                          const ReqList<AppendReq> &reqs, int32_t total_new_tok, cudaStream_t s,
+                          bool early_trigger = false);
 cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
                               const uint16_t *depth, int64_t n, uint64_t *keys, cudaStream_t s);
 cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth,

@@ -121,10 +121,15 @@ __global__ void __launch_bounds__(256) append_kernel(
     const uint16_t *__restrict__ k_new, const uint16_t *__restrict__ v_new, int64_t stride_tok,
     uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
     const int32_t *__restrict__ block_table, int32_t max_blocks, const __grid_constant__ ReqList<AppendReq> L,
-    int32_t total_new_tok) {
-  // the tile kernel launched right after this append (programmatic dependent launch) may
-  // become resident now; it waits (griddepcontrol.wait) before reading the pool
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    int32_t total_new_tok, int32_t early_trigger) {
+  // early_trigger (the append of the tile-path rows only): the tile kernel launched right
+  // after it (programmatic dependent launch) may become resident now; it waits
+  // (griddepcontrol.wait) before reading the pool.  The decode kernel, a dependent of the tile
+  // kernel that does NOT wait, reads only decode-class rows, which an earlier append on the
+  // stream wrote.  The decode-class append never triggers early: a tile kernel launched right
+  // after it (no tile-path rows) starts only once those rows are complete, and so does the
+  // decode kernel behind it.
+  if (early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const AppendReq *reqs = L.ptr ? L.ptr : L.req;
   const int32_t *tok_pre = L.ptr ? L.pre_ptr : L.pre;
   const int num_reqs = L.n;
@@ -181,14 +186,16 @@ __global__ void __launch_bounds__(256) append_kernel(
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
                           const int32_t *block_table, int32_t max_blocks,
-                          const ReqList<AppendReq> &L, int32_t total_new_tok, cudaStream_t s) {
+                          const ReqList<AppendReq> &L, int32_t total_new_tok, cudaStream_t s,
+                          bool early_trigger) {
   const int64_t units = (int64_t)total_new_tok * Hkv;
   if (units <= 0 || L.n <= 0) return cudaSuccess;
   static bool carve = (cudaFuncSetAttribute(append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared), true);
   (void)carve;
   append_kernel<<<(unsigned)((units + kUnitsPerCta - 1) / kUnitsPerCta), 256, 0, s>>>(
-      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, L, total_new_tok);
+      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, L, total_new_tok,
+      early_trigger ? 1 : 0);
   return cudaGetLastError();
 }
 

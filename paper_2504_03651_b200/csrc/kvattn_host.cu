@@ -660,11 +660,11 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
                            stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
                            static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
                            b->max_blocks, la, pa.back(), s));
-    if (!rb.empty())
+    if (!rb.empty())  // the tile kernel (PDL) may start while these rows are written
       CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
                              stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
                              static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                             b->max_blocks, lb, pbv.back(), s));
+                             b->max_blocks, lb, pbv.back(), s, /*early_trigger=*/true));
   }
   if (side && !rb.empty()) {  // fork after the table update, before the decode-class append
     CUDA_TRY(cudaEventRecord(p->ev_afork, s));
