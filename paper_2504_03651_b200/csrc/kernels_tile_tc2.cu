@@ -432,9 +432,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       for (int j = 0; j < nt_t; ++j, ++Gs) {
         if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
         mbar_wait(&bar_s[t], Gs & 1);  // QK_t(j) done; so is PV_t(j-1) (issued earlier)
-        // PV_t(j-1) is complete too: the commit behind bar_s tracks every earlier tcgen05 op of
-        // the MMA thread.  bar_o is waited only in the epilogue (no phase is skipped twice: the
-        // next item's PVs need this group's P first)
+        if (j >= 1) mbar_wait(&bar_o[t], (Gs - 1) & 1);  // observe that completion (no-op wait)
         if (kTimestamps && (warp == 4 || warp == 8)) ts(1 + t);
         fence_after();
         if (p.debug_flags & 1) {  // diagnostics: measure the MMA/TMA pipeline without softmax
