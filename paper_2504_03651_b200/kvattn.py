@@ -426,14 +426,23 @@ class ManagerStep:
         ci, cids, cst = chains if isinstance(chains, tuple) else self.chains_csr(chains)
         plen = pool_ids.numel() if pool_ids is not None else 0
         dlen = del_ids.numel() if del_ids is not None else 0
-        u = ManagerUpdate(int(now) & 0xFFFFFFFF, len(ci) - 1, ci.ctypes.data, cids.ctypes.data,
-                          cst.ctypes.data, 1 if recount else 0, _ptr(pool_ids) if plen else None, plen,
-                          _ptr(del_ids) if dlen else None, dlen)
-        need = ctypes.c_size_t()
         L = load()
-        _check(L.kv_manager_step_workspace_size(ctypes.byref(self.meta), ctypes.byref(u), ctypes.byref(need)))
-        if self.ws.numel() < need.value:
-            self.ws = torch.empty(need.value, dtype=torch.uint8, device=self.state.device)
+        # the marshalled update is reused while the same arrays / tensors are passed (the cache
+        # holds references, so an identity cannot be recycled while cached); in-place edits of
+        # the arrays keep their addresses
+        key = (ci, cids, cst, pool_ids, del_ids, plen, dlen, int(ci[-1]) if len(ci) else 0)
+        c = getattr(self, "_ucache", None)
+        if (c is None or any(a is not b for a, b in zip(c[0][:5], key[:5])) or c[0][5:] != key[5:]):
+            u = ManagerUpdate(0, len(ci) - 1, ci.ctypes.data, cids.ctypes.data, cst.ctypes.data, 0,
+                              _ptr(pool_ids) if plen else None, plen, _ptr(del_ids) if dlen else None, dlen)
+            need = ctypes.c_size_t()
+            _check(L.kv_manager_step_workspace_size(ctypes.byref(self.meta), ctypes.byref(u), ctypes.byref(need)))
+            c = self._ucache = (key, u, need.value)
+        _, u, need_b = c
+        u.now = int(now) & 0xFFFFFFFF
+        u.recount = 1 if recount else 0
+        if self.ws.numel() < need_b:
+            self.ws = torch.empty(need_b, dtype=torch.uint8, device=self.state.device)
         _check(L.kv_manager_step(ctypes.byref(self.meta), ctypes.byref(u), _ptr(self.keys), _ptr(self.n_active),
                                  _ptr(self.ws), self.ws.numel(), _stream(stream)))
         return self.keys
