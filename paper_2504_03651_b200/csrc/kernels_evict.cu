@@ -66,7 +66,9 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 // block's winner slot is reset, then takes the max element index listing it (atomicMax), and
 // only that element applies its chain's state.  Then the reference counts (recount: zeroed
 // by the host + atomicAdd; incremental: atomicAdd / atomicSub), then keys + active count.
-__global__ void manager_win_init_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win) {
+__global__ void manager_win_init_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win,
+                                        unsigned long long *__restrict__ n_active) {
+  if (n_active && blockIdx.x == 0 && threadIdx.x == 0) *n_active = 0ull;  // counted by the keys kernel
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr; e += (int64_t)gridDim.x * blockDim.x)
     win[tr_ids[e]] = -1;
 }
@@ -160,11 +162,13 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (recount) e = cudaMemsetAsync(rc, 0, (size_t)n * sizeof(uint32_t), s);
-  if (e == cudaSuccess && n_active) e = cudaMemsetAsync(n_active, 0, sizeof(int64_t), s);
+  // the active count is zeroed by the winner-init kernel when there are transitions
+  if (e == cudaSuccess && n_active && n_tr <= 0) e = cudaMemsetAsync(n_active, 0, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   auto grid_for = [](int64_t m) { return (int)std::min<int64_t>((m + 255) / 256, 148 * 8); };
   if (n_tr > 0) {
-    manager_win_init_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win);
+    manager_win_init_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win,
+                                                           reinterpret_cast<unsigned long long *>(n_active));
     manager_win_max_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
