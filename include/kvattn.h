@@ -203,6 +203,8 @@ kva_status kva_plan_set_timing_events(kva_plan *plan, void *tile_begin, void *ti
                                       void *decode_begin, void *decode_end);
 /* Number of kernel launches hybrid_attention_run_phases(plan, phases) enqueues. */
 kva_status kva_plan_launch_count(const kva_plan *plan, int32_t phases, int32_t *n_launches);
+/* Plans use the pool's side stream and events: destroy every plan of a pool (and let its
+ * enqueued work finish) before kv_pool_destroy. */
 kva_status kva_plan_destroy(kva_plan *plan);
 /* Plan statistics: counts of work items per kernel and algorithmic bytes/flops. */
 typedef struct {

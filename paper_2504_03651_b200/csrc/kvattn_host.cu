@@ -284,6 +284,9 @@ struct kva_pool {
   // kv_append's side-stream part (rows read only by the tile kernel): ev_app marks its end;
   // later calls on the pool order themselves after it (kv_pool_sync for anything else)
   cudaEvent_t ev_afork = nullptr, ev_app = nullptr;
+  // plan uploads (shared by the pool's plans: a plan created later re-records them, which only
+  // orders an earlier plan's run after the later upload as well — never a cycle)
+  cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
   bool app_pending = false;
   cudaStream_t aux_lo = nullptr;  // least-priority side stream of those writes (yields to decode)
   // burst-reserve threshold: < 0 = none
@@ -330,7 +333,9 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_afork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_app, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&p->ev_app, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_up0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_up1, cudaEventDisableTiming) != cudaSuccess) {
       delete p;
       return fail(KVA_ERR_CUDA, "creating the side stream/events failed");
     }
@@ -366,6 +371,8 @@ extern "C" kva_status kv_pool_destroy(kva_pool *p) {
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->ev_afork) cudaEventDestroy(p->ev_afork);
     if (p->ev_app) cudaEventDestroy(p->ev_app);
+    if (p->ev_up0) cudaEventDestroy(p->ev_up0);
+    if (p->ev_up1) cudaEventDestroy(p->ev_up1);
   }
   delete p;
   return KVA_OK;
@@ -708,14 +715,11 @@ struct kva_plan {
   TileList tiles;                          // tcgen05 tile items (inline kernel parameter or uploaded)
   int n_dec = 0, n_tile = 0, n_mrows = 0;  // work units: decode (split, head), tiles, merge (row, head)
   // the plan arrays are uploaded on the pool's side stream (ordered after `stream`'s prior work
-  // by ev_up0); a kernel that reads uploaded arrays on `stream` first waits ev_up1
+  // by ev_up0); a kernel that reads uploaded arrays on `stream` first waits ev_up1 (both owned
+  // by the pool)
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
   bool uploaded = false;
   kva_pool *pool = nullptr;  // for the side-stream append event (the pool outlives its plans)
-  ~kva_plan() {
-    if (ev_up0) cudaEventDestroy(ev_up0);
-    if (ev_up1) cudaEventDestroy(ev_up1);
-  }
   int device = 0;
   bool tile_tc = true;
   int tile_impl = 2;
@@ -1034,9 +1038,9 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     // upload on the side stream, ordered after everything already enqueued on `stream`
     // (WAR on the workspace), so the decode launch on `stream` does not queue behind a
     // copy-engine transfer
-    e = cudaEventCreateWithFlags(&pl->ev_up0, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_up1, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(pl->ev_up0, s);
+    pl->ev_up0 = p->ev_up0;
+    pl->ev_up1 = p->ev_up1;
+    e = cudaEventRecord(pl->ev_up0, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->aux, pl->ev_up0, 0);
     if (e == cudaSuccess) e = p->staging.upload(slot, ws, off, p->aux);
     if (e == cudaSuccess) e = cudaEventRecord(pl->ev_up1, p->aux);
