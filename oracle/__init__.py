@@ -67,9 +67,11 @@ def _load():
                                               i32, P, P, i32, i32, P, P, P, P]
             _lib.orc_evict_keys.argtypes = [P, P, P, P, i64, P]
             _lib.orc_evict_select.argtypes = [P, i64, i64, P, P]
+            _lib.orc_evict_select_apply.argtypes = [P, i64, i64, P, P, P]
+            _lib.orc_release_blocks.argtypes = [P, i32, P, i64]
             _lib.orc_validate.argtypes = [i32, i32, i32, i32, P, P, P, i32, P, i32, P, i32]
             for f in ("orc_attention", "orc_attention_rows", "orc_kv_append", "orc_kv_append_t",
-                      "orc_manager_step",
+                      "orc_manager_step", "orc_evict_select_apply", "orc_release_blocks",
                       "orc_evict_keys", "orc_evict_select", "orc_validate"):
                 getattr(_lib, f).restype = ctypes.c_int
     return _lib
@@ -241,6 +243,29 @@ def evict_select(keys, k: int):
     nsel = np.zeros(1, np.int64)
     s = lib.orc_evict_select(_p(kk), len(kk), int(k), _p(out), _p(nsel))
     return s, out[: int(nsel[0])]
+
+
+def evict_select_apply(keys, k: int, free_bits):
+    """evict_select with apply: the same order, then the selected
+    blocks' free bits are set.  Works on a copy; returns (status, ids, free_bits')."""
+    lib = _load()
+    kk = _c(keys, np.uint64)
+    out = np.full(max(int(k), 0), -1, np.int32)
+    nsel = np.zeros(1, np.int64)
+    fb = _c(free_bits, np.uint32).copy()
+    assert len(fb) >= (len(kk) + 31) // 32
+    s = lib.orc_evict_select_apply(_p(kk), len(kk), int(k), _p(out), _p(nsel), _p(fb))
+    return s, out[: int(nsel[0])], fb
+
+
+def release_blocks(free_bits, num_blocks: int, ids):
+    """Return blocks to the free pool: each id allocated and listed once,
+    else INVALID with nothing changed.  Works on a copy; returns (status, free_bits')."""
+    lib = _load()
+    fb = _c(free_bits, np.uint32).copy()
+    ii = _c(ids, np.int32)
+    s = lib.orc_release_blocks(_p(fb), int(num_blocks), _p(ii), len(ii))
+    return s, fb
 
 
 def validate(b: dict):

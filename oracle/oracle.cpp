@@ -449,6 +449,36 @@ int orc_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_id
   return m < k ? ST_EVICTION_SHORT : ST_OK;
 }
 
+/* evict_select with apply (SURVEY §8(c) c1.4 "if apply is set, mark the selected blocks
+ * free"; P:440 the evicted blocks return to the free table; "victims ... removed").
+ * The selection is orc_evict_select's; then, for each selected id, its free bit (bit b%32 of
+ * word b/32) is set.  free_bits has ceil(n/32) words; nothing else changes. */
+int orc_evict_select_apply(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
+                           int64_t *n_selected, uint32_t *free_bits) {
+  int st = orc_evict_select(keys, n, k, out_ids, n_selected);
+  if (st != ST_OK && st != ST_EVICTION_SHORT) return st;
+  for (int64_t s = 0; s < *n_selected; ++s)
+    free_bits[out_ids[s] / 32] |= 1u << (out_ids[s] % 32);
+  return st;
+}
+
+/* Release blocks to the free pool ("preempts and release the KV cache of the victim
+ * request"; S:143-146 removed blocks become free).  Every id must be in [0, num_blocks),
+ * currently allocated (free bit clear) and listed once, else INVALID with nothing changed;
+ * then each id's free bit is set. */
+int orc_release_blocks(uint32_t *free_bits, int32_t num_blocks, const int32_t *ids, int64_t n) {
+  std::vector<char> seen(num_blocks > 0 ? num_blocks : 0, 0);
+  for (int64_t s = 0; s < n; ++s) {
+    int32_t b = ids[s];
+    if (b < 0 || b >= num_blocks) return ST_INVALID;
+    if ((free_bits[b / 32] >> (b % 32)) & 1u) return ST_INVALID;  /* already free */
+    if (seen[b]) return ST_INVALID;                                  /* listed twice */
+    seen[b] = 1;
+  }
+  for (int64_t s = 0; s < n; ++s) free_bits[ids[s] / 32] |= 1u << (ids[s] % 32);
+  return ST_OK;
+}
+
 /* Group validation only (for boundary tests). */
 int orc_validate(int32_t num_reqs, int32_t Hq, int32_t Hkv, int32_t d,
                  const int32_t *q_indptr, const int32_t *ctx_len,

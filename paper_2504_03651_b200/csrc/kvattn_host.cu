@@ -287,6 +287,10 @@ struct kva_pool {
   // plan uploads (shared by the pool's plans: a plan created later re-records them, which only
   // orders an earlier plan's run after the later upload as well — never a cycle)
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
+  // guards the staging ring and the record -> wait -> upload -> record sequence on the shared
+  // upload events (calls on one pool must be serialised anyway; this keeps a
+  // violation from silently reordering another plan's upload)
+  std::mutex up_mu;
   bool app_pending = false;
   cudaStream_t aux_lo = nullptr;  // least-priority side stream of those writes (yields to decode)
   // burst-reserve threshold: < 0 = none
@@ -509,6 +513,8 @@ static size_t append_upload_bytes(int R, int64_t nalloc) {  // both request list
 
 extern "C" kva_status kv_append_workspace_size(const kva_batch_desc *b, size_t *bytes) {
   if (!b || !bytes) return fail(KVA_ERR_INVALID, "null argument");
+  // the same descriptor checks kv_append runs (any block id passes: no pool here)
+  if (kva_status st = validate_batch(b, INT32_MAX, 1); st != KVA_OK) return st;
   // upper bound on allocations: every new position's block
   int64_t nalloc = 0;
   for (int i = 0; i < b->num_reqs; ++i) {
@@ -626,6 +632,7 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     std::copy(ap.ids.begin(), ap.ids.end(), al.ids);
   }
   if (up_a || up_b || up_al) {
+    std::lock_guard<std::mutex> lk(p->up_mu);
     Staging::Slot *slot = nullptr;
     CUDA_TRY(p->staging.get(up, &slot));
     uint8_t *h = static_cast<uint8_t *>(slot->host);
@@ -948,8 +955,9 @@ static size_t plan_bytes(const PlanBuild &pb, int d, size_t *arrays_bytes) {
 
 extern "C" kva_status hybrid_attention_workspace_size(const kva_batch_desc *b, size_t *bytes) {
   if (!b || !bytes) return fail(KVA_ERR_INVALID, "null argument");
-  if (b->num_kv_heads <= 0 || b->num_q_heads % b->num_kv_heads)
-    return fail(KVA_ERR_INVALID, "bad head counts");
+  // build_plan walks group chains and indexes per-group arrays: the descriptor is validated
+  // first (groups, parents, shapes; the table's unallocated new-position entries may be -1)
+  if (kva_status st = validate_batch(b, INT32_MAX, 1); st != KVA_OK) return st;
   PlanBuild pb;
   build_plan(b, pb);
   *bytes = plan_bytes(pb, b->head_dim, nullptr);
@@ -1010,6 +1018,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   const bool need_upload = (!pb.tile.empty() && !tile_inline) || !pb.row_list.empty() || !dec_inline || !mrg_inline;
   hs.lap("plan.inline_copy");
   if (need_upload) {
+    std::lock_guard<std::mutex> lk(p->up_mu);
     Staging::Slot *slot = nullptr;
     cudaError_t e = p->staging.get(arrays, &slot);
     if (e != cudaSuccess) {

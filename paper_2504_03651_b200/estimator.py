@@ -135,7 +135,20 @@ def calibrate(samples, floor_grid: int = 64) -> Params:
     A = np.stack([mx, mn], 1)
     if np.linalg.matrix_rank(A) < 2:
         raise CalibrationError("pure-decode samples do not separate max(L) from mean(L)")
-    (gamma, delta), *_ = np.linalg.lstsq(A / td[:, None], np.ones_like(td), rcond=None)
+    # relative least squares under the SPEC invariant gamma, delta >= 0 (CostModelParams): a
+    # two-variable NNLS — the unconstrained optimum if it is feasible, else the better of the
+    # two one-coefficient fits on the boundary (KKT for a convex quadratic with two bounds)
+    Aw, bw = A / td[:, None], np.ones_like(td)
+    (gamma, delta), *_ = np.linalg.lstsq(Aw, bw, rcond=None)
+    if gamma < 0 or delta < 0:
+        cand = []
+        for j in (0, 1):
+            col = Aw[:, j]
+            x = max(float(col @ bw / (col @ col)), 0.0)
+            sol = [0.0, 0.0]
+            sol[j] = x
+            cand.append((float(((Aw @ np.array(sol)) - bw) @ ((Aw @ np.array(sol)) - bw)), sol))
+        gamma, delta = min(cand)[1]
 
     # lambda: 1-D least squares on mixed samples, T = lam*(max - min) + min
     p0 = Params(alpha, beta, c, float(gamma), float(delta), 0.0)

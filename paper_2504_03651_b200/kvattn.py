@@ -274,8 +274,14 @@ def last_error() -> str:
     return load().kva_last_error().decode()
 
 
-def _workspace(nbytes, device):
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+def _workspace(nbytes, device, stream=None):
+    """Default scratch for a call enqueued on `stream`.  The caching allocator tracks the
+    stream a block was allocated on; the block is marked as used by `stream` as well, so it is
+    not handed to a new allocation before `stream`'s work on it has finished."""
+    ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    if stream is not None and stream != torch.cuda.current_stream(ws.device):
+        ws.record_stream(stream)
+    return ws
 
 
 def kv_append_workspace_size(batch: Batch) -> int:
@@ -290,7 +296,7 @@ def kv_append(pool: Pool, batch: Batch, k_new: torch.Tensor, v_new: torch.Tensor
     L = load()
     d = batch.desc()
     if workspace is None:
-        workspace = _workspace(kv_append_workspace_size(batch), k_new.device)
+        workspace = _workspace(kv_append_workspace_size(batch), k_new.device, stream)
     deficit = ctypes.c_int32(0)
     st = L.kv_append(pool.handle, ctypes.byref(d), _ptr(k_new), _ptr(v_new), k_new.stride(0),
                      ctypes.byref(deficit), _ptr(workspace), workspace.numel(), _stream(stream))
@@ -312,8 +318,9 @@ class Plan:
         L = load()
         device = device or pool.k_pool.device
         if workspace is None:
-            workspace = _workspace(hybrid_attention_workspace_size(batch), device)
+            workspace = _workspace(hybrid_attention_workspace_size(batch), device, stream)
         self.workspace = workspace
+        self.pool = pool  # the C plan uses the pool's side stream / events: keep it alive
         self.handle = ctypes.c_void_p()
         _check(L.hybrid_attention_plan(pool.handle, ctypes.byref(batch.desc()), _ptr(workspace),
                                        workspace.numel(), _stream(stream), ctypes.byref(self.handle)))
@@ -370,7 +377,7 @@ def hybrid_attention(pool: Pool, batch: Batch, q: torch.Tensor, out: torch.Tenso
     if out is None:
         out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
     if workspace is None:
-        workspace = _workspace(hybrid_attention_workspace_size(batch), q.device)
+        workspace = _workspace(hybrid_attention_workspace_size(batch), q.device, stream)
     od = OUT_F32 if out.dtype == torch.float32 else OUT_BF16
     _check(L.hybrid_attention(pool.handle, ctypes.byref(batch.desc()), _ptr(q), q.stride(0),
                               q.stride(1), _ptr(out), out.stride(0), out.stride(1), od, _ptr(lse),
@@ -464,7 +471,7 @@ def evict_select(keys: torch.Tensor, k: int, out_ids: torch.Tensor | None = None
     if out_ids is None:
         out_ids = torch.empty(max(k, 1), dtype=torch.int32, device=keys.device)
     if workspace is None:
-        workspace = _workspace(evict_select_workspace_size(n, k), keys.device)
+        workspace = _workspace(evict_select_workspace_size(n, k), keys.device, stream)
     nsel = ctypes.c_int64(0)
     if not sync:
         _check(L.evict_select(_ptr(keys), n, k, _ptr(out_ids), None, int(bool(apply)),

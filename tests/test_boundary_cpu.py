@@ -131,3 +131,32 @@ def test_batch_descriptor_cache_follows_rebinding(K):
     d2 = b.desc()
     assert d2 is not d1 and d2.ctx_len == b.ctx_len.ctypes.data
     assert K.validate_batch(b, nb, 0) == K.OK
+
+
+def test_workspace_size_validates_groups(K):
+    """*_workspace_size runs the call's descriptor checks first: a self- or cyclic parent and an
+    out-of-range group_of return ERR_GROUP (the planner walks parent chains and indexes
+    per-group arrays; it must never see such a descriptor)."""
+    import subprocess
+    import sys
+    reqs = [W.ReqSpec(W.OFFLINE_DECODE, 100, 1, 0), W.ReqSpec(W.OFFLINE_DECODE, 120, 1, 1)]
+    wl = W.make_workload(W.custom_config("wg", 4, 2, 64, 17, reqs, [2, 4], group_parent=[-1, 0]))
+    assert K.hybrid_attention_workspace_size(_batch(K, wl)) > 0
+    cases = [dict(group_parent=np.array([-1, 1], np.int32)),            # self-parented
+             dict(group_parent=np.array([1, 0], np.int32)),             # cycle / later parent
+             dict(group_of=np.array([0, 5], np.int32))]                 # group out of range
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, workloads as W, "
+            "paper_2504_03651_b200 as K\n" % ROOT +
+            "reqs=[W.ReqSpec(W.OFFLINE_DECODE,100,1,0),W.ReqSpec(W.OFFLINE_DECODE,120,1,1)]\n"
+            "wl=W.make_workload(W.custom_config('wg',4,2,64,17,reqs,[2,4],group_parent=[-1,0]))\n"
+            "for over in %r:\n"
+            "    b=dict(wl.batch); b.update({k: np.array(v, np.int32) for k, v in over.items()})\n"
+            "    for f in (K.hybrid_attention_workspace_size, K.kv_append_workspace_size):\n"
+            "        try:\n"
+            "            f(K.Batch(b, None)); print('OK')\n"
+            "        except K.KvaError as e:\n"
+            "            print(e.status)\n" % [{k: v.tolist() for k, v in c.items()} for c in cases])
+    # in a subprocess with a timeout: the bug this guards against was a hang
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split() == [str(K.ERR_GROUP)] * (2 * len(cases)), r.stdout

@@ -92,3 +92,25 @@ def test_prose_form_round_trip():
     f = E.calibrate(s)
     assert _rel(f.mu, 0.3) < 0.01
     assert E.batch_time_prose(0.3, 0.1, p) == pytest.approx(0.33, rel=1e-12)
+
+
+def test_calibration_params_nonnegative_under_noise():
+    """SPEC CostModelParams invariant (gamma, delta >= 0): decode samples whose noise makes the
+    unconstrained fit put a negative weight on max(L) still calibrate to non-negative
+    coefficients, and decode_time stays monotone in every L."""
+    rng = np.random.default_rng(3)
+    base = _samples(P, rng)
+    dec = []
+    for _ in range(8):    # max(L) anti-correlated with time: unconstrained gamma < 0
+        n = int(rng.integers(4, 40))
+        lens = list(rng.integers(50, 400, n))
+        lens[0] = int(rng.integers(400, 4000))
+        t = 2e-5 * float(np.mean(lens)) * (1 + 0.05 * rng.standard_normal()) - 1e-7 * lens[0] + 1e-4
+        dec.append({"prefill_spans": [], "decode_lens": lens, "time_s": max(t, 1e-6)})
+    samples = [s for s in base if not (s["decode_lens"] and not s["prefill_spans"])] + dec
+    raw, *_ = np.linalg.lstsq(np.array([[max(s["decode_lens"]), np.mean(s["decode_lens"])] for s in dec])
+                              / np.array([s["time_s"] for s in dec])[:, None], np.ones(len(dec)), rcond=None)
+    assert min(raw) < 0        # the case the constraint exists for
+    fit = E.calibrate(samples)
+    assert fit.gamma >= 0 and fit.delta >= 0
+    assert E.decode_time([100, 200], fit) <= E.decode_time([100, 300], fit)

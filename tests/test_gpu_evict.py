@@ -53,23 +53,30 @@ def test_evict_random_small(seed):
     assert np.array_equal(ids.cpu().numpy(), ref_ids)
 
 
-def test_evict_apply_marks_free():
+@pytest.mark.parametrize("n,k", [(4096, 100), (1 << 20, 1 << 16)])
+def test_evict_apply_marks_free(n, k):
+    """apply = 1: the device free bitmap and the pool's host mirror
+    afterwards equal the oracle's evict_select_apply on the same pre-existing bitmap (the
+    state-0 blocks free), bit-exact, at a small size and at the full `evict` size."""
     import paper_2504_03651_b200 as K
-    ev = W.make_evict(n=4096, k=100, seed=9)
+    ev = W.make_evict(n=n, k=k, seed=9)
     keys = _gpu_keys(ev)
-    nb = 4096
-    kp = torch.zeros((nb, 1, 16, 64), dtype=torch.bfloat16, device="cuda")
-    bits = np.zeros((nb + 31) // 32, np.uint32)
+    bits = np.zeros((n + 31) // 32, np.uint32)
+    idx = np.nonzero(ev.state == 0)[0]
+    np.bitwise_or.at(bits, idx // 32, np.uint32(1) << (idx % 32).astype(np.uint32))
+    _, ref_keys = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    s, ref_ids, ref_bits = oracle.evict_select_apply(ref_keys, k, bits)
+    kp = torch.zeros((n, 1, 16, 64), dtype=torch.bfloat16, device="cuda")
     fb = K.free_bits_tensor(bits, "cuda")
-    pool = K.Pool(kp, kp.clone(), fb)
-    ids, n = K.evict_select(keys, 100, apply=True, pool=pool)
+    pool = K.Pool(kp, kp, fb)
+    n0 = pool.free_count()
+    ids, nsel = K.evict_select(keys, k, apply=True, pool=pool)
     torch.cuda.synchronize()
-    got = fb.cpu().numpy().view(np.uint32)
-    exp = np.zeros_like(bits)
-    for i in ids.cpu().numpy():
-        exp[i // 32] |= np.uint32(1 << (i % 32))
-    assert np.array_equal(got, exp)
-    assert pool.free_count() == 100
+    assert nsel == len(ref_ids) and np.array_equal(ids.cpu().numpy(), ref_ids)
+    assert np.array_equal(fb.cpu().numpy().view(np.uint32), ref_bits)
+    assert pool.free_count() == n0 + nsel
+    pool.resync()                       # the mirror re-read from the device agrees
+    assert pool.free_count() == n0 + nsel
 
 
 def test_evict_short():
@@ -101,8 +108,12 @@ def test_release_blocks_roundtrip_and_errors():
             wl.free_bits.view(np.uint8), bitorder="little"))[0][-1])], np.int32))
     with pytest.raises(K.KvaError):            # listed twice
         K.kv_release_blocks(pool, np.array([new_ids[0], new_ids[0]], np.int32))
+    fb_before = fb.cpu().numpy().view(np.uint32).copy()
+    s_ref, fb_ref = oracle.release_blocks(fb_before, wl.batch["num_blocks"], new_ids)
+    assert s_ref == oracle.OK
     K.kv_release_blocks(pool, new_ids)
     torch.cuda.synchronize()
+    assert np.array_equal(fb.cpu().numpy().view(np.uint32), fb_ref)
     assert pool.free_count() == n0
     assert np.array_equal(fb.cpu().numpy().view(np.uint32), wl.free_bits)
     batch2 = K.Batch(wl.batch, dev)

@@ -224,13 +224,26 @@ def test_shared_prefix_prefill_members():
     assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
 
 
-@pytest.mark.parametrize("name", ["llama7b", "qwen14b", "llama70b", "qwen14b-p"])
-def test_full_size_sampled(name):
-    """BASELINE configs at full size, in the bench's launch configuration; sampled rows."""
+def _full_size(name):
     wl = W.make_workload(name, device="cuda")
-    gg = gpu_step(wl, out_dtype=torch.float32)
     wl_cpu = W.Workload(wl.cfg, wl.batch, wl.k_pool.cpu(), wl.v_pool.cpu(), wl.free_bits,
                         wl.k_new.cpu(), wl.v_new.cpu(), wl.q.cpu(), wl.head_range, wl.kv_head_range)
+    return wl, wl_cpu
+
+
+def _check_sampled(gg, wl_cpu, rows, heads, bf16=False):
+    ref, ref_lse, bt = oracle_rows(wl_cpu, rows, heads)
+    assert np.array_equal(gg["batch"].table_dev.cpu().numpy(), bt)
+    o = gg["out"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
+    l = gg["lse"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
+    return assert_attention_close(o, l, ref, ref_lse, bf16=bf16)
+
+
+@pytest.mark.parametrize("name", ["llama7b", "qwen14b", "qwen14b-p"])
+def test_full_size_sampled(name):
+    """BASELINE configs at full size, in the bench's launch configuration; sampled rows."""
+    wl, wl_cpu = _full_size(name)
+    gg = gpu_step(wl, out_dtype=torch.float32)
     b = wl.batch
     Hq = b["num_q_heads"]
     rng = np.random.default_rng(5)
@@ -239,11 +252,94 @@ def test_full_size_sampled(name):
     rows = np.array(dec_rows * 2 + list(rng.integers(0, wl.total_q, 512)), np.int32)
     heads = np.concatenate([np.zeros(len(dec_rows), np.int32), np.full(len(dec_rows), Hq - 1, np.int32),
                             rng.integers(0, Hq, 512).astype(np.int32)])
-    ref, ref_lse, bt = oracle_rows(wl_cpu, rows, heads)
-    assert np.array_equal(gg["batch"].table_dev.cpu().numpy(), bt)
-    o = gg["out"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
-    l = gg["lse"][torch.from_numpy(rows).long(), torch.from_numpy(heads).long()]
-    assert_attention_close(o, l, ref, ref_lse)
+    _check_sampled(gg, wl_cpu, rows, heads)
+
+
+def test_full_size_llama7b_bf16_output():
+    """The bench's own output mode (bf16 O, llama7b = configs[1]) at full size: every decode row
+    x every 4th head + 1,024 chunk (row, head) pairs, against the H7 bound 1e-2 + 2^-8|O|."""
+    wl, wl_cpu = _full_size("llama7b")
+    gg = gpu_step(wl, out_dtype=torch.bfloat16)
+    b = wl.batch
+    Hq = b["num_q_heads"]
+    qi = np.asarray(b["q_indptr"])
+    rng = np.random.default_rng(7)
+    dec = [int(qi[i]) for i in range(b["num_reqs"]) if qi[i + 1] - qi[i] == 1]
+    rows = [r for r in dec for _ in range(0, Hq, 4)]
+    heads = [h for _ in dec for h in range(0, Hq, 4)]
+    chunk_rows = np.concatenate([np.arange(qi[i], qi[i + 1]) for i in range(b["num_reqs"]) if qi[i + 1] - qi[i] > 1])
+    rows += rng.choice(chunk_rows, 1024).tolist()
+    heads += rng.integers(0, Hq, 1024).tolist()
+    _check_sampled(gg, wl_cpu, np.array(rows, np.int32), np.array(heads, np.int32), bf16=True)
+
+
+def test_full_size_llama70b_decode_all_heads_and_chunk_boundaries():
+    """llama70b (configs[4]) at full size, SURVEY §8(d) sampling: every decode row x all 64
+    heads, plus 4,096 seeded (chunk row, head) pairs of which a third sit on tcgen05 item
+    boundaries (first / last token of a 128-row M-tile = 16 tokens x g 8), a third put the causal
+    diagonal on the first / last key of a 128-key tile, and a third are uniform."""
+    wl, wl_cpu = _full_size("llama70b")
+    gg = gpu_step(wl, out_dtype=torch.float32)
+    b = wl.batch
+    Hq = b["num_q_heads"]
+    g = Hq // b["num_kv_heads"]
+    qi = np.asarray(b["q_indptr"])
+    ctx = np.asarray(b["ctx_len"])
+    rng = np.random.default_rng(70)
+    dec = [int(qi[i]) for i in range(b["num_reqs"]) if qi[i + 1] - qi[i] == 1]
+    rows = [r for r in dec for _ in range(Hq)]
+    heads = [h for _ in dec for h in range(Hq)]
+    chunks = [i for i in range(b["num_reqs"]) if qi[i + 1] - qi[i] > 1]
+    tok_per_tile = 128 // g
+    for kind in range(3):
+        for _ in range(4096 // 3 + (1 if kind == 0 else 0)):
+            i = chunks[int(rng.integers(len(chunks)))]
+            ql = int(qi[i + 1] - qi[i])
+            pos0 = int(ctx[i]) - ql
+            if kind == 0:
+                t = int(rng.integers(ql // tok_per_tile)) * tok_per_tile + int(rng.choice([0, tok_per_tile - 1]))
+            elif kind == 1:
+                p = (int(rng.integers(pos0, int(ctx[i]))) // 128) * 128 + int(rng.choice([0, 127]))
+                t = min(max(p - pos0, 0), ql - 1)
+            else:
+                t = int(rng.integers(ql))
+            rows.append(int(qi[i]) + t)
+            heads.append(int(rng.choice([0, g - 1])) + g * int(rng.integers(Hq // g)) if kind < 2
+                         else int(rng.integers(Hq)))
+    assert len(rows) - len(dec) * Hq == 4096
+    _check_sampled(gg, wl_cpu, np.array(rows, np.int32), np.array(heads, np.int32))
+
+
+def test_many_requests_uploaded_lists():
+    """> kInlineReqs (400) decode-class requests, > kInlineTiles (560) tile items and
+    > kInlineAlloc (1,536) new blocks: the decode / merge / append request lists, the tile list
+    and the allocation list are uploaded instead of passed as kernel parameters.  1,200 decode
+    -class requests (q_len x g <= 16, g = 1), 500 of them cascade members of one group, and 420
+    short prefill chunks; element-by-element against the oracle, tables / pool / bitmap
+    bit-exact."""
+    rng = np.random.default_rng(61)
+    reqs = []
+    for _ in range(700):
+        ql = int(rng.integers(6, 17))
+        reqs.append(W.ReqSpec(W.ONLINE_DECODE, ql + int(rng.integers(0, 700)), ql))
+    for _ in range(500):
+        ql = int(rng.integers(1, 5))
+        reqs.append(W.ReqSpec(W.OFFLINE_DECODE, 8 * 16 + ql + int(rng.integers(0, 200)), ql, 0))
+    for _ in range(420):
+        ql = int(rng.integers(17, 65))
+        reqs.append(W.ReqSpec(W.OFFLINE_PREFILL, ql + int(rng.integers(0, 200)), ql))
+    order = rng.permutation(len(reqs))
+    reqs = [reqs[i] for i in order]
+    wl = W.make_workload(W.custom_config("many", 2, 2, 64, 61, reqs, [8]))
+    bt = wl.batch["block_table"]
+    new_blocks = sum(int((bt[i, :(r.ctx + 15) // 16] == -1).sum()) for i, r in enumerate(reqs))
+    assert new_blocks > 1536, new_blocks
+    gg = gpu_step(wl)
+    r = oracle_step(wl)
+    _check_append(gg, r)
+    assert_attention_close(gg["out"], gg["lse"], r["out"], r["lse"])
+    st = gg["plan"].stats()
+    assert st["n_tile_items"] > 560 and st["n_cascade_items"] > 0, st
 
 
 def test_append_side_stream_ordering():

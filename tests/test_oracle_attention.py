@@ -293,3 +293,33 @@ def test_validation_errors():
     bad = dict(b)
     bad["num_q_heads"] = 3  # Hq % Hkv != 0
     assert oracle.validate(bad) == oracle.INVALID
+
+
+@pytest.mark.parametrize("d,g,seed", [(64, 1, 21), (128, 4, 22), (64, 5, 23)])
+def test_attention_rows_pinned(d, g, seed):
+    """orc_attention_rows (the reference of every full-size sampled GPU test and of the
+    cpu_baseline) against the dense numpy textbook definition, row by row, and bit-exactly
+    against orc_attention: every request's first and last query row (request boundaries,
+    including its causal diagonal) plus random rows, every head, in shuffled order."""
+    rng = np.random.default_rng(seed)
+    cfg = _random_cfg(rng, d, g, nreq=5, seed=seed, with_group=True)
+    wl = W.make_workload(cfg, preappended=True)
+    b, kp, vp, q = _post_state(wl)
+    qi = np.asarray(b["q_indptr"])
+    Hq = b["num_q_heads"]
+    bnd = sorted({int(x) for i in range(b["num_reqs"]) for x in (qi[i], qi[i + 1] - 1)})
+    rnd = rng.integers(0, int(qi[-1]), 40).tolist()
+    rows = np.array([r for r in bnd + rnd for _ in range(Hq)], np.int32)
+    heads = np.array([h for _ in bnd + rnd for h in range(Hq)], np.int32)
+    perm = rng.permutation(len(rows))
+    rows, heads = rows[perm], heads[perm]
+    st, o_rows, l_rows = oracle.attention_rows(b, kp, vp, q, rows, heads, nthreads=3)
+    assert st == oracle.OK
+    ref, ref_lse = _dense_reference(b, kp, vp, q)
+    np.testing.assert_allclose(o_rows, ref[rows, heads], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(l_rows, ref_lse[rows, heads], rtol=0, atol=1e-12)
+    st, full, full_lse = oracle.attention(b, kp, vp, q)
+    assert np.array_equal(o_rows, full[rows, heads]) and np.array_equal(l_rows, full_lse[rows, heads])
+    # out-of-range rows / heads are rejected
+    assert oracle.attention_rows(b, kp, vp, q, [int(qi[-1])], [0])[0] == oracle.INVALID
+    assert oracle.attention_rows(b, kp, vp, q, [0], [Hq])[0] == oracle.INVALID

@@ -146,3 +146,47 @@ def test_large_select_matches_heap():
     s, got = oracle.evict_select(keys, ev.k)
     heap = HeapFreeTable(ev.state, ev.rc, ev.lat, ev.depth)
     assert list(got) == heap.evict(ev.k)
+
+
+def _bits_of(fb, n):
+    return {b for b in range(n) if (int(fb[b // 32]) >> (b % 32)) & 1}
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_evict_apply_sets_exactly_the_victims_free(seed):
+    """SURVEY c1.4 apply (P:440 the victims return to the free table; S:146 removed): the free
+    set afterwards is the free set before plus exactly the selected ids — set arithmetic on
+    Python sets, with the selection itself pinned by the heap free table above."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 3000))
+    state = rng.integers(0, 6, n).astype(np.uint8)
+    rc = np.where(rng.random(n) < 0.3, rng.integers(1, 5, n), 0).astype(np.uint32)
+    lat = rng.integers(0, 20, n).astype(np.uint32)
+    fb = np.zeros((n + 31) // 32, np.uint32)
+    for b in range(n):
+        if state[b] == 0:
+            fb[b // 32] |= np.uint32(1 << (b % 32))
+    _, keys = oracle.evict_keys(state, rc, lat, None)
+    k = int(rng.integers(0, n + 5))
+    s, ids = oracle.evict_select(keys, k)
+    s2, ids2, fb2 = oracle.evict_select_apply(keys, k, fb)
+    assert s2 == s and list(ids2) == list(ids)
+    before = {b for b in range(n) if state[b] == 0}
+    assert _bits_of(fb2, n) == before | set(ids.tolist())
+    assert not (before & set(ids.tolist()))   # a free block is never a victim (key inf)
+    assert len(_bits_of(fb2, n)) == len(before) + len(ids)
+
+
+def test_release_blocks_oracle():
+    """P:448 release / S:143-146: allocated ids become free; a free, duplicated or
+    out-of-range id is INVALID and changes nothing."""
+    n = 70
+    fb = np.zeros(3, np.uint32)
+    fb[0] = 0x0000FFFF            # blocks 0..15 free
+    s, fb2 = oracle.release_blocks(fb, n, [20, 69, 16])
+    assert s == oracle.OK and _bits_of(fb2, n) == set(range(16)) | {16, 20, 69}
+    for bad in ([3], [20, 20], [70], [-1], [21, 5]):
+        s, fb3 = oracle.release_blocks(fb, n, bad)
+        assert s == oracle.INVALID and np.array_equal(fb3, fb), bad
+    s, fb4 = oracle.release_blocks(fb, n, [])
+    assert s == oracle.OK and np.array_equal(fb4, fb)
