@@ -45,16 +45,23 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch + process group + max-over-ranks only (no GPU; CPU tests)")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (default); gloo only to smoke-test the N>1 code path on one GPU")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------------------------------
-def dist_setup(args):
+def dist_setup(args, cpu=False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and cpu:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+        return rank, world, local
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -242,6 +249,7 @@ def run_ours(args, rank, world, local):
     # KVA_BENCH_EVICT_PIPELINE=0: fork every step (serialises it behind the previous step).
     evict_pipeline = os.environ.get("KVA_BENCH_EVICT_PIPELINE", "1") == "1"
     fork_next = {"v": True}
+    gather_on = {"v": True}
 
     def step(time_idx=None):
         n = 0
@@ -273,7 +281,7 @@ def run_ours(args, rank, world, local):
             plan.set_span_buffer(spans[time_idx])
             span_used.append(time_idx)
         plan.run(q, out, lse, stream=stream)
-        if world > 1:
+        if world > 1 and gather_on["v"]:
             kdist.gather_outputs(out, gbuf)
         if ev is not None:
             stream.wait_event(ev_join)
@@ -466,6 +474,28 @@ def run_ours(args, rank, world, local):
                 ts_.append(a.elapsed_time(b))
         plan_s.close()
         dec_alone = statistics.median(ts_)
+    gather = None
+    if world > 1:
+        # a7 reported on its own: the all-gather alone, and the step without it
+        import torch.distributed as dist
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            kdist.gather_outputs(out, gbuf)
+        b.record(stream)
+        barrier()
+        g_ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+        dist.all_reduce(g_ms, op=dist.ReduceOp.MAX)
+        gather_on["v"] = False
+        ms_ng = timed(args.steps)
+        gather_on["v"] = True
+        recv = (world - 1) * out.numel() * out.element_size()
+        gather = {"ms": g_ms.item(), "bytes_received_per_rank": recv,
+                  "GBps_per_rank": recv / (g_ms.item() * 1e-3) / 1e9,
+                  "ms_per_step_without_gather": ms_ng, "ms_per_step_with_gather": ms,
+                  "backend": dist.get_backend(), "timing": "CUDA events around K back-to-back "
+                  "all_gather_into_tensor calls on the bench stream, max over ranks"}
     ms_e2e = None
     if not args.no_e2e and (not args.profile or os.environ.get("KVA_BENCH_E2E_IN_PROFILE") == "1"):
         ms_e2e = timed_e2e_pipelined(args.steps)
@@ -505,6 +535,8 @@ def run_ours(args, rank, world, local):
                      "peak_source": peak_src},
         "clocks": ck, "gpu_launches": gpu_launches,
     }
+    if gather is not None:
+        res["config"]["gather"] = gather
     tile_avg = statistics.mean(tile_ms) if tile_ms else 0.0
     if tile_avg > 1.5 * (dec_avg if dec_ms else 0.0):
         # tensor-bound batch (long prefill chunks): the dominant kernel is the tcgen05 tile kernel
@@ -612,8 +644,59 @@ def run_reference(args, rank, world):
     }
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_spawn(args):
+    """`--gpus N` (N > 1) outside torchrun: re-launch this command under torch.distributed.run
+    with N ranks on 127.0.0.1 (one process per GPU) and exit with its status.  Under torchrun
+    (WORLD_SIZE set) the world size must equal --gpus.  NCCL init logging goes to stderr so the
+    ranks and the transport are on record."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if args.gpus != int(ws) and "--gpus" in " ".join(sys.argv):
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    import subprocess
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    raise SystemExit(subprocess.run(cmd, env=env).returncode)
+
+
+def dry_run(args, rank, world):
+    """--dry-run: the launch / process-group / max-over-ranks plumbing without a GPU (CPU tests
+    of the spawn path): every rank contributes its rank to a MAX all-reduce; rank 0 prints."""
+    import torch.distributed as dist
+    t = torch.tensor([float(rank)])
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "max_rank": int(t.item()),
+                          "backend": dist.get_backend() if world > 1 else None}), flush=True)
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
+    if args.dry_run:
+        rank, world, _ = dist_setup(args, cpu=True)
+        dry_run(args, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

@@ -76,3 +76,21 @@ def test_head_ranges_cover_all_heads():
             assert all(a[1] == b[0] for a, b in zip(qs, qs[1:]))
     with pytest.raises(ValueError):
         head_ranges(4, 4, 8, 0)
+
+
+def test_bench_gpus_n_spawns_n_ranks():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself under
+    torch.distributed.run with 2 ranks (127.0.0.1); --dry-run exercises that launch, the
+    process group and the max-over-ranks reduction without a GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout          # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["max_rank"] == 1 and d["backend"] == "gloo"
