@@ -150,11 +150,12 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
                                 cudaStream_t s);
 size_t evict_select_ws_bytes(int64_t n, int64_t k);
+// evict_select: one cooperative kernel of `ctas` CTAs (<= 0: #SMs / 2); free_bits != nullptr:
+// the selected blocks are also marked free (apply)
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
-                                int64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t s);
+                                int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
+                                int ctas, cudaStream_t s);
 constexpr int kReleaseBatch = 4000;  // ids per release launch (kernel-parameter payload)
 cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s);
-cudaError_t launch_free_ids(uint32_t *free_bits, const int32_t *ids, const int64_t *d_count,
-                            int64_t k, cudaStream_t s);
 
 }  // namespace kva

@@ -1,0 +1,762 @@
+// kernels_select.cu — evict_select: the first k blocks of the eviction order.
+//
+// Order: "When evicting the KV cache, we will first consider the priority of the KV cache
+// entry, and then the last access time" (priorities P:331-334, encoded into the u64
+// keys by evict_keys, readings #18-#20); equal keys are broken by block id.  The result
+// is the ascending (key, id) order of the evictable keys (key != UINT64_MAX), truncated to k
+// ("victims ... in eviction order").
+//
+// One cooperative persistent kernel (C CTAs x 512 threads, grid barriers between phases) runs
+// a most-significant-digit radix partition truncated to the top k, on a "composite" key that
+// is unique per block: the bits that vary among the evictable keys (constant bits carry no
+// order), followed by the block id.  Composite order == (key, id) order.
+//   phase 0   OR / OR-of-complements / count of the evictable keys (-> which bits vary, E)
+//   phase 1   histogram of the top 11-bit digit; each CTA reserves its range in every bin
+//   round r   every CTA scans the digit-r histogram, finds the boundary bin b holding rank
+//             k-1 of the current segment, and scatters its elements: bins < b are taken
+//             (their output range is known: bin start = exclusive prefix), bin b is either
+//             taken whole, finished by one sort (<= kCap elements) or becomes the next
+//             round's segment (its digit r+1 is counted in the same pass), bins > b dropped
+//   buckets   every taken bin with >= 2 elements is a bucket at a known output offset: warps
+//             sort buckets of <= 256 pairs in registers, CTAs sort <= 2048 (registers +
+//             shared-memory exchanges), larger ones are partitioned again by one CTA (next
+//             digit) -> next level
+// The k-th element's bin shrinks ~2048x per round, so the uniform-ish `evict` workload needs
+// two rounds over 2^20 and ~125k keys, and one bucket level: four grid barriers in all.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace kva {
+namespace {
+
+constexpr int kT = 512;              // threads per CTA
+constexpr int kNW = kT / 32;
+constexpr int kDig = 11;             // radix digit bits
+constexpr int kBins = 1 << kDig;
+constexpr int kCap = 2048;           // pairs one CTA sorts in shared memory (24 KB)
+constexpr int kWarpMax = 256;        // pairs one warp sorts in registers (8 per lane)
+constexpr int kMaxRuns = 8;          // runs of varying key bits kept apart (more are merged)
+constexpr int kMaxLevels = 16;
+constexpr int kMaxC = 512;
+constexpr uint64_t kInf = ~0ull;
+
+struct Part {  // per-CTA phase-0 result
+  unsigned long long o, a, c, pad;
+};
+struct Ctl {
+  unsigned long long t[32];  // phase timestamps of CTA 0 (%globaltimer ns; diagnostics)
+  unsigned int n_small[kMaxLevels], n_large[kMaxLevels], n_big[kMaxLevels];
+  unsigned int rounds, levels, pad[2];
+};
+
+struct Layout {
+  size_t ctl, part, hist, wk[2], wi[2], sk[2], si[2], rs[2], rl[2], total;
+  int64_t nw, ns, nrec;
+};
+inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+Layout layout(int64_t n, int64_t k) {
+  Layout L{};
+  L.nw = std::max<int64_t>(n, 1);
+  L.ns = std::min<int64_t>(std::max<int64_t>(k, 1), L.nw) + kCap;
+  L.nrec = L.ns / 2 + 64;
+  size_t p = 0;
+  auto take = [&](size_t bytes) { const size_t at = p; p = up256(p + bytes); return at; };
+  L.ctl = take(sizeof(Ctl));
+  L.part = take(sizeof(Part) * kMaxC);
+  L.hist = take(sizeof(unsigned int) * 3 * kBins);
+  for (int i = 0; i < 2; ++i) L.wk[i] = take(8 * (size_t)L.nw);
+  for (int i = 0; i < 2; ++i) L.wi[i] = take(4 * (size_t)L.nw);
+  for (int i = 0; i < 2; ++i) L.sk[i] = take(8 * (size_t)L.ns);
+  for (int i = 0; i < 2; ++i) L.si[i] = take(4 * (size_t)L.ns);
+  for (int i = 0; i < 2; ++i) L.rs[i] = take(16 * (size_t)L.nrec);
+  for (int i = 0; i < 2; ++i) L.rl[i] = take(16 * (size_t)L.nrec);
+  L.total = p;
+  return L;
+}
+
+struct SelArgs {
+  const uint64_t *keys;
+  int64_t n, k;
+  int32_t *out_ids;
+  int64_t *d_count;
+  uint32_t *free_bits;  // nullable: apply (mark the selected blocks free)
+  Ctl *ctl;
+  Part *part;
+  unsigned int *hist;  // [3][kBins]
+  uint64_t *wk[2];     // segment (key, id) ping-pong, [n]
+  int32_t *wi[2];
+  uint64_t *sk[2];     // output-aligned staging ping-pong, [k + kCap]
+  int32_t *si[2];
+  uint4 *rs[2], *rl[2];  // bucket records (off, size, take, dig | src << 8): <= 256 / larger
+};
+
+__device__ __forceinline__ bool pair_gt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
+  return ka > kb || (ka == kb && ia > ib);
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan (kT threads); `total` = block sum.  Ends with a barrier.
+__device__ __forceinline__ unsigned block_scan(unsigned v, unsigned *s_w, unsigned &total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = lane < kNW ? s_w[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kNW) s_w[lane] = t;
+  }
+  __syncthreads();
+  total = s_w[kNW - 1];
+  const unsigned r = x - v + (w > 0 ? s_w[w - 1] : 0u);
+  __syncthreads();
+  return r;
+}
+
+// Shared-memory histogram increment (d < 0: none).  The lanes sharing the first valid lane's
+// digit (the common case: neighbouring blocks of one chain share their class) are counted by
+// one atomic, the others one by one.
+__device__ __forceinline__ void hist_add(unsigned *h, int d) {
+  const unsigned valid = __ballot_sync(0xffffffffu, d >= 0);
+  if (!valid) return;
+  const int leader = __ffs(valid) - 1;
+  const int d0 = __shfl_sync(0xffffffffu, d, leader);
+  const unsigned same = __ballot_sync(0xffffffffu, d == d0);
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&h[d0], (unsigned)__popc(same));
+  else if (d >= 0 && d != d0) atomicAdd(&h[d], 1u);
+}
+
+// Position of this lane's element in bin d (d < 0: none): the pre-increment value of cur[d]
+// plus its rank among the lanes that share the first valid lane's digit (one atomic for them).
+__device__ __forceinline__ unsigned bin_claim(unsigned *cur, int d) {
+  const unsigned valid = __ballot_sync(0xffffffffu, d >= 0);
+  if (!valid) return 0u;
+  const int leader = __ffs(valid) - 1;
+  const int d0 = __shfl_sync(0xffffffffu, d, leader);
+  const unsigned same = __ballot_sync(0xffffffffu, d == d0);
+  unsigned base = 0;
+  if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&cur[d0], (unsigned)__popc(same));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (d == d0) return base + __popc(same & lanemask_lt());
+  return d >= 0 ? atomicAdd(&cur[d], 1u) : 0u;
+}
+
+// Add this CTA's bin counts to the grid's (global) counts; s_off[d] = this CTA's offset in bin d.
+// The kBins / kT atomics of a thread are issued before any result is used (L2 round trips).
+__device__ __forceinline__ void flush_counts(const unsigned *s_cnt, unsigned *s_off, unsigned *g) {
+  constexpr int U = kBins / kT;
+  unsigned v[U], o[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = s_cnt[threadIdx.x + u * kT];
+#pragma unroll
+  for (int u = 0; u < U; ++u) o[u] = v[u] ? atomicAdd(&g[threadIdx.x + u * kT], v[u]) : 0u;
+#pragma unroll
+  for (int u = 0; u < U; ++u) s_off[threadIdx.x + u * kT] = o[u];
+}
+
+// The composite key: the compressed key ck (the varying key bits, runs packed towards bit 0,
+// most significant run highest: ck = sum_i (key & mask_i) >> sh_i, an order-preserving
+// injection on the evictable keys), then idb id bits.  Segments, staging and buckets hold
+// (ck, id); only the input keys are compressed (once per pass over them).
+struct Comp {
+  int nr, idb, B, nd;
+  unsigned long long cst;  // the key bits outside the runs (equal in every evictable key)
+  unsigned long long mask[kMaxRuns];
+  int sh[kMaxRuns];
+};
+// the first 4 runs in registers (the `evict` keys have 3: priority code, LAT, depth), the
+// rest read from shared memory
+struct CompR {
+  int nr;
+  unsigned long long m0, m1, m2, m3;
+  int s0, s1, s2, s3;
+  const Comp *c;
+};
+__device__ __forceinline__ CompR comp_regs(const Comp &c) {
+  CompR r;
+  r.nr = c.nr;
+  r.m0 = c.mask[0]; r.m1 = c.mask[1]; r.m2 = c.mask[2]; r.m3 = c.mask[3];
+  r.s0 = c.sh[0]; r.s1 = c.sh[1]; r.s2 = c.sh[2]; r.s3 = c.sh[3];
+  r.c = &c;
+  return r;
+}
+__device__ __forceinline__ uint64_t compress(const CompR &r, uint64_t key) {
+  uint64_t ck = ((key & r.m0) >> r.s0) | ((key & r.m1) >> r.s1) | ((key & r.m2) >> r.s2) | ((key & r.m3) >> r.s3);
+  if (r.nr > 4)
+    for (int i = 4; i < r.nr; ++i) ck |= (key & r.c->mask[i]) >> r.c->sh[i];
+  return ck;
+}
+// bits [lo, lo + w) of the composite (ck << idb) | id, w <= kDig
+struct DigSel {
+  int lo, w, idb;
+};
+__device__ __forceinline__ DigSel dig_sel(const Comp &c, int r) {
+  const int hi = c.B - kDig * r;
+  DigSel d;
+  d.lo = hi > kDig ? hi - kDig : 0;
+  d.w = hi > d.lo ? hi - d.lo : 0;
+  d.idb = c.idb;
+  return d;
+}
+__device__ __forceinline__ int digit(const DigSel &s, uint64_t ck, int32_t id) {
+  uint64_t v;
+  if (s.lo >= s.idb) v = ck >> (s.lo - s.idb);
+  else v = (ck << (s.idb - s.lo)) | ((uint64_t)(uint32_t)id >> s.lo);  // idb - lo <= kDig
+  return (int)((uint32_t)v & ((1u << s.w) - 1u));
+}
+
+__device__ __forceinline__ void emit(const SelArgs &a, int64_t pos, int32_t id) {
+  a.out_ids[pos] = id;
+  if (a.free_bits) atomicOr(a.free_bits + (id >> 5), 1u << (id & 31));
+}
+
+// Bitonic sort of N = G*E pairs held by a group of G threads (G = 32: one warp; G = kT: the
+// CTA), element j of thread t = index G*j + t.  Exchanges at stride >= G stay in the thread,
+// 32 <= stride < G go through shared memory (sbk / sbi, G*E pairs), stride < 32 by shuffles.
+// Stage loops are not unrolled (instruction-cache footprint).
+template <int E, int G>
+__device__ __forceinline__ void group_sort(uint64_t (&x)[E], int32_t (&y)[E], uint64_t *sbk, int32_t *sbi) {
+  const int t = G == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  constexpr unsigned N = (unsigned)G * E;
+#pragma unroll 1
+  for (unsigned s2 = 2; s2 <= N; s2 <<= 1) {
+#pragma unroll 1
+    for (unsigned st = s2 >> 1; st > 0; st >>= 1) {
+      if (st >= (unsigned)G) {
+        const unsigned js = st / G;  // 1, 2 or 4 (E <= 8)
+        auto pass = [&](auto jsc) {
+          constexpr int JS = decltype(jsc)::value;
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            if ((j & JS) || (j | JS) >= E) continue;
+            const int k = j | JS;
+            const bool asc = (((unsigned)(G * j + t)) & s2) == 0;
+            if (pair_gt(x[j], y[j], x[k], y[k]) == asc) {
+              const uint64_t tk = x[j]; x[j] = x[k]; x[k] = tk;
+              const int32_t ti = y[j]; y[j] = y[k]; y[k] = ti;
+            }
+          }
+        };
+        if (js == 1) pass(std::integral_constant<int, 1>{});
+        else if (js == 2) pass(std::integral_constant<int, 2>{});
+        else pass(std::integral_constant<int, 4>{});
+      } else if (st >= 32) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) { sbk[G * j + t] = x[j]; sbi[G * j + t] = y[j]; }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const unsigned i = (unsigned)(G * j + t), p = i ^ st;
+          const uint64_t px = sbk[p];
+          const int32_t py = sbi[p];
+          const bool keep_min = ((i & st) == 0) == ((i & s2) == 0);
+          if (pair_gt(x[j], y[j], px, py) == keep_min) { x[j] = px; y[j] = py; }
+        }
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const unsigned i = (unsigned)(G * j + t);
+          const uint64_t px = __shfl_xor_sync(0xffffffffu, x[j], (int)st);
+          const int32_t py = __shfl_xor_sync(0xffffffffu, y[j], (int)st);
+          const bool keep_min = ((i & st) == 0) == ((i & s2) == 0);
+          if (pair_gt(x[j], y[j], px, py) == keep_min) { x[j] = px; y[j] = py; }
+        }
+      }
+    }
+  }
+}
+
+// Sort the bucket [off, off + size) of (sk, si) with a group of G threads and emit its first
+// `take` ids at out[off ...].
+template <int E, int G>
+__device__ __forceinline__ void sort_bucket(const SelArgs &a, const uint64_t *sk, const int32_t *si, unsigned off,
+                                            unsigned size, unsigned take, uint64_t *sbk, int32_t *sbi) {
+  const int t = G == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  uint64_t x[E];
+  int32_t y[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(G * j + t);
+    x[j] = i < size ? __ldcg(sk + off + i) : kInf;
+    y[j] = i < size ? __ldcg(si + off + i) : INT32_MAX;
+  }
+  group_sort<E, G>(x, y, sbk, sbi);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(G * j + t);
+    if (i < take) emit(a, (int64_t)off + i, y[j]);
+  }
+}
+
+__global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_constant__ SelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ __align__(16) unsigned char s_buf[kCap * 12];  // 24 KB: two bin arrays | a sort buffer
+  __shared__ unsigned s_w[kNW];
+  __shared__ unsigned long long s_red[3][kNW];
+  __shared__ Comp s_comp;
+  __shared__ unsigned s_bnd[4];
+  unsigned *s_cnt = reinterpret_cast<unsigned *>(s_buf);  // [kBins] this CTA's counts per bin
+  unsigned *s_off = s_cnt + kBins;                         // [kBins] its reserved offsets / cursors
+  const int C = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  Ctl *ctl = a.ctl;
+  int tp = 0;
+  auto stamp = [&]() {
+    if (c == 0 && tid == 0 && tp < 32) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ctl->t[tp] = t;
+    }
+    ++tp;
+  };
+  stamp();
+  const int64_t n = a.n;
+  const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // even: 16-B aligned slices
+  const int64_t lo = std::min<int64_t>(n, c * per), hi = std::min<int64_t>(n, lo + per);
+  const bool vec = (reinterpret_cast<uintptr_t>(a.keys) & 15) == 0;
+
+  // Walk this CTA's slice of the input keys: f(key, id), 2 x 4 keys in flight per thread.
+  auto for_slice = [&](auto &&f) {
+    if (vec) {
+      const int64_t v0 = lo >> 1, v1 = hi >> 1;  // lo even
+      const uint4 *src = reinterpret_cast<const uint4 *>(a.keys);
+      // 4-deep register pipeline of 16-B loads; the body (f) appears twice in the code
+      auto ld = [&](int64_t i) { return i < v1 ? __ldcg(src + i) : make_uint4(~0u, ~0u, ~0u, ~0u); };
+      uint4 q0 = ld(v0 + tid), q1 = ld(v0 + kT + tid), q2 = ld(v0 + 2 * kT + tid), q3 = ld(v0 + 3 * kT + tid);
+#pragma unroll 1
+      for (int64_t b = v0; b < v1; b += kT) {
+        const uint4 v = q0;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = ld(b + 4 * kT + tid);
+        const int64_t i = b + tid;
+        f(((uint64_t)v.y << 32) | v.x, (int32_t)(2 * i));
+        f(((uint64_t)v.w << 32) | v.z, (int32_t)(2 * i + 1));
+      }
+      if ((hi & 1) && hi > lo) {  // odd tail of the last slice: thread 0 of a full warp pass
+        const uint64_t kk = tid == 0 ? a.keys[hi - 1] : kInf;
+        f(kk, (int32_t)(hi - 1));
+      }
+    } else {
+      for (int64_t b = lo; b < hi; b += kT) {
+        const int64_t i = b + tid;
+        f(i < hi ? a.keys[i] : kInf, (int32_t)i);
+      }
+    }
+  };
+
+  // ---------------- phase 0: which bits vary among the evictable keys, how many ----------------
+  {
+    unsigned long long o = 0, an = 0, cn = 0;
+    for_slice([&](uint64_t key, int32_t) {
+      if (key != kInf) {
+        o |= key;
+        an |= ~key;
+        ++cn;
+      }
+    });
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      o |= __shfl_xor_sync(0xffffffffu, o, s);
+      an |= __shfl_xor_sync(0xffffffffu, an, s);
+      cn += __shfl_xor_sync(0xffffffffu, cn, s);
+    }
+    if (lane == 0) { s_red[0][w] = o; s_red[1][w] = an; s_red[2][w] = cn; }
+    __syncthreads();
+    if (tid == 0) {
+      Part p{0, 0, 0, 0};
+      for (int i = 0; i < kNW; ++i) { p.o |= s_red[0][i]; p.a |= s_red[1][i]; p.c += s_red[2][i]; }
+      a.part[c] = p;
+    }
+    for (int i = c * kT + tid; i < 2 * kBins; i += C * kT) a.hist[i] = 0u;  // digit-0 and -1 counts
+    if (c == 0 && tid < kMaxLevels) {
+      ctl->n_small[tid] = 0u;
+      ctl->n_large[tid] = 0u;
+      ctl->n_big[tid] = 0u;
+    }
+  }
+  stamp();
+  grid.sync();
+  stamp();
+
+  // ---------------- phase 1: composite layout + digit-0 histogram ----------------
+  unsigned long long E;
+  {
+    unsigned long long o = 0, an = 0, cn = 0;
+    if (tid < C) {
+      const Part p = a.part[tid];
+      o = p.o; an = p.a; cn = p.c;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      o |= __shfl_xor_sync(0xffffffffu, o, s);
+      an |= __shfl_xor_sync(0xffffffffu, an, s);
+      cn += __shfl_xor_sync(0xffffffffu, cn, s);
+    }
+    if (lane == 0) { s_red[0][w] = o; s_red[1][w] = an; s_red[2][w] = cn; }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long O = 0, A = 0, N = 0;
+      for (int i = 0; i < kNW; ++i) { O |= s_red[0][i]; A |= s_red[1][i]; N += s_red[2][i]; }
+      const uint64_t V = O & A;  // set in some evictable key and clear in another
+      // runs of set bits of V, most significant first; gaps merged (smallest first) past kMaxRuns
+      int rlo[32], rhi[32], nr = 0;
+      for (uint64_t rem = V; rem;) {
+        const int hb = 63 - __clzll((long long)rem);
+        const uint64_t zeros = hb ? (~rem & ((1ull << hb) - 1ull)) : 0ull;  // clear bits below hb
+        const int lb = zeros ? 64 - __clzll((long long)zeros) : 0;            // run = [lb, hb]
+        rhi[nr] = hb; rlo[nr] = lb; ++nr;
+        rem &= lb ? ((1ull << lb) - 1ull) : 0ull;
+      }
+      while (nr > kMaxRuns) {
+        int best = 0, gap = 1 << 30;
+        for (int i = 0; i + 1 < nr; ++i) {
+          const int g = rlo[i] - rhi[i + 1];
+          if (g < gap) { gap = g; best = i; }
+        }
+        rlo[best] = rlo[best + 1];
+        for (int i = best + 1; i + 1 < nr; ++i) { rlo[i] = rlo[i + 1]; rhi[i] = rhi[i + 1]; }
+        --nr;
+      }
+      Comp cp{};
+      cp.nr = nr;
+      int bits = 0;
+      for (int i = nr - 1; i >= 0; --i) {  // least significant run lands at bit 0
+        const int len = rhi[i] - rlo[i] + 1;
+        cp.mask[i] = (len >= 64 ? ~0ull : ((1ull << len) - 1ull)) << rlo[i];
+        cp.sh[i] = rlo[i] - bits;
+        bits += len;
+      }
+      unsigned long long mall = 0;
+      for (int i = 0; i < nr; ++i) mall |= cp.mask[i];
+      cp.cst = O & ~A & ~mall;
+      int idb = 0;
+      while (idb < 31 && ((int64_t)1 << idb) < n) ++idb;
+      cp.idb = idb;
+      cp.B = bits + idb;
+      cp.nd = cp.B > 0 ? (cp.B + kDig - 1) / kDig : 1;
+      s_comp = cp;
+      s_red[2][0] = N;
+      if (c == 0) *a.d_count = (int64_t)std::min<unsigned long long>(N, (unsigned long long)a.k);
+    }
+    __syncthreads();
+    E = s_red[2][0];
+  }
+  if (E == 0) return;  // uniform: nothing evictable (*d_count = 0)
+  const Comp &cp = s_comp;
+  const CompR cr = comp_regs(cp);
+  {
+    for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;
+    const DigSel ds0 = dig_sel(cp, 0);
+    __syncthreads();
+    stamp();
+    for_slice([&](uint64_t key, int32_t id) { hist_add(s_cnt, key != kInf ? digit(ds0, compress(cr, key), id) : -1); });
+    __syncthreads();
+    stamp();
+    flush_counts(s_cnt, s_off, a.hist);
+  }
+  stamp();
+  grid.sync();
+  stamp();
+
+  // ---------------- rounds: partition the segment holding rank k-1 ----------------
+  const unsigned long long kk = (unsigned long long)a.k;
+  bool full = E <= kk;                 // the whole segment is taken
+  unsigned long long need = full ? E : kk;
+  unsigned out_base = 0;
+  unsigned m_lo = 0, m_cnt = 0;        // rounds >= 1: this CTA's range of the segment in wk/wi
+  unsigned rec_small = 0, rec_large = 0;  // CTA 0: level-0 records appended so far
+  int r = 0;
+  for (;; ++r) {
+    const unsigned *Hr = a.hist + (r % 3) * kBins;
+    {  // zero the digit-(r+2) counts (last read in round r-1)
+      unsigned *Hz = a.hist + ((r + 2) % 3) * kBins;
+      for (int i = c * kT + tid; i < kBins; i += C * kT) Hz[i] = 0u;
+    }
+    unsigned h[4], ex[4];
+    unsigned sum = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      h[u] = __ldcg(Hr + 4 * tid + u);
+      sum += h[u];
+    }
+    unsigned tot;
+    unsigned run = block_scan(sum, s_w, tot);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { ex[u] = run; run += h[u]; }
+    if (!full) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if ((unsigned long long)ex[u] < need && need <= (unsigned long long)ex[u] + h[u]) {
+          s_bnd[0] = 4 * tid + u;
+          s_bnd[1] = ex[u];
+          s_bnd[2] = h[u];
+        }
+    }
+    __syncthreads();
+    // bin categories: [0, sure_end) taken; bin b: finish-sort (fin) or next segment (nxt)
+    int b = kBins, sure_end = kBins;
+    bool fin = false, nxt = false;
+    unsigned long long need_b = 0;
+    unsigned less_b = 0, h_b = 0;
+    if (!full) {
+      b = (int)s_bnd[0];
+      less_b = s_bnd[1];
+      h_b = s_bnd[2];
+      need_b = need - less_b;
+      if (need_b == h_b) sure_end = b + 1;
+      else {
+        sure_end = b;
+        if (h_b <= (unsigned)kCap) fin = true;
+        else nxt = true;
+      }
+    }
+    const unsigned m_lo_next = nxt ? s_off[b] : 0u, m_cnt_next = nxt ? s_cnt[b] : 0u;
+    __syncthreads();
+    // absolute destinations: taken / finished bins -> output-aligned staging (bit 31: a
+    // singleton bin, emitted directly); the next segment -> wk/wi from 0
+    unsigned nrec = 0;  // this thread's level-0 bucket records: small count | large count << 16
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int d = 4 * tid + u;
+      const bool tk = d < sure_end || (fin && d == b);
+      if (tk) s_off[d] += (out_base + ex[u]) | (h[u] == 1u && d < sure_end ? 0x80000000u : 0u);
+      if (tk && h[u] >= 2u) nrec += h[u] <= (unsigned)kWarpMax ? 1u : 0x10000u;
+    }
+    if (c == 0) {  // CTA 0 alone appends the rounds' records: running totals, no atomics
+      unsigned tot_rec;
+      unsigned at = block_scan(nrec, s_w, tot_rec);
+      unsigned at_s = rec_small + (at & 0xFFFFu), at_l = rec_large + (at >> 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 4 * tid + u;
+        if ((d < sure_end || (fin && d == b)) && h[u] >= 2u) {
+          const unsigned take = d < sure_end ? h[u] : (unsigned)need_b;
+          const uint4 rec = make_uint4(out_base + ex[u], h[u], take, (unsigned)(r + 1));
+          if (h[u] <= (unsigned)kWarpMax) a.rs[0][at_s++] = rec;
+          else {
+            a.rl[0][at_l++] = rec;
+            if (h[u] > (unsigned)kCap) atomicAdd(&ctl->n_big[0], 1u);
+          }
+        }
+      }
+      rec_small += tot_rec & 0xFFFFu;
+      rec_large += tot_rec >> 16;
+      if (tid == 0) {
+        ctl->n_small[0] = rec_small;
+        ctl->n_large[0] = rec_large;
+      }
+    }
+    if (nxt)
+      for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;  // digit-(r+1) counts of the next segment
+    __syncthreads();
+
+    stamp();
+    const int wsrc = r & 1, wdst = (r + 1) & 1;
+    const DigSel dsr = dig_sel(cp, r), dsn = dig_sel(cp, r + 1);
+    auto place = [&](uint64_t key, int32_t id, bool valid) {  // key: compressed
+      int d = valid ? digit(dsr, key, id) : -1;
+      const bool taken = d >= 0 && (d < sure_end || (fin && d == b));
+      const bool seg = nxt && d == b;
+      if (!taken && !seg) d = -1;
+      const unsigned pos = bin_claim(s_off, d);
+      if (taken) {
+        if (pos & 0x80000000u) {
+          emit(a, pos & 0x7FFFFFFFu, id);
+        } else {
+          a.sk[0][pos] = key;
+          a.si[0][pos] = id;
+        }
+      } else if (seg) {
+        a.wk[wdst][pos] = key;
+        a.wi[wdst][pos] = id;
+      }
+      hist_add(s_cnt, seg ? digit(dsn, key, id) : -1);
+    };
+    if (r == 0) {
+      // keys above bin b are dropped before compressing: digit > b <=> key >= t_hi (compress is
+      // an order isomorphism on keys that agree outside the runs; t_hi = the smallest such key
+      // whose compressed value has digit b + 1), when digit 0 lies within the key bits
+      uint64_t t_hi = kInf;
+      if (!full && dsr.lo >= cp.idb) {
+        const int sh = dsr.lo - cp.idb, kb = cp.B - cp.idb;  // compressed key bits
+        const uint64_t x = (uint64_t)(b + 1) << sh;
+        if (sh + dsr.w < kb || (kb < 64 && x < (1ull << kb))) {
+          uint64_t t = cp.cst;
+          for (int i = 0; i < cp.nr; ++i) t |= (x << cp.sh[i]) & cp.mask[i];
+          t_hi = t;
+        }
+      }
+      for_slice([&](uint64_t key, int32_t id) {
+        const bool v = key < t_hi;  // also excludes kInf
+        place(v ? compress(cr, key) : 0ull, id, v);
+      });
+    } else {
+      const uint64_t *xk = a.wk[wsrc];
+      const int32_t *xi = a.wi[wsrc];
+      for (unsigned base = 0; base < m_cnt; base += 2 * kT) {
+        const unsigned i0 = base + tid, i1 = base + kT + tid;
+        const bool v0 = i0 < m_cnt, v1 = i1 < m_cnt;
+        const uint64_t k0 = v0 ? __ldcg(xk + m_lo + i0) : kInf, k1 = v1 ? __ldcg(xk + m_lo + i1) : kInf;
+        const int32_t d0 = v0 ? __ldcg(xi + m_lo + i0) : 0, d1 = v1 ? __ldcg(xi + m_lo + i1) : 0;
+        place(k0, d0, v0);
+        place(k1, d1, v1);
+      }
+    }
+    stamp();
+    if (nxt) {  // reserve this CTA's ranges in the next segment's digit bins
+      __syncthreads();
+      unsigned *Hn = a.hist + ((r + 1) % 3) * kBins;
+      flush_counts(s_cnt, s_off, Hn);
+      need = need_b;
+      out_base += less_b;
+      m_lo = m_lo_next;
+      m_cnt = m_cnt_next;
+    }
+    stamp();
+    grid.sync();
+    stamp();
+    if (!nxt) break;
+  }
+  if (c == 0 && tid == 0) ctl->rounds = (unsigned)(r + 1);
+
+  // ---------------- buckets: sort every taken bin of >= 2 pairs ----------------
+  uint64_t *sbk = reinterpret_cast<uint64_t *>(s_buf);
+  int32_t *sbi = reinterpret_cast<int32_t *>(s_buf + kCap * 8);
+  for (int lv = 0; lv < kMaxLevels; ++lv) {
+    const int L = lv & 1;
+    const unsigned nl = __ldcg(&ctl->n_large[lv]), ns = __ldcg(&ctl->n_small[lv]);
+    const bool more = __ldcg(&ctl->n_big[lv]) != 0u;
+    for (unsigned ri = c; ri < nl; ri += C) {
+      const uint4 rec = __ldcg(a.rl[L] + ri);
+      const unsigned off = rec.x, size = rec.y, take = rec.z, dg = rec.w & 0xFF, src = rec.w >> 8;
+      const uint64_t *xk = a.sk[src];
+      const int32_t *xi = a.si[src];
+      if (size <= (unsigned)kCap) {  // the CTA: registers + shared-memory exchanges
+        if (size <= (unsigned)kT) sort_bucket<1, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        else if (size <= 2u * kT) sort_bucket<2, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        else sort_bucket<4, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        __syncthreads();
+      } else {  // partition by the next digit into the other staging buffer -> next level
+        uint64_t *yk = a.sk[src ^ 1];
+        int32_t *yi = a.si[src ^ 1];
+        const DigSel dsp = dig_sel(cp, dg);
+        for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;
+        __syncthreads();
+        for (unsigned base = 0; base < size; base += kT) {
+          const unsigned i = base + tid;
+          hist_add(s_cnt, i < size ? digit(dsp, __ldcg(xk + off + i), __ldcg(xi + off + i)) : -1);
+        }
+        __syncthreads();
+        unsigned hh[4], sm = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { hh[u] = s_cnt[4 * tid + u]; sm += hh[u]; }
+        unsigned tt;
+        unsigned rr = block_scan(sm, s_w, tt);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int d = 4 * tid + u;
+          s_off[d] = (off + rr) | (hh[u] == 1u ? 0x80000000u : 0u);
+          if (hh[u] >= 2u) {
+            const uint4 r2 = make_uint4(off + rr, hh[u], hh[u], (unsigned)(dg + 1) | ((src ^ 1u) << 8));
+            if (hh[u] <= (unsigned)kWarpMax) {
+              a.rs[L ^ 1][atomicAdd(&ctl->n_small[lv + 1], 1u)] = r2;
+            } else {
+              a.rl[L ^ 1][atomicAdd(&ctl->n_large[lv + 1], 1u)] = r2;
+              if (hh[u] > (unsigned)kCap) atomicAdd(&ctl->n_big[lv + 1], 1u);
+            }
+          }
+          rr += hh[u];
+        }
+        __syncthreads();
+        for (unsigned base = 0; base < size; base += kT) {
+          const unsigned i = base + tid;
+          const bool v = i < size;
+          const uint64_t key = v ? __ldcg(xk + off + i) : 0ull;
+          const int32_t id = v ? __ldcg(xi + off + i) : 0;
+          const unsigned pos = bin_claim(s_off, v ? digit(dsp, key, id) : -1);
+          if (v) {
+            if (pos & 0x80000000u) emit(a, pos & 0x7FFFFFFFu, id);
+            else { yk[pos] = key; yi[pos] = id; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    stamp();
+    for (unsigned ri = (unsigned)(c * kNW + w); ri < ns; ri += (unsigned)(C * kNW)) {
+      const uint4 rec = __ldcg(a.rs[L] + ri);
+      const unsigned off = rec.x, size = rec.y, take = rec.z, src = rec.w >> 8;
+      if (size <= 32) sort_bucket<1, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+      else if (size <= 64) sort_bucket<2, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+      else if (size <= 128) sort_bucket<4, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+      else sort_bucket<8, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+    }
+    stamp();
+    if (!more) {
+      if (c == 0 && tid == 0) ctl->levels = (unsigned)(lv + 1);
+      break;
+    }
+    grid.sync();
+    stamp();
+  }
+}
+
+}  // namespace
+
+size_t evict_select_ws_bytes(int64_t n, int64_t k) { return layout(n, k).total; }
+
+cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids, int64_t *d_count,
+                                uint32_t *free_bits, void *ws, size_t ws_bytes, int ctas, cudaStream_t s) {
+  const Layout L = layout(n, k);
+  if (ws_bytes < L.total) return cudaErrorInvalidValue;
+  uint8_t *p = static_cast<uint8_t *>(ws);
+  SelArgs a{};
+  a.keys = keys;
+  a.n = n;
+  a.k = k;
+  a.out_ids = out_ids;
+  a.d_count = d_count;
+  a.free_bits = free_bits;
+  a.ctl = reinterpret_cast<Ctl *>(p + L.ctl);
+  a.part = reinterpret_cast<Part *>(p + L.part);
+  a.hist = reinterpret_cast<unsigned int *>(p + L.hist);
+  for (int i = 0; i < 2; ++i) {
+    a.wk[i] = reinterpret_cast<uint64_t *>(p + L.wk[i]);
+    a.wi[i] = reinterpret_cast<int32_t *>(p + L.wi[i]);
+    a.sk[i] = reinterpret_cast<uint64_t *>(p + L.sk[i]);
+    a.si[i] = reinterpret_cast<int32_t *>(p + L.si[i]);
+    a.rs[i] = reinterpret_cast<uint4 *>(p + L.rs[i]);
+    a.rl[i] = reinterpret_cast<uint4 *>(p + L.rl[i]);
+  }
+  const int nsm = sm_count();
+  int C = ctas > 0 ? ctas : nsm / 2;
+  C = std::max(1, std::min(C, std::min(kMaxC, 2 * nsm)));
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(evict_select_kernel), 0);
+  if (e != cudaSuccess) return e;
+  void *args[] = {(void *)&a};
+  return cudaLaunchCooperativeKernel((void *)evict_select_kernel, dim3(C), dim3(kT), args, 0, s);
+}
+
+}  // namespace kva

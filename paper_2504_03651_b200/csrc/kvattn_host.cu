@@ -1466,8 +1466,9 @@ extern "C" kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, i
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t *w = static_cast<uint8_t *>(ws);
   int64_t *d_count = reinterpret_cast<int64_t *>(w);
-  CUDA_TRY(launch_evict_select(keys, n, k, out_ids, d_count, w + 256, ws_bytes - 256, s));
-  if (apply) CUDA_TRY(launch_free_ids(pool->desc.free_bits, out_ids, d_count, k, s));
+  static const int ctas = [] { const char *e = getenv("KVA_EVICT_CTAS"); return e ? atoi(e) : 0; }();
+  CUDA_TRY(launch_evict_select(keys, n, k, out_ids, d_count, apply ? pool->desc.free_bits : nullptr, w + 256,
+                               ws_bytes - 256, ctas, s));
   if (!n_selected) return KVA_OK;  // asynchronous mode: count stays on the device
   int64_t cnt = 0;
   CUDA_TRY(cudaMemcpyAsync(&cnt, d_count, sizeof cnt, cudaMemcpyDeviceToHost, s));

@@ -134,14 +134,11 @@ def test_evict_k_larger_than_evictable_and_zero():
     assert n == 0
 
 
-@pytest.mark.parametrize("impl", ["coop", "fast"])
-@pytest.mark.parametrize("case", ["all_equal", "two_values", "short", "k1", "k_all", "clustered", "few_ev"])
-def test_fast_path_adversarial(case, impl, monkeypatch):
-    """n = 2^17 (sample-bucket fast path + exact fallback): heavy ties, fewer evictable blocks
-    than k, k = 1, k = n, keys clustered in one bucket, very few evictable blocks."""
-    import paper_2504_03651_b200 as K
-    monkeypatch.setenv("KVA_EVICT_IMPL", impl)
-    n = 1 << 17
+_ADV = ["all_equal", "two_values", "short", "k1", "k_all", "clustered", "few_ev", "outliers_half",
+        "take_all_skewed", "many_runs", "fin_bucket", "deep_ties"]
+
+
+def _adversarial(case, n):
     rng = np.random.default_rng(sum(map(ord, case)))
     keys = rng.integers(0, 1 << 62, n, dtype=np.uint64)
     k = 5000
@@ -162,8 +159,61 @@ def test_fast_path_adversarial(case, impl, monkeypatch):
         keys[:] = np.uint64(0xFFFFFFFFFFFFFFFF)
         keys[rng.choice(n, 37, replace=False)] = rng.integers(0, 100, 37).astype(np.uint64)
         k = 20
+    elif case == "outliers_half":
+        # almost every key equal, a few outliers far above: the k-th key's bin holds nearly all
+        # keys round after round (segment rounds down to the id bits)
+        keys[:] = np.uint64(5)
+        idx = rng.choice(n, 64, replace=False)
+        keys[idx] = (np.uint64(1) << np.uint64(60)) + rng.integers(0, 1 << 40, 64).astype(np.uint64)
+        k = n // 2
+    elif case == "take_all_skewed":
+        # E <= k and one taken bin far larger than a CTA sort: partitioned bucket levels
+        keys[:] = np.uint64(1)
+        idx = rng.choice(n, n // 10, replace=False)
+        keys[idx] = rng.integers(1 << 50, 1 << 61, len(idx)).astype(np.uint64)
+        k = n + 7
+    elif case == "many_runs":
+        # varying bits in 32 separate runs (more than the kernel keeps apart: gaps merged)
+        keys = (rng.integers(0, 1 << 63, n, dtype=np.uint64) & np.uint64(0x5555555555555555)).astype(np.uint64)
+        k = 3 * n // 4
+    elif case == "fin_bucket":
+        # the k-th key's bin is small: finished by one sort with take < size
+        keys = rng.integers(0, 1 << 20, n, dtype=np.uint64)
+        k = 777
+    elif case == "deep_ties":
+        # 3 distinct keys; k inside the middle one, ties broken by id deep in the id bits
+        keys = rng.choice(np.array([3, 1 << 33, (1 << 33) + 1], np.uint64), n).astype(np.uint64)
+        k = n // 2 + 3
+    return keys, k
+
+
+@pytest.mark.parametrize("case", _ADV)
+def test_select_adversarial(case):
+    """n = 2^17: heavy ties, fewer evictable blocks than k, k = 1, k = n, clustered keys, very
+    few evictable blocks, a boundary bin that stays huge for several rounds, taken bins larger
+    than a CTA sort (partition levels), > 8 runs of varying bits, a finish-sorted boundary bin."""
+    import paper_2504_03651_b200 as K
+    n = 1 << 17
+    keys, k = _adversarial(case, n)
     d = torch.from_numpy(keys.view(np.int64)).cuda()
     ids, nsel = K.evict_select(d, k)
     s, ref = oracle.evict_select(keys, k)
     assert nsel == len(ref)
     assert np.array_equal(ids.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 1000, 4099, 65537])
+def test_select_small_odd_and_unaligned(n):
+    """Odd n (the last slice's odd tail) and a keys pointer that is not 16-B aligned (scalar loads)."""
+    import paper_2504_03651_b200 as K
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 1 << 12, n + 1, dtype=np.uint64)
+    keys[rng.random(n + 1) < 0.1] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    d = torch.from_numpy(keys.view(np.int64)).cuda()
+    for off in (0, 1):
+        kk = keys[off:off + n]
+        for k in {1, max(1, n // 3), n}:
+            ids, nsel = K.evict_select(d[off:off + n], k)
+            s, ref = oracle.evict_select(kk, k)
+            assert nsel == len(ref)
+            assert np.array_equal(ids.cpu().numpy(), ref), (off, k)

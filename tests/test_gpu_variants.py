@@ -62,9 +62,11 @@ def test_decode_impl_parity(env, tmp_path):
     _run(env, "dec_" + "_".join(env.values()), tmp_path)
 
 
-def test_evict_select_coop_only_matches_fast_path(tmp_path):
-    """The cooperative kernel (default) and the sample-bucket path (KVA_EVICT_IMPL=fast) give the
-    oracle's eviction order on the full-size `evict` config and its straddle variant."""
+@pytest.mark.parametrize("ctas", ["1", "7", "148", "296"])
+def test_evict_select_grid_sizes(ctas):
+    """The selection's per-CTA bin reservations and segment ranges give the oracle's eviction
+    order for any cooperative grid size (KVA_EVICT_CTAS), on the full-size `evict` config, its
+    straddle variant and a skewed adversarial case."""
     code = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, %r)
@@ -77,12 +79,17 @@ for straddle in (False, True):
     _, rk = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
     _, rids = oracle.evict_select(rk, ev.k)
     assert np.array_equal(ids.cpu().numpy(), rids), straddle
+rng = np.random.default_rng(5)
+keys = np.full(1 << 16, 5, np.uint64)
+keys[rng.choice(1 << 16, 50, replace=False)] = np.uint64(1 << 61)
+ids, n = K.evict_select(torch.from_numpy(keys.view(np.int64)).cuda(), 40000)
+_, rids = oracle.evict_select(keys, 40000)
+assert np.array_equal(ids.cpu().numpy(), rids)
 print("OK")
 """ % ROOT
-    for env in ({}, {"KVA_EVICT_IMPL": "fast"}):
-        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
-                           text=True, timeout=600)
-        assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, KVA_EVICT_CTAS=ctas),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
 def test_pdl_merge_waits_for_the_tile_kernel(tmp_path):
