@@ -2,7 +2,8 @@
 """bench.py — one iteration of the co-scheduled serving loop's device hot path per step
 (SURVEY §8(a) rows a1-a8): kv_append (+ block allocation) -> hybrid_attention (plan + tile /
 decode split-KV / LSE-merge kernels) -> [G>1: NCCL all-gather of O over NVLink] ->
-evict_keys + evict_select (1M-block pool, top-64k) -> release of this step's blocks.
+kv_manager_step + evict_select (1M-block pool, top-64k) -> kv_truncate (rollback of this step's
+allocations, so that every step is the same iteration).
 
 Contract: `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on rank 0.
 `--impl reference` times the fp64 CPU oracle (the reference arm of this tier) instead.
@@ -179,15 +180,10 @@ def run_ours(args, rank, world, local):
     pool = K.Pool(wl.k_pool, wl.v_pool, K.free_bits_tensor(wl.free_bits, dev))
     batch = K.Batch(wl.batch, dev)
     pristine_host = batch.table_host.copy()
-    # the table entries kv_append fills (the -1 entries of each request's new positions): the
-    # per-step reset and the release touch only these, not the whole host table
-    _ql = np.diff(batch.q_indptr)
-    new_idx = np.array([i * pristine_host.shape[1] + kb
-                        for i in range(len(batch.ctx_len))
-                        for kb in range((int(batch.ctx_len[i]) - int(_ql[i])) // 16, (int(batch.ctx_len[i]) + 15) // 16)
-                        if pristine_host[i, kb] == -1], dtype=np.int64)
-    table_flat = batch.table_host.reshape(-1)
-    assert np.shares_memory(table_flat, batch.table_host)
+    # every step ends by rolling the iteration back (kv_truncate to the pre-append lengths:
+    # the blocks kv_append allocated are released and their table entries reset, host mirror
+    # and device table), so that every step appends and allocates the same way
+    keep_len = (batch.ctx_len - np.diff(batch.q_indptr)).astype(np.int32)
     ws_app = torch.empty(K.kv_append_workspace_size(batch), dtype=torch.uint8, device=dev)
     ws_att = torch.empty(K.hybrid_attention_workspace_size(batch), dtype=torch.uint8, device=dev)
     q, k_new, v_new = wl.q, wl.k_new, wl.v_new
@@ -207,7 +203,9 @@ def run_ours(args, rank, world, local):
                   depth=t(evw.depth, np.int16), k=evw.k, n=len(evw.state))
         chains, mpool = W.make_manager_update(evw, now=1 << 20, seed=1)
         ev["mgr"] = K.ManagerStep(ev["state"], ev["rc"], ev["lat"], ev["depth"])
-        ev["chains"] = K.ManagerStep.chains_csr(chains)
+        # the transition chains are the finished requests' block-table rows: device-resident,
+        # handed to the manager as device arrays (no per-step upload; ids range-checked on the GPU)
+        ev["chains"] = K.ManagerStep.chains_to_device(K.ManagerStep.chains_csr(chains), dev)
         # incremental reference counts: each iteration 1% of the offline pool's requests leave
         # (finished) and as many new requests with the same prompts join (steady state)
         rng_p = np.random.default_rng(11)
@@ -230,9 +228,10 @@ def run_ours(args, rank, world, local):
     # start -> last CTA end of the decode and tile kernels; kva_plan_set_span_buffer) — no stream
     # operation between the kernels, so the programmatic-dependent-launch chain stays intact
     # (CUDA events between them cost ~20 us per step)
-    spans = torch.zeros((args.steps, 4), dtype=torch.int64, device=dev)
+    spans = torch.zeros((args.steps, 6), dtype=torch.int64, device=dev)
     spans[:, 0] = -1
     spans[:, 2] = -1
+    spans[:, 4] = -1
     span_used = []
 
     ev_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("KVA_BENCH_EVICT_PRIO", "0")))
@@ -267,9 +266,6 @@ def run_ours(args, rank, world, local):
                            sync=False)
             ev_join.record(ev_stream)
             n += 3
-        # host table back to pristine (only the entries kv_append fills change); the device table
-        # needs no reset: this step's alloc_write rewrites exactly those entries before any read
-        table_flat[new_idx] = -1
         if ev is not None and gate_attn:  # before the append: the attention pair follows it directly
             stream.wait_event(ev_keys)
         K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
@@ -285,9 +281,7 @@ def run_ours(args, rank, world, local):
             kdist.gather_outputs(out, gbuf)
         if ev is not None:
             stream.wait_event(ev_join)
-        allocated = table_flat[new_idx]
-        allocated = allocated[allocated >= 0]
-        K.kv_release_blocks(pool, allocated, stream=stream)
+        K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
         launches["n"] += n
         plan.close()
@@ -357,9 +351,6 @@ def run_ours(args, rank, world, local):
                            sync=False)
             ev_join.record(ev_stream)
             n += 3
-        # host table back to pristine (only the entries kv_append fills change); the device table
-        # needs no reset: this step's alloc_write rewrites exactly those entries before any read
-        table_flat[new_idx] = -1
         stream.wait_event(ev_in[i % 2])
         if i >= 2:
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done
@@ -382,9 +373,7 @@ def run_ours(args, rank, world, local):
             ev_out[i % 2].record(cs_out)
         if ev is not None:
             stream.wait_event(ev_join)
-        allocated = table_flat[new_idx]
-        allocated = allocated[allocated >= 0]
-        K.kv_release_blocks(pool, allocated, stream=stream)
+        K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
         launches["n"] += n
         plan.close()
@@ -437,11 +426,9 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         step()
     barrier()
-    # the partial reset restores the whole pristine host table (every step starts identically)
-    chk = batch.table_host.copy()
-    assert np.array_equal(batch.table_dev.cpu().numpy(), chk), "device table != host mirror"
-    chk.reshape(-1)[new_idx] = -1
-    assert np.array_equal(chk, pristine_host), "kv_append changed table entries outside new_idx"
+    # the rollback restores the pristine table on both sides (every step starts identically)
+    assert np.array_equal(batch.table_host, pristine_host), "host table != pristine after kv_truncate"
+    assert np.array_equal(batch.table_dev.cpu().numpy(), pristine_host), "device table != pristine"
     plan0 = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
     stats = plan0.stats()
     plan0.close()
@@ -458,6 +445,21 @@ def run_ours(args, rank, world, local):
               if stats["n_decode_items"] > 0 and sp[i, 1] > 0 and sp[i, 1] >= sp[i, 0]]
     tile_ms = [float(sp[i, 3] - sp[i, 2]) * 1e-6 for i in span_used
                if stats["n_tile_items"] > 0 and sp[i, 3] > 0 and sp[i, 3] >= sp[i, 2]]
+    # hybrid_attention alone (tokens/s = query tokens / time of hybrid_attention for
+    # one layer): first attention kernel start -> last end (tile, decode, merge spans) per step;
+    # and the device step period from one step's merge end to the next one's
+    att_ms, period_ms = [], []
+    for i in span_used:
+        st = [sp[i, j] for j in (0, 2, 4) if sp[i, j] != np.uint64(0xFFFFFFFFFFFFFFFF)]
+        en = [sp[i, j] for j in (1, 3, 5) if sp[i, j] > 0]
+        if st and en:
+            att_ms.append(float(max(en) - min(st)) * 1e-6)
+    ends = [int(sp[i, 5]) for i in span_used if sp[i, 5] > 0]
+    period_ms = [(b - a) * 1e-6 for a, b in zip(ends, ends[1:])]
+
+    def pct(v, q):
+        v = sorted(v)
+        return v[min(len(v) - 1, int(q * len(v)))] if v else None
     # standalone decode-kernel timing (same plan, no co-running kernels): context for the
     # in-step roofline above, which is measured while the tile kernel shares the GPU
     dec_alone = None
@@ -522,7 +524,7 @@ def run_ours(args, rank, world, local):
                    "step": "kv_append+hybrid_attention(plan,tile,decode,merge)" +
                            ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)" +
                             (" [eviction pass pipelined: issued after the previous step's selection]" if (ev is not None and evict_pipeline) else "")) +
-                           "+release",
+                           "+kv_truncate(rollback of the step's allocations)",
                    "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
@@ -547,6 +549,16 @@ def run_ours(args, rank, world, local):
                            "traffic": ncu_traffic(args.config, "tile_tc2_kernel"),
                            "flops_per_launch": stats["tile_flops"], "peak_source": tp_src,
                            "decode_hbm": {"achieved_GBps": achieved, "frac": achieved / peak}}
+    if att_ms:
+        res["attention_only"] = {
+            "ms_median": pct(att_ms, 0.5), "ms_p10": pct(att_ms, 0.1), "ms_p90": pct(att_ms, 0.9),
+            "tokens_per_s": tokens / (pct(att_ms, 0.5) * 1e-3),
+            "timing": "per timed step: first attention-kernel CTA start -> last tile/decode/merge CTA end "
+                      "(in-kernel %globaltimer), kv_append / manager / eviction excluded"}
+    if period_ms:
+        res["step_period_ms"] = {"p10": pct(period_ms, 0.1), "median": pct(period_ms, 0.5),
+                                 "p90": pct(period_ms, 0.9),
+                                 "timing": "device time between consecutive steps' last merge CTA end"}
     if dec_alone:
         a = dec_bytes / (dec_alone * 1e-3) / 1e9
         res["config"]["decode_kernel_standalone"] = {"ms": dec_alone, "GBps": a, "frac_of_peak": a / peak,

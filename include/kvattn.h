@@ -91,8 +91,7 @@ kva_status kv_pool_destroy(kva_pool *pool);
 kva_status kv_pool_free_count(const kva_pool *pool, int64_t *n_free);
 /* Re-read free_bits from the device (synchronous) after the caller edited it. */
 kva_status kv_pool_resync(kva_pool *pool);
-/* Make `stream` wait (device-side, no host sync) for the pool's side-stream kv_append writes
- * (see kv_append "Ordering"). */
+/* No-op (every kv_append write is on the caller's stream; see kv_append "Ordering"). */
 kva_status kv_pool_sync(kva_pool *pool, kva_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
@@ -150,13 +149,12 @@ kva_status kva_validate_batch(const kva_batch_desc *desc, int32_t num_blocks, in
  *   k_new, v_new : device bf16 [total_q][num_kv_heads][head_dim]; token stride
  *                  new_stride_tok elements (>= num_kv_heads*head_dim), heads contiguous.
  *   workspace    : device scratch of kv_append_workspace_size() bytes (16-B aligned).
- * Ordering: the table update and the rows of decode-class requests (q_len * Hq/Hkv <= 16,
- *   read by the decode kernel) are written in order on `stream`; the rows of the other
- *   requests (read only by the tensor-core tile kernel) are written on the pool's side stream
- *   so that the decode kernel does not queue behind them.  Every later call taking this pool
- *   (kv_append, hybrid_attention_run with the tile or all phases, kv_release_blocks) orders
- *   itself after those writes; other work on `stream` that reads the pool or reuses
- *   k_new / v_new calls kv_pool_sync(pool, stream) first.
+ * Ordering: everything is enqueued on `stream` in two kernels: (1) the rows of decode-class
+ *   requests (q_len * Hq/Hkv <= 16; their <= 2 blocks resolved on the host) together with the
+ *   new table entries and free bits, (2) the rows of the other requests (read only by the
+ *   tensor-core tile kernel, which hybrid_attention_run launches with programmatic dependent
+ *   launch so that it becomes resident while (2) still writes, and waits for it in-kernel).
+ *   kv_pool_sync is a no-op kept for callers written against an earlier side-stream variant.
  * Errors: KVA_NEEDS_EVICTION (needed > free, *deficit_blocks = needed - free, nothing
  * enqueued); KVA_ERR_CAPACITY (ceil(ctx/16) > num_blocks for some request);
  * KVA_ERR_GROUP (an appended position inside a group prefix); KVA_ERR_INVALID.
@@ -197,11 +195,12 @@ kva_status hybrid_attention_run_phases(const kva_plan *plan, const void *q, int6
 /* Instrumentation: cudaEvent_t handles (or NULL) recorded immediately before/after the tile
  * kernel launch (on the stream it runs on) and the decode kernel launch (on the caller's
  * stream) by every later run of this plan — per-kernel timing inside an overlapped step. */
-/* Instrumentation without stream operations: if dev_span (device, 4 x u64) is set, every later
+/* Instrumentation without stream operations: if dev_span (device, 6 x u64) is set, every later
  * run of this plan records %globaltimer nanoseconds: [0] = min start and [1] = max end over the
- * decode kernel's CTAs, [2] / [3] = the same for the tile kernel (atomicMin / atomicMax: the
- * caller initialises [0], [2] to UINT64_MAX and [1], [3] to 0).  Unlike timing events this does
- * not break the programmatic-dependent-launch chain of the run.  NULL disables it. */
+ * decode kernel's CTAs, [2] / [3] = the same for the tile kernel, [4] / [5] for the merge kernel
+ * (atomicMin / atomicMax: the caller initialises [0], [2], [4] to UINT64_MAX and [1], [3], [5]
+ * to 0).  Unlike timing events this does not break the programmatic-dependent-launch chain of
+ * the run.  NULL disables it. */
 kva_status kva_plan_set_span_buffer(kva_plan *plan, unsigned long long *dev_span);
 kva_status kva_plan_set_timing_events(kva_plan *plan, void *tile_begin, void *tile_end,
                                       void *decode_begin, void *decode_end);
@@ -251,6 +250,18 @@ kva_status hybrid_attention(kva_pool *pool, const kva_batch_desc *desc, const vo
  * victim request").  ids: HOST int32 [n], each allocated (not free) and distinct, else
  * KVA_ERR_INVALID with no change.  Sets the device free bits on `stream` and the mirror. */
 kva_status kv_release_blocks(kva_pool *pool, const int32_t *ids, int64_t n, kva_stream_t stream);
+/* kv_truncate: shorten requests to their first keep_len[i] tokens (recompute-mode preemption
+ * releasing a victim's KV, or the rollback of an iteration's kv_append): the blocks of
+ * row i at block indices [cdiv(keep_len[i], 16), cdiv(ctx_len[i], 16)) that are not -1 are
+ * returned to the free pool (device free bits + host mirror) and those table entries set to -1
+ * in the host mirror AND the device table (one kernel on `stream`, lists as kernel
+ * parameters).  keep_len: HOST int32 [num_reqs]; -1 leaves request i untouched, otherwise
+ * 0 <= keep_len[i] <= ctx_len[i].  Reads only ctx_len, max_blocks, the tables and the group
+ * fields of the descriptor; ctx_len / q_indptr are the caller's to update.  Errors (nothing
+ * changed): KVA_ERR_INVALID for a bad keep_len, an id out of range, already free or listed
+ * twice; KVA_ERR_GROUP if the cut lies inside the request's shared prefix (its blocks belong
+ * to the group). */
+kva_status kv_truncate(kva_pool *pool, kva_batch_desc *desc, const int32_t *keep_len, kva_stream_t stream);
 
 enum { KVA_BLK_FREE = 0, KVA_BLK_RUNNING_ONLINE = 1, KVA_BLK_PINNED = 2,
        KVA_BLK_ACTIVE_OFFLINE = 3, KVA_BLK_FINISHED_ONLINE = 4, KVA_BLK_FINISHED_OFFLINE = 5 };
@@ -304,6 +315,11 @@ typedef struct {
   int64_t pool_len;
   const int32_t *del_ids;       /* device [del_len] (incremental mode only) */
   int64_t del_len;
+  /* 1: chain_indptr / chain_ids / chain_state are DEVICE arrays (e.g. the finished requests'
+   * block-table rows already on the GPU): no upload and no host id check — ids outside
+   * [0, num_blocks) are skipped on the device; n_chain_ids (host) = chain_indptr[n_chains]. */
+  int32_t chains_on_device;
+  int64_t n_chain_ids;
 } kva_manager_update;
 kva_status kv_manager_step_workspace_size(const kva_block_meta *meta, const kva_manager_update *u,
                                           size_t *bytes);

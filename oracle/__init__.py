@@ -268,6 +268,37 @@ def release_blocks(free_bits, num_blocks: int, ids):
     return s, fb
 
 
+def truncate(b: dict, free_bits, keep_len):
+    """Shorten request i to its first keep_len[i] tokens ("preempts and release the KV
+    cache of the victim request"; -1 = untouched): the non-(-1) table entries of row i at block
+    indices [ceil(keep/16), ceil(ctx/16)) are released (release_blocks: allocated, each once)
+    and set to -1.  A cut inside the request's group prefix is GROUP; a keep_len outside
+    [0, ctx] is INVALID.  Works on copies; returns (status, free_bits', block_table')."""
+    bt = np.array(b["block_table"], np.int32, copy=True)
+    fb = _c(free_bits, np.uint32).copy()
+    gof, gpb = b.get("group_of"), b.get("group_prefix_blocks")
+    ids, ent = [], []
+    for i, keep in enumerate(np.asarray(keep_len, np.int64)):
+        if keep == -1:
+            continue
+        ctx = int(b["ctx_len"][i])
+        if keep < 0 or keep > ctx:
+            return INVALID, fb, bt
+        k0 = -(-int(keep) // 16)
+        if gof is not None and gof[i] >= 0 and k0 < int(gpb[gof[i]]):
+            return GROUP, fb, bt
+        for k in range(k0, -(-ctx // 16)):
+            if bt[i, k] != -1:
+                ids.append(int(bt[i, k]))
+                ent.append((i, k))
+    s, fb2 = release_blocks(fb, b["num_blocks"], np.array(ids, np.int32))
+    if s != OK:
+        return s, fb, bt
+    for i, k in ent:
+        bt[i, k] = -1
+    return OK, fb2, bt
+
+
 def validate(b: dict):
     lib = _load()
     R, qi, ctx, bt, gof, gpb = _batch_args(b)

@@ -74,9 +74,11 @@ struct ReqList {
   R req[kInlineReqs];
 };
 
-// Per-request append info (kv_append).
+// Per-request append info (kv_append).  blk[0..1]: the ids of blocks pos0/16 and pos0/16 + 1
+// when the host resolved them (decode-class requests: <= 16 new tokens, so <= 2 blocks; the
+// kernel then reads no table entry and needs no ordering behind the table update), else -1.
 struct AppendReq {
-  int32_t q_row0, q_len, pos0, table_row;
+  int32_t q_row0, q_len, pos0, table_row, blk[2];
 };
 
 struct AttnParams {
@@ -99,7 +101,8 @@ struct AttnParams {
   const int32_t *row_list;
   unsigned long long *dbg;  // optional timestamps (diagnostics; KVA_DEBUG_TS), nullable
   // optional kernel spans (%globaltimer ns): [0] = min decode CTA start, [1] = max decode CTA
-  // end, [2] / [3] = the same for the tile kernel (kva_plan_set_span_buffer), nullable
+  // end, [2] / [3] = the same for the tile kernel, [4] / [5] for the merge kernel
+  // (kva_plan_set_span_buffer), nullable
   unsigned long long *span;
   int32_t debug_flags;      // diagnostics only (KVA_DEBUG_FLAGS): 1 = tile softmax skipped
 };
@@ -135,12 +138,15 @@ struct AllocList {
   int32_t tbl[kInlineAlloc];
   int32_t ids[kInlineAlloc];
 };
-cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const AllocList &al, cudaStream_t s);
+// Append of a request list; al != nullptr: the same launch also publishes the allocation (table
+// entries + free bits) — only for a list whose requests all carry resolved blk ids (it reads
+// no table entry), so no ordering between the two parts is needed.
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
-                          const int32_t *block_table, int32_t max_blocks,
+                          int32_t *block_table, int32_t max_blocks,
                           const ReqList<AppendReq> &reqs, int32_t total_new_tok, cudaStream_t s,
-                          bool early_trigger = false);
+                          bool early_trigger = false, const AllocList *al = nullptr,
+                          uint32_t *free_bits = nullptr);
 cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const uint32_t *lat,
                               const uint16_t *depth, int64_t n, uint64_t *keys, cudaStream_t s);
 cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth,
@@ -155,7 +161,9 @@ size_t evict_select_ws_bytes(int64_t n, int64_t k);
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
                                 int ctas, cudaStream_t s);
-constexpr int kReleaseBatch = 4000;  // ids per release launch (kernel-parameter payload)
-cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s);
+constexpr int kReleaseBatch = 3800;  // ids (+ table entries) per release launch (kernel parameter)
+// free bits of ids_host[0, n) set; tbl_host != nullptr: table[tbl_host[i]] = -1 as well
+cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,
+                               const int32_t *tbl_host = nullptr, int32_t *table = nullptr);
 
 }  // namespace kva

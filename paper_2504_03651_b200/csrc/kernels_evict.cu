@@ -6,6 +6,8 @@
 // order-preserving u64 codes (readings #18-#20); equal keys are broken by block id.
 //
 // The selection itself (evict_select) is in kernels_select.cu.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -13,6 +15,8 @@
 #include <string>
 
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace kva {
 
@@ -48,88 +52,121 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 }
 
 // ---------------------------------------------------------------------------------------
-// KV-manager step.  Transitions arrive as the caller's raw chains (host
-// validated, uploaded unchanged); "last chain wins" is resolved on the device: every listed
-// block's winner slot is reset, then takes the max element index listing it (atomicMax), and
-// only that element applies its chain's state.  Then the reference counts (recount: zeroed
-// by the host + atomicAdd; incremental: atomicAdd / atomicSub), then keys + active count.
-__global__ void manager_win_init_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win,
-                                        unsigned long long *__restrict__ n_active) {
-  if (n_active && blockIdx.x == 0 && threadIdx.x == 0) *n_active = 0ull;  // counted by the keys kernel
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr; e += (int64_t)gridDim.x * blockDim.x)
-    win[tr_ids[e]] = -1;
-}
-__global__ void manager_win_max_kernel(const int32_t *__restrict__ tr_ids, int64_t n_tr, int32_t *__restrict__ win) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr; e += (int64_t)gridDim.x * blockDim.x)
-    atomicMax(&win[tr_ids[e]], (int32_t)e);
+// KV-manager step: one cooperative kernel, phases separated by grid barriers.
+// Transitions arrive as the caller's raw chains (host validated, uploaded unchanged); "last
+// chain wins" is resolved on the device: every listed block's winner slot is reset, then
+// takes the max element index listing it (atomicMax), and only that element applies its
+// chain's state.  Then the reference counts (recount: zeroed + atomicAdd; incremental:
+// atomicAdd / atomicSub), then keys + active count.
+//   phase 0  rc = 0 (recount), win[id] = -1 for listed ids, *n_active = 0
+//   phase 1  win[id] = max element index listing id
+//   phase 2  winners apply (state, lat = now); rc += pool chains, -= deleted chains
+//   phase 3  keys (evict_keys' encoding) + active count
+struct MgrArgs {
+  uint8_t *state;
+  uint32_t *rc, *lat;
+  const uint16_t *depth;
+  int64_t n;
+  uint32_t now;
+  const int32_t *tr_ids;
+  int64_t n_tr;
+  const int32_t *tr_indptr;
+  const uint8_t *tr_state;
+  int32_t n_chains;
+  int32_t *win;
+  int32_t recount;
+  const int32_t *pool_ids;
+  int64_t pool_len;
+  const int32_t *del_ids;
+  int64_t del_len;
+  uint64_t *keys;
+  unsigned long long *n_active;
+};
+
+__device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t la, uint32_t dp, unsigned &act) {
+  act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
+  if (s == 0 || s == 1 || s == 2 || s > 5) return kInf;
+  uint64_t code;
+  if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
+  else code = (s == 4) ? 1ull : 0ull;
+  return (code << 48) | ((uint64_t)la << 16) | (0xFFFFull - (uint64_t)dp);
 }
 
-__global__ void manager_apply_kernel(uint8_t *__restrict__ state, uint32_t *__restrict__ rc,
-                                     uint32_t *__restrict__ lat, int64_t n, uint32_t now,
-                                     const int32_t *__restrict__ tr_ids, int64_t n_tr,
-                                     const int32_t *__restrict__ tr_indptr, const uint8_t *__restrict__ tr_state,
-                                     int32_t n_chains, const int32_t *__restrict__ win,
-                                     const int32_t *__restrict__ pool_ids, int64_t pool_len,
-                                     const int32_t *__restrict__ del_ids, int64_t del_len) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tr + pool_len + del_len;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < n_tr) {
-      const int32_t id = tr_ids[e];  // validated on the host
-      if (win[id] != (int32_t)e) continue;  // a later chain lists this block too
-      int lo = 0, hi = n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
+__global__ void __launch_bounds__(256) manager_kernel(const __grid_constant__ MgrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  // phase 0
+  if (a.recount) {
+    const int64_t n4 = (reinterpret_cast<uintptr_t>(a.rc) & 15) ? 0 : a.n / 4;
+    for (int64_t q = t0; q < n4; q += nt) reinterpret_cast<uint4 *>(a.rc)[q] = make_uint4(0, 0, 0, 0);
+    for (int64_t b = 4 * n4 + t0; b < a.n; b += nt) a.rc[b] = 0u;
+  }
+  // transition ids outside [0, n) (possible only for device-resident chains, which the host
+  // does not check) are skipped in every phase
+  for (int64_t e = t0; e < a.n_tr; e += nt) {
+    const int32_t id = a.tr_ids[e];
+    if ((uint32_t)id < (uint64_t)a.n) a.win[id] = -1;
+  }
+  if (a.n_active && t0 == 0) *a.n_active = 0ull;
+  grid.sync();  // (also orders the n_active reset before phase 3's adds)
+  // phase 1
+  if (a.n_tr > 0) {
+    for (int64_t e = t0; e < a.n_tr; e += nt) {
+      const int32_t id = a.tr_ids[e];
+      if ((uint32_t)id < (uint64_t)a.n) atomicMax(&a.win[id], (int32_t)e);
+    }
+    grid.sync();
+  }
+  // phase 2
+  const int64_t m = a.n_tr + a.pool_len + a.del_len;
+  for (int64_t e = t0; e < m; e += nt) {
+    if (e < a.n_tr) {
+      const int32_t id = a.tr_ids[e];
+      if ((uint32_t)id >= (uint64_t)a.n || a.win[id] != (int32_t)e) continue;  // out of range / a later chain lists it
+      int lo = 0, hi = a.n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (tr_indptr[mid] <= e) lo = mid;
+        if (a.tr_indptr[mid] <= e) lo = mid;
         else hi = mid - 1;
       }
-      state[id] = tr_state[lo];
-      lat[id] = now;
-    } else if (e < n_tr + pool_len) {
-      const int32_t id = pool_ids[e - n_tr];
-      if ((uint64_t)id < (uint64_t)n) atomicAdd(&rc[id], 1u);
+      a.state[id] = a.tr_state[lo];
+      a.lat[id] = a.now;
+    } else if (e < a.n_tr + a.pool_len) {
+      const int32_t id = a.pool_ids[e - a.n_tr];
+      if ((uint64_t)id < (uint64_t)a.n) atomicAdd(&a.rc[id], 1u);
     } else {
-      const int32_t id = del_ids[e - n_tr - pool_len];
-      if ((uint64_t)id < (uint64_t)n) atomicSub(&rc[id], 1u);
+      const int32_t id = a.del_ids[e - a.n_tr - a.pool_len];
+      if ((uint64_t)id < (uint64_t)a.n) atomicSub(&a.rc[id], 1u);
     }
   }
-}
-
-__global__ void manager_keys_kernel(const uint8_t *__restrict__ state, const uint32_t *__restrict__ rc,
-                                    const uint32_t *__restrict__ lat, const uint16_t *__restrict__ depth,
-                                    int64_t n, uint64_t *__restrict__ keys,
-                                    unsigned long long *__restrict__ n_active) {
-  unsigned int act = 0;
-  auto one = [&](uint32_t s, uint32_t r, uint32_t la, uint32_t dp) -> uint64_t {
-    act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
-    if (s == 0 || s == 1 || s == 2 || s > 5) return kInf;
-    uint64_t code;
-    if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
-    else code = (s == 4) ? 1ull : 0ull;
-    return (code << 48) | ((uint64_t)la << 16) | (0xFFFFull - (uint64_t)dp);
-  };
-  // 4 blocks per thread with vector loads/stores when the arrays allow it (torch allocations
-  // are 256-B aligned), scalar tail
+  if (m > 0) grid.sync();
+  // phase 3: 4 blocks per thread with vector loads/stores when the arrays allow it (torch
+  // allocations are 256-B aligned), scalar tail
+  unsigned act = 0;
+  const uint8_t *state = a.state;
+  const uint32_t *rc = a.rc, *lat = a.lat;
+  const uint16_t *depth = a.depth;
+  uint64_t *keys = a.keys;
   const bool vec = ((reinterpret_cast<uintptr_t>(state) | reinterpret_cast<uintptr_t>(rc) |
                      reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(keys) |
                      (depth ? reinterpret_cast<uintptr_t>(depth) : 0)) & 15) == 0;
-  const int64_t n4 = vec ? n / 4 : 0;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s4 = reinterpret_cast<const uint32_t *>(state)[q];
-    const uint4 r4 = reinterpret_cast<const uint4 *>(rc)[q];
-    const uint4 l4 = reinterpret_cast<const uint4 *>(lat)[q];
+  const int64_t n4 = vec ? a.n / 4 : 0;
+  for (int64_t q = t0; q < n4; q += nt) {
+    const uint32_t s4 = __ldcg(reinterpret_cast<const uint32_t *>(state) + q);
+    const uint4 r4 = __ldcg(reinterpret_cast<const uint4 *>(rc) + q);
+    const uint4 l4 = __ldcg(reinterpret_cast<const uint4 *>(lat) + q);
     uint2 d4 = make_uint2(0u, 0u);
     if (depth) d4 = reinterpret_cast<const uint2 *>(depth)[q];
-    const uint64_t k0 = one(s4 & 0xFF, r4.x, l4.x, d4.x & 0xFFFF);
-    const uint64_t k1 = one((s4 >> 8) & 0xFF, r4.y, l4.y, d4.x >> 16);
-    const uint64_t k2 = one((s4 >> 16) & 0xFF, r4.z, l4.z, d4.y & 0xFFFF);
-    const uint64_t k3 = one(s4 >> 24, r4.w, l4.w, d4.y >> 16);
+    const uint64_t k0 = manager_key(s4 & 0xFF, r4.x, l4.x, d4.x & 0xFFFF, act);
+    const uint64_t k1 = manager_key((s4 >> 8) & 0xFF, r4.y, l4.y, d4.x >> 16, act);
+    const uint64_t k2 = manager_key((s4 >> 16) & 0xFF, r4.z, l4.z, d4.y & 0xFFFF, act);
+    const uint64_t k3 = manager_key(s4 >> 24, r4.w, l4.w, d4.y >> 16, act);
     reinterpret_cast<ulonglong2 *>(keys)[2 * q] = make_ulonglong2(k0, k1);
     reinterpret_cast<ulonglong2 *>(keys)[2 * q + 1] = make_ulonglong2(k2, k3);
   }
-  for (int64_t b = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
-       b += (int64_t)gridDim.x * blockDim.x)
-    keys[b] = one(state[b], rc[b], lat[b], depth ? depth[b] : 0u);
-  if (n_active) {  // one atomic per CTA (a per-warp atomic on one address serialises in L2)
+  for (int64_t b = 4 * n4 + t0; b < a.n; b += nt)
+    keys[b] = manager_key(__ldcg(state + b), __ldcg(rc + b), __ldcg(lat + b), depth ? depth[b] : 0u, act);
+  if (a.n_active) {  // one atomic per CTA (a per-warp atomic on one address serialises in L2)
     __shared__ unsigned int s_act;
     if (threadIdx.x == 0) s_act = 0u;
     __syncthreads();
@@ -137,7 +174,7 @@ __global__ void manager_keys_kernel(const uint8_t *__restrict__ state, const uin
     for (int o = 16; o > 0; o >>= 1) act += __shfl_xor_sync(0xffffffffu, act, o);
     if ((threadIdx.x & 31) == 0 && act) atomicAdd(&s_act, act);
     __syncthreads();
-    if (threadIdx.x == 0 && s_act) atomicAdd(n_active, (unsigned long long)s_act);
+    if (threadIdx.x == 0 && s_act) atomicAdd(a.n_active, (unsigned long long)s_act);
   }
 }
 
@@ -147,48 +184,51 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 int32_t *win, bool recount, const int32_t *pool_ids, int64_t pool_len,
                                 const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
                                 cudaStream_t s) {
-  cudaError_t e = cudaSuccess;
-  if (recount) e = cudaMemsetAsync(rc, 0, (size_t)n * sizeof(uint32_t), s);
-  // the active count is zeroed by the winner-init kernel when there are transitions
-  if (e == cudaSuccess && n_active && n_tr <= 0) e = cudaMemsetAsync(n_active, 0, sizeof(int64_t), s);
-  if (e != cudaSuccess) return e;
-  auto grid_for = [](int64_t m) { return (int)std::min<int64_t>((m + 255) / 256, 148 * 8); };
-  if (n_tr > 0) {
-    manager_win_init_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win,
-                                                           reinterpret_cast<unsigned long long *>(n_active));
-    manager_win_max_kernel<<<grid_for(n_tr), 256, 0, s>>>(tr_ids, n_tr, win);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  const int64_t m = n_tr + pool_len + del_len;
-  if (m > 0) {
-    manager_apply_kernel<<<grid_for(m), 256, 0, s>>>(state, rc, lat, n, now, tr_ids, n_tr, tr_indptr, tr_state,
-                                                     n_chains, win, pool_ids, pool_len, del_ids, del_len);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  if (n > 0) {
-    manager_keys_kernel<<<grid_for(n), 256, 0, s>>>(state, rc, lat, depth, n, keys,
-                                                    reinterpret_cast<unsigned long long *>(n_active));
-    e = cudaGetLastError();
-  }
-  return e;
+  MgrArgs a{state, rc, lat, depth, n, now, tr_ids, n_tr, tr_indptr, tr_state, n_chains, win,
+            recount ? 1 : 0, pool_ids, pool_len, del_ids, del_len, keys,
+            reinterpret_cast<unsigned long long *>(n_active)};
+  if (n <= 0 && n_active == nullptr) return cudaSuccess;
+  // two 256-thread CTAs per SM (co-resident on an idle GPU: cooperative launch); every phase is
+  // a grid-stride pass over <= 2^20 elements (a few per thread)
+  const int grid = std::max(1, std::min<int>(2 * sm_count(), (int)((std::max<int64_t>(n, n_tr + pool_len + del_len) + 255) / 256)));
+  void *args[] = {(void *)&a};
+  return cudaLaunchCooperativeKernel((void *)manager_kernel, dim3(grid), dim3(256), args, 0, s);
 }
 
-struct ReleaseIds {
+// Release: set the free bits of the listed blocks and (truncate) write -1 into the listed
+// block-table entries.  The lists travel as a kernel parameter (no upload); capacity templated
+// so that a short list does not pay for a 30 KB parameter block.
+template <int CAP>
+struct ReleaseList {
   int32_t n;
-  int32_t ids[kReleaseBatch];
+  int32_t *table;  // nullable: entries tbl[0, n) are set to -1
+  int32_t ids[CAP];
+  int32_t tbl[CAP];
 };
-__global__ void release_ids_kernel(uint32_t *free_bits, const __grid_constant__ ReleaseIds r) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x)
+template <int CAP>
+__global__ void release_ids_kernel(uint32_t *free_bits, const __grid_constant__ ReleaseList<CAP> r) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     atomicOr(free_bits + (r.ids[i] >> 5), 1u << (r.ids[i] & 31));
+    if (r.table) r.table[r.tbl[i]] = -1;
+  }
+}
+template <int CAP>
+static cudaError_t release_launch(uint32_t *free_bits, const int32_t *ids, const int32_t *tbl, int32_t *table, int n,
+                                  cudaStream_t s) {
+  ReleaseList<CAP> r;
+  r.n = n;
+  r.table = tbl ? table : nullptr;
+  std::memcpy(r.ids, ids, sizeof(int32_t) * n);
+  if (tbl) std::memcpy(r.tbl, tbl, sizeof(int32_t) * n);
+  release_ids_kernel<CAP><<<(n + 255) / 256, 256, 0, s>>>(free_bits, r);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s) {
+cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,
+                               const int32_t *tbl_host, int32_t *table) {
   if (n <= 0) return cudaSuccess;
-  ReleaseIds r;
-  r.n = n;
-  std::memcpy(r.ids, ids_host, sizeof(int32_t) * n);
-  release_ids_kernel<<<(n + 255) / 256, 256, 0, s>>>(free_bits, r);
-  return cudaGetLastError();
+  if (n <= 256) return release_launch<256>(free_bits, ids_host, tbl_host, table, n, s);
+  return release_launch<kReleaseBatch>(free_bits, ids_host, tbl_host, table, n, s);
 }
 
 }  // namespace kva

@@ -22,6 +22,11 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
                                                     int n_units) {
   constexpr int V = D / 32;  // 4 (d=128) or 2 (d=64)
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (p.span && threadIdx.x == 0) {  // instrumentation: CTA start
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    atomicMin(&p.span[4], t0);
+  }
   if (w >= n_units) return;
   const int m = w / p.Hkv, h = w - m * p.Hkv;  // m = (request, row)
   const MergeReq *reqs = RL.ptr ? RL.ptr : RL.req;
@@ -32,7 +37,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
     if (pre[mid] <= m) lo = mid;
     else hi = mid - 1;
   }
-  const MergeReq mq = reqs[lo];
+  const MergeReq &mq = reqs[lo];  // (a reference: dynamic casc_slot[i] indexing without a stack copy)
   const int r = m - pre[lo];
   const int nc = mq.n_casc;
   const int n = nc + mq.nsplit;
@@ -40,26 +45,46 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
   auto slot_of = [&](int i) {
     return i < nc ? mq.casc_slot[i] + h * mq.casc_hstride[i] + r : split0 + (i - nc) * mq.rows;
   };
+  // every partial's lse and O vector requested before any is used (one L2 round trip each for
+  // up to kBatch partials): lane i < n loads lse_i, the warp max + weights by shuffles
+  constexpr int kBatch = 8;
   float L = -CUDART_INF_F;
-  for (int i = lane; i < n; i += 32) L = fmaxf(L, p.part_lse[slot_of(i)]);
+  for (int i = lane; i < n; i += 32) L = fmaxf(L, __ldg(p.part_lse + slot_of(i)));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xffffffffu, L, o));
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   float sum = 0.f;
-  for (int i = 0; i < n; ++i) {
-    const int sl = slot_of(i);
-    const float lj = __ldg(p.part_lse + sl);
-    const float wgt = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
-    sum += wgt;
-    const float *src = p.part_o + (int64_t)sl * D + lane * V;
-    if constexpr (V == 4) {
-      const float4 x = __ldg(reinterpret_cast<const float4 *>(src));
-      acc[0] += wgt * x.x; acc[1] += wgt * x.y; acc[2] += wgt * x.z; acc[3] += wgt * x.w;
-    } else {
-      const float2 x = __ldg(reinterpret_cast<const float2 *>(src));
-      acc[0] += wgt * x.x; acc[1] += wgt * x.y;
+  for (int i0 = 0; i0 < n; i0 += kBatch) {
+    const int nb = min(kBatch, n - i0);
+    float my_w = 0.f;  // lane j < nb: weight of partial i0 + j
+    if (lane < nb) {
+      const float lj = __ldg(p.part_lse + slot_of(i0 + lane));
+      my_w = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
+    }
+    float xs[kBatch][V];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      if (j < nb) {
+        const float *src = p.part_o + (int64_t)slot_of(i0 + j) * D + lane * V;
+        if constexpr (V == 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4 *>(src));
+          xs[j][0] = x.x; xs[j][1] = x.y; xs[j][2] = x.z; xs[j][3] = x.w;
+        } else {
+          const float2 x = __ldg(reinterpret_cast<const float2 *>(src));
+          xs[j][0] = x.x; xs[j][1] = x.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const float wgt = __shfl_sync(0xffffffffu, my_w, j);
+      if (j < nb) {
+        sum += wgt;
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] += wgt * xs[j][v];
+      }
     }
   }
   const float inv = 1.f / sum;
@@ -80,6 +105,11 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
       *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
   }
   if (p.lse && lane == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
+  if (p.span && lane == 0) {  // instrumentation: warp end
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicMax(&p.span[5], t1);
+  }
 }
 
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n_units, cudaStream_t s) {
@@ -93,35 +123,36 @@ cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n
 }
 
 // ---------------------------------------------------------------------------------------
-// a2: KV append.  (1) alloc_write publishes the ids the host allocator chose (smallest free
-// first, reading #13) in the device block table and clears their free bits; (2) the scatter
-// copies every (new token, local kv-head) row of a request list (exclusive token prefix
-// tok_pre) to slot (table[i][t/16], t % 16).
+// a2: KV append.  The scatter copies every (new token, local kv-head) row of a request list
+// (exclusive token prefix tok_pre) to slot (block(t/16), t % 16), the block id taken from the
+// request's host-resolved ids (decode-class) or the block table.  The launch of the
+// decode-class list also publishes the ids the host allocator chose (smallest free first,
+// reading #13): table entries written and free bits cleared by its trailing CTAs.
 // ---------------------------------------------------------------------------------------
-__global__ void alloc_write_kernel(int32_t *__restrict__ block_table, uint32_t *__restrict__ free_bits,
-                                   const __grid_constant__ AllocList al) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= al.n) return;
-  const int32_t id = al.ids_ptr ? al.ids_ptr[i] : al.ids[i];
-  block_table[al.tbl_ptr ? al.tbl_ptr[i] : al.tbl[i]] = id;
-  atomicAnd(free_bits + (id >> 5), ~(1u << (id & 31)));
-}
-
-cudaError_t launch_alloc_write(int32_t *block_table, uint32_t *free_bits, const AllocList &al, cudaStream_t s) {
-  if (al.n <= 0) return cudaSuccess;
-  alloc_write_kernel<<<(al.n + 255) / 256, 256, 0, s>>>(block_table, free_bits, al);
-  return cudaGetLastError();
-}
-
 // One CTA moves kUnitsPerCta (token, kv-head) rows of K and V: phase 1 resolves each unit's
-// destination slot (binary search of q_indptr + one table read) into shared memory, phase 2
-// copies with every thread issuing all its 16-byte loads before its stores (ILP).
+// destination slot (binary search of q_indptr + the request's block id) into shared memory,
+// phase 2 copies with every thread issuing all its 16-byte loads before its stores (ILP).
 constexpr int kUnitsPerCta = 32;
-__global__ void __launch_bounds__(256) append_kernel(
-    const uint16_t *__restrict__ k_new, const uint16_t *__restrict__ v_new, int64_t stride_tok,
-    uint16_t *__restrict__ k_pool, uint16_t *__restrict__ v_pool, int32_t Hkv, int32_t d,
-    const int32_t *__restrict__ block_table, int32_t max_blocks, const __grid_constant__ ReqList<AppendReq> L,
-    int32_t total_new_tok, int32_t early_trigger) {
+struct AppendArgs {
+  const uint16_t *k_new, *v_new;
+  int64_t stride_tok;
+  uint16_t *k_pool, *v_pool;
+  int32_t Hkv, d;
+  int32_t *block_table;
+  int32_t max_blocks, total_new_tok, early_trigger, n_app_ctas;
+  uint32_t *free_bits;
+};
+template <bool ALLOC>
+struct AllocParam {
+  AllocList al;
+};
+template <>
+struct AllocParam<false> {};
+
+template <bool ALLOC>
+__global__ void __launch_bounds__(256) append_kernel(const __grid_constant__ AppendArgs a,
+                                                     const __grid_constant__ ReqList<AppendReq> L,
+                                                     const __grid_constant__ AllocParam<ALLOC> ap) {
   // early_trigger (the append of the tile-path rows only): the tile kernel launched right
   // after it (programmatic dependent launch) may become resident now; it waits
   // (griddepcontrol.wait) before reading the pool.  The decode kernel, a dependent of the tile
@@ -129,12 +160,24 @@ __global__ void __launch_bounds__(256) append_kernel(
   // stream wrote.  The decode-class append never triggers early: a tile kernel launched right
   // after it (no tile-path rows) starts only once those rows are complete, and so does the
   // decode kernel behind it.
-  if (early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if constexpr (ALLOC) {
+    if ((int)blockIdx.x >= a.n_app_ctas) {  // allocation publishing
+      const AllocList &al = ap.al;
+      const int i = ((int)blockIdx.x - a.n_app_ctas) * blockDim.x + threadIdx.x;
+      if (i >= al.n) return;
+      const int32_t id = al.ids_ptr ? al.ids_ptr[i] : al.ids[i];
+      a.block_table[al.tbl_ptr ? al.tbl_ptr[i] : al.tbl[i]] = id;
+      atomicAnd(a.free_bits + (id >> 5), ~(1u << (id & 31)));
+      return;
+    }
+  }
   const AppendReq *reqs = L.ptr ? L.ptr : L.req;
   const int32_t *tok_pre = L.ptr ? L.pre_ptr : L.pre;
   const int num_reqs = L.n;
+  const int Hkv = a.Hkv, d = a.d;
   __shared__ int64_t s_src[kUnitsPerCta], s_dst[kUnitsPerCta];
-  const int64_t n_units = (int64_t)total_new_tok * Hkv;
+  const int64_t n_units = (int64_t)a.total_new_tok * Hkv;
   const int64_t u0 = (int64_t)blockIdx.x * kUnitsPerCta;
   if (threadIdx.x < kUnitsPerCta) {
     const int64_t unit = u0 + threadIdx.x;
@@ -149,8 +192,9 @@ __global__ void __launch_bounds__(256) append_kernel(
       const AppendReq rq = reqs[lo];
       const int off = j - tok_pre[lo];
       const int t = rq.pos0 + off;
-      const int32_t id = block_table[(int64_t)rq.table_row * max_blocks + t / kBlock];
-      src = (int64_t)(rq.q_row0 + off) * stride_tok + (int64_t)h * d;
+      const int32_t id = rq.blk[0] >= 0 ? rq.blk[t / kBlock - rq.pos0 / kBlock]
+                                        : a.block_table[(int64_t)rq.table_row * a.max_blocks + t / kBlock];
+      src = (int64_t)(rq.q_row0 + off) * a.stride_tok + (int64_t)h * d;
       dst = (((int64_t)id * Hkv + h) * kBlock + t % kBlock) * d;
     }
     s_src[threadIdx.x] = src;
@@ -173,29 +217,41 @@ __global__ void __launch_bounds__(256) append_kernel(
       const int tensor = r / cpr, part = r % cpr;
       if (s_src[u] >= 0) {
         isv[k] = tensor;
-        v[k] = __ldg(reinterpret_cast<const uint4 *>((tensor ? v_new : k_new) + s_src[u] + part * 8));
+        v[k] = __ldg(reinterpret_cast<const uint4 *>((tensor ? a.v_new : a.k_new) + s_src[u] + part * 8));
         dsto[k] = s_dst[u] + part * 8;
       }
     }
   }
 #pragma unroll
   for (int k = 0; k < kMaxIt; ++k)
-    if (dsto[k] >= 0) *reinterpret_cast<uint4 *>((isv[k] ? v_pool : k_pool) + dsto[k]) = v[k];
+    if (dsto[k] >= 0) *reinterpret_cast<uint4 *>((isv[k] ? a.v_pool : a.k_pool) + dsto[k]) = v[k];
 }
 
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
                           uint16_t *k_pool, uint16_t *v_pool, int32_t Hkv, int32_t d,
-                          const int32_t *block_table, int32_t max_blocks,
+                          int32_t *block_table, int32_t max_blocks,
                           const ReqList<AppendReq> &L, int32_t total_new_tok, cudaStream_t s,
-                          bool early_trigger) {
-  const int64_t units = (int64_t)total_new_tok * Hkv;
-  if (units <= 0 || L.n <= 0) return cudaSuccess;
-  static bool carve = (cudaFuncSetAttribute(append_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                            cudaSharedmemCarveoutMaxShared), true);
-  (void)carve;
-  append_kernel<<<(unsigned)((units + kUnitsPerCta - 1) / kUnitsPerCta), 256, 0, s>>>(
-      k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks, L, total_new_tok,
-      early_trigger ? 1 : 0);
+                          bool early_trigger, const AllocList *al, uint32_t *free_bits) {
+  const int64_t units = L.n > 0 ? (int64_t)total_new_tok * Hkv : 0;
+  const int n_app = (int)((units + kUnitsPerCta - 1) / kUnitsPerCta);
+  const int n_alloc = al ? (al->n + 255) / 256 : 0;
+  if (n_app + n_alloc <= 0) return cudaSuccess;
+  AppendArgs a{k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks,
+               total_new_tok, early_trigger ? 1 : 0, n_app, free_bits};
+  if (al && al->n > 0) {
+    static bool carve = (cudaFuncSetAttribute(append_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              cudaSharedmemCarveoutMaxShared), true);
+    (void)carve;
+    AllocParam<true> ap;
+    ap.al = *al;
+    append_kernel<true><<<(unsigned)(n_app + n_alloc), 256, 0, s>>>(a, L, ap);
+  } else {
+    if (n_app <= 0) return cudaSuccess;
+    static bool carve = (cudaFuncSetAttribute(append_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              cudaSharedmemCarveoutMaxShared), true);
+    (void)carve;
+    append_kernel<false><<<(unsigned)n_app, 256, 0, s>>>(a, L, AllocParam<false>{});
+  }
   return cudaGetLastError();
 }
 

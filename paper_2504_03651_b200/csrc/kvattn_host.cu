@@ -281,9 +281,6 @@ struct kva_pool {
   // decode kernel on the caller's stream; fork/join by events)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // kv_append's side-stream part (rows read only by the tile kernel): ev_app marks its end;
-  // later calls on the pool order themselves after it (kv_pool_sync for anything else)
-  cudaEvent_t ev_afork = nullptr, ev_app = nullptr;
   // plan uploads (shared by the pool's plans: a plan created later re-records them, which only
   // orders an earlier plan's run after the later upload as well — never a cycle)
   cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
@@ -291,8 +288,6 @@ struct kva_pool {
   // upload events (calls on one pool must be serialised anyway; this keeps a
   // violation from silently reordering another plan's upload)
   std::mutex up_mu;
-  bool app_pending = false;
-  cudaStream_t aux_lo = nullptr;  // least-priority side stream of those writes (yields to decode)
   // burst-reserve threshold: < 0 = none
   int64_t threshold_blocks = -1, active_blocks = 0;
 };
@@ -333,11 +328,8 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&p->aux, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&p->aux_lo, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_afork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_app, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_up0, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_up1, cudaEventDisableTiming) != cudaSuccess) {
       delete p;
@@ -370,11 +362,8 @@ extern "C" kva_status kv_pool_destroy(kva_pool *p) {
     DeviceGuard dg(p->desc.device);
     p->staging.release();
     if (p->aux) cudaStreamDestroy(p->aux);
-    if (p->aux_lo) cudaStreamDestroy(p->aux_lo);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
-    if (p->ev_afork) cudaEventDestroy(p->ev_afork);
-    if (p->ev_app) cudaEventDestroy(p->ev_app);
     if (p->ev_up0) cudaEventDestroy(p->ev_up0);
     if (p->ev_up1) cudaEventDestroy(p->ev_up1);
   }
@@ -383,10 +372,8 @@ extern "C" kva_status kv_pool_destroy(kva_pool *p) {
 }
 
 extern "C" kva_status kv_pool_sync(kva_pool *p, kva_stream_t stream) {
+  (void)stream;  // every kv_append write is on the caller's stream: nothing to order
   if (!p) return fail(KVA_ERR_INVALID, "null pool");
-  if (!p->app_pending) return KVA_OK;
-  DeviceGuard dg(p->desc.device);
-  CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), p->ev_app, 0));
   return KVA_OK;
 }
 
@@ -575,8 +562,10 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
   // allocate: descriptor order, positions ascending, smallest free id first (reading #13)
   hs.lap("append.count");
   std::vector<uint32_t> fh = p->free_host;  // commit only after everything is enqueued
+  std::vector<int32_t> first_new(b->num_reqs);  // request i's allocations: ap.ids[first_new[i] ...]
   int scan = 0;
   for (int i = 0; i < b->num_reqs; ++i) {
+    first_new[i] = (int32_t)ap.ids.size();
     const int ql = qlen(b, i), ctx = b->ctx_len[i], start = ctx - ql;
     const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
     for (int k = start / kBlock; k < cdiv(ctx, kBlock); ++k) {
@@ -591,20 +580,23 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   hs.lap("append.guard");
-  // earlier side-stream appends may still read this workspace / write the pool
-  if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));
-  // Split by the kernel that reads the new rows: decode-class requests (served by the decode
-  // kernel on `stream`) are appended on `stream`; the rest (read only by the tile kernel, which
-  // runs on the pool's side stream) are appended on the side stream, off the decode kernel's
-  // critical path.  Lists travel as kernel parameters unless they overflow the inline capacity.
+  // Two request lists: decode-class requests (<= 16 rows: their <= 2 blocks resolved here, so
+  // their append reads no table entry and shares one launch with the allocation publishing),
+  // then the rest (prefill chunks, whose rows are read only by the tile kernel: that launch
+  // reads the freshly written table and lets the tile kernel start early, PDL).  Lists travel
+  // as kernel parameters unless they overflow the inline capacity.
   const int g = b->num_q_heads / b->num_kv_heads;
   std::vector<AppendReq> ra, rb;
   std::vector<int32_t> pa{0}, pbv{0};
   for (int i = 0; i < b->num_reqs; ++i) {
     const int ql = qlen(b, i);
     if (ql == 0) continue;
-    const AppendReq rq{b->q_indptr[i], ql, b->ctx_len[i] - ql, i};
+    AppendReq rq{b->q_indptr[i], ql, b->ctx_len[i] - ql, i, {-1, -1}};
     if (ql * g <= kDecodeRows) {
+      const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+      int cur = first_new[i];
+      const int kb0 = rq.pos0 / kBlock, kb1 = cdiv(b->ctx_len[i], kBlock);
+      for (int k = kb0; k < kb1 && k < kb0 + 2; ++k) rq.blk[k - kb0] = row[k] != -1 ? row[k] : ap.ids[cur++];
       ra.push_back(rq);
       pa.push_back(pa.back() + ql);
     } else {
@@ -659,45 +651,13 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
     CUDA_TRY(p->staging.upload(slot, workspace, off, s));
   }
   hs.lap("append.lists");
-  CUDA_TRY(launch_alloc_write(b->block_table, p->desc.free_bits, al, s));
-  hs.lap("append.launch_alloc");
-  // Default: both appends on `stream` (decode-class rows first); the tile kernel, launched next
-  // with programmatic dependent launch, becomes resident while the tile-path rows are still
-  // being written and waits for them in-kernel, and the decode kernel (dependent of the tile
-  // kernel) starts meanwhile.  KVA_APPEND_SIDE=1: tile-path rows on a side stream instead.
-  static const bool side = [] {
-    const char *e = getenv("KVA_APPEND_SIDE");
-    return e && std::string(e) == "1";
-  }();
-  if (!side) {
-    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
-                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
-                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                           b->max_blocks, la, pa.back(), s));
-    if (!rb.empty())  // the tile kernel (PDL) may start while these rows are written
-      CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
-                             stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
-                             static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                             b->max_blocks, lb, pbv.back(), s, /*early_trigger=*/true));
-  }
-  if (side && !rb.empty()) {  // fork after the table update, before the decode-class append
-    CUDA_TRY(cudaEventRecord(p->ev_afork, s));
-    CUDA_TRY(cudaStreamWaitEvent(p->aux_lo, p->ev_afork, 0));
-  }
-  if (side)
-    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
-                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
-                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                           b->max_blocks, la, pa.back(), s));
-  if (side && !rb.empty()) {
-    CUDA_TRY(launch_append(static_cast<const uint16_t *>(k_new), static_cast<const uint16_t *>(v_new),
-                           stride_tok, static_cast<uint16_t *>(p->desc.k_pool),
-                           static_cast<uint16_t *>(p->desc.v_pool), Hkv, d, b->block_table,
-                           b->max_blocks, lb, pbv.back(), p->aux_lo));
-    CUDA_TRY(cudaEventRecord(p->ev_app, p->aux_lo));
-    CUDA_TRY(cudaStreamWaitEvent(p->aux, p->ev_app, 0));  // the tile kernel's stream
-    p->app_pending = true;
-  }
+  uint16_t *kp = static_cast<uint16_t *>(p->desc.k_pool), *vp = static_cast<uint16_t *>(p->desc.v_pool);
+  const uint16_t *kn = static_cast<const uint16_t *>(k_new), *vn = static_cast<const uint16_t *>(v_new);
+  CUDA_TRY(launch_append(kn, vn, stride_tok, kp, vp, Hkv, d, b->block_table, b->max_blocks, la, pa.back(), s,
+                         false, &al, p->desc.free_bits));
+  if (!rb.empty())  // the tile kernel (PDL) may start while these rows are written
+    CUDA_TRY(launch_append(kn, vn, stride_tok, kp, vp, Hkv, d, b->block_table, b->max_blocks, lb, pbv.back(), s,
+                           /*early_trigger=*/true));
   hs.lap("append.launch_append");
   p->active_blocks += ap.need;  // every new block belongs to a running request
   // commit host state: free mirror + caller's host table mirror
@@ -1177,7 +1137,6 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   // rows appended on the side stream are read only by the tile kernel: on `s` it waits for them
   // (on the side stream it is ordered after them already)
   auto wait_append = [&]() -> kva_status {
-    if (pl->pool->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, pl->pool->ev_app, 0));
     return KVA_OK;
   };
   auto run_tile = [&]() -> kva_status {
@@ -1289,23 +1248,39 @@ extern "C" kva_status kva_plan_launch_count(const kva_plan *pl, int32_t phases, 
 // ------------------------------------------------------------------------------------------
 // block release (recompute-mode preemption / finished requests)
 // ------------------------------------------------------------------------------------------
+// Marks ids[0, n) allocated -> free in the host mirror; on an invalid list (out of range,
+// already free, listed twice) every mark is undone and the error returned.
+static kva_status mark_released(kva_pool *p, const int32_t *ids, int64_t n) {
+  const int nb = p->desc.num_blocks;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t id = ids[i];
+    kva_status st = KVA_OK;
+    if (id < 0 || id >= nb) st = fail(KVA_ERR_INVALID, "block id %d out of range", id);
+    else if ((p->free_host[id >> 5] >> (id & 31)) & 1u) {
+      bool twice = false;  // set by this call (an earlier element) or free before it?
+      for (int64_t j = 0; j < i && !twice; ++j) twice = ids[j] == id;
+      st = twice ? fail(KVA_ERR_INVALID, "block %d listed twice", id) : fail(KVA_ERR_INVALID, "block %d is already free", id);
+    }
+    if (st != KVA_OK) {
+      for (int64_t j = 0; j < i; ++j) p->free_host[ids[j] >> 5] &= ~(1u << (ids[j] & 31));
+      return st;
+    }
+    p->free_host[id >> 5] |= 1u << (id & 31);
+  }
+  p->n_free += n;
+  return KVA_OK;
+}
+
 extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t n,
                                         kva_stream_t stream) {
   if (!p || n < 0 || (n > 0 && !ids)) return fail(KVA_ERR_INVALID, "bad arguments");
   if (n == 0) return KVA_OK;
   HSection hs;
-  const int nb = p->desc.num_blocks;
-  std::vector<uint8_t> seen(nb, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    if (ids[i] < 0 || ids[i] >= nb) return fail(KVA_ERR_INVALID, "block id %d out of range", ids[i]);
-    if ((p->free_host[ids[i] >> 5] >> (ids[i] & 31)) & 1u)
-      return fail(KVA_ERR_INVALID, "block %d is already free", ids[i]);
-    if (seen[ids[i]]++) return fail(KVA_ERR_INVALID, "block %d listed twice", ids[i]);
-  }
+  kva_status st = mark_released(p, ids, n);
   hs.lap("release.check");
+  if (st != KVA_OK) return st;
   DeviceGuard dg(p->desc.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (p->app_pending) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_app, 0));  // released blocks' writes
   // ids travel as kernel parameters (<= kReleaseBatch per launch): no device scratch,
   // no host<->device copy, stream-ordered like every other call
   for (int64_t off = 0; off < n; off += kReleaseBatch) {
@@ -1313,8 +1288,46 @@ extern "C" kva_status kv_release_blocks(kva_pool *p, const int32_t *ids, int64_t
     CUDA_TRY(launch_release_ids(p->desc.free_bits, ids + off, cnt, s));
   }
   hs.lap("release.launch");
-  for (int64_t i = 0; i < n; ++i) p->free_host[ids[i] >> 5] |= 1u << (ids[i] & 31);
-  p->n_free += n;
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_truncate(kva_pool *p, kva_batch_desc *b, const int32_t *keep_len, kva_stream_t stream) {
+  if (!p || !b || (b->num_reqs > 0 && !keep_len)) return fail(KVA_ERR_INVALID, "bad arguments");
+  if (b->num_reqs < 0) return fail(KVA_ERR_INVALID, "num_reqs < 0");
+  if (b->num_reqs == 0) return KVA_OK;
+  if (!b->ctx_len || !b->block_table || !b->block_table_host || b->max_blocks <= 0)
+    return fail(KVA_ERR_INVALID, "ctx_len, block_table, block_table_host and max_blocks required");
+  HSection hs;
+  std::vector<int32_t> tbl, ids;
+  for (int i = 0; i < b->num_reqs; ++i) {
+    const int keep = keep_len[i], ctx = b->ctx_len[i];
+    if (keep == -1) continue;
+    if (keep < 0 || keep > ctx || ctx > b->max_blocks * kBlock)
+      return fail(KVA_ERR_INVALID, "request %d: keep_len %d not in [0, ctx_len %d]", i, keep, ctx);
+    const int k0 = cdiv(keep, kBlock);
+    if (b->group_of && b->group_of[i] >= 0 && b->group_prefix_blocks && b->group_of[i] < b->num_groups &&
+        k0 < b->group_prefix_blocks[b->group_of[i]])
+      return fail(KVA_ERR_GROUP, "request %d: truncation inside its shared prefix", i);
+    const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+    for (int k = k0; k < cdiv(ctx, kBlock); ++k) {
+      if (row[k] == -1) continue;
+      tbl.push_back(i * b->max_blocks + k);
+      ids.push_back(row[k]);
+    }
+  }
+  const int64_t n = (int64_t)ids.size();
+  if (n == 0) return KVA_OK;
+  kva_status st = mark_released(p, ids.data(), n);
+  hs.lap("truncate.check");
+  if (st != KVA_OK) return st;
+  DeviceGuard dg(p->desc.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int64_t off = 0; off < n; off += kReleaseBatch) {
+    const int cnt = (int)std::min<int64_t>(kReleaseBatch, n - off);
+    CUDA_TRY(launch_release_ids(p->desc.free_bits, ids.data() + off, cnt, s, tbl.data() + off, b->block_table));
+  }
+  for (int32_t t : tbl) b->block_table_host[t] = -1;
+  hs.lap("truncate.launch");
   return KVA_OK;
 }
 
@@ -1362,7 +1375,12 @@ kva_status manager_validate(const kva_block_meta *m, const kva_manager_update *u
   if (u->n_chains < 0 || u->pool_len < 0 || u->del_len < 0) return fail(KVA_ERR_INVALID, "negative counts");
   if (u->pool_len > 0 && !u->pool_ids) return fail(KVA_ERR_INVALID, "pool_ids required");
   if (u->del_len > 0 && (!u->del_ids || u->recount)) return fail(KVA_ERR_INVALID, "del_ids only in incremental mode");
-  if (u->n_chains > 0) {
+  if (u->n_chains > 0 && u->chains_on_device) {
+    if (!u->chain_indptr || !u->chain_state || (u->n_chain_ids > 0 && !u->chain_ids))
+      return fail(KVA_ERR_INVALID, "chain arrays required");
+    if (u->n_chain_ids < 0 || u->n_chain_ids > INT32_MAX) return fail(KVA_ERR_INVALID, "n_chain_ids out of range");
+    *tot_out = u->n_chain_ids;
+  } else if (u->n_chains > 0) {
     if (!u->chain_indptr || !u->chain_state) return fail(KVA_ERR_INVALID, "chain arrays required");
     if (u->chain_indptr[0] != 0) return fail(KVA_ERR_INVALID, "chain_indptr[0] != 0");
     for (int32_t j = 0; j < u->n_chains; ++j) {
@@ -1389,7 +1407,9 @@ size_t manager_ws_bytes(int64_t n, int64_t tot, int32_t nc) {
 extern "C" kva_status kv_manager_step_workspace_size(const kva_block_meta *m, const kva_manager_update *u,
                                                      size_t *bytes) {
   if (!m || !u || !bytes) return fail(KVA_ERR_INVALID, "null argument");
-  const int64_t tot = (u->n_chains > 0 && u->chain_indptr) ? u->chain_indptr[u->n_chains] : 0;
+  const int64_t tot = u->n_chains <= 0 ? 0
+                      : u->chains_on_device ? std::max<int64_t>(0, u->n_chain_ids)
+                      : (u->chain_indptr ? u->chain_indptr[u->n_chains] : 0);
   *bytes = manager_ws_bytes(m->num_blocks, tot, std::max(0, u->n_chains));
   return KVA_OK;
 }
@@ -1411,7 +1431,13 @@ extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager
   uint8_t *w = static_cast<uint8_t *>(ws);
   const size_t o_ind = align256((size_t)tot * 4), o_st = o_ind + align256((size_t)(nc + 1) * 4);
   const size_t o_win = o_st + align256((size_t)nc + 1);
-  if (tot > 0) {  // upload the raw chains (no per-element host work beyond validation)
+  const int32_t *d_ids = reinterpret_cast<const int32_t *>(w), *d_ind = reinterpret_cast<const int32_t *>(w + o_ind);
+  const uint8_t *d_st = w + o_st;
+  if (u->chains_on_device) {
+    d_ids = u->chain_ids;
+    d_ind = u->chain_indptr;
+    d_st = u->chain_state;
+  } else if (tot > 0) {  // upload the raw chains (no per-element host work beyond validation)
     std::lock_guard<std::mutex> lk(g_mgr_mu);
     Staging::Slot *slot = nullptr;
     CUDA_TRY(g_mgr_staging.get(o_win, &slot));
@@ -1422,9 +1448,7 @@ extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager
     CUDA_TRY(g_mgr_staging.upload(slot, ws, o_st + nc, s));
   }
   hs.lap("manager.upload");
-  CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now,
-                               reinterpret_cast<const int32_t *>(w), tot,
-                               reinterpret_cast<const int32_t *>(w + o_ind), w + o_st, nc,
+  CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now, d_ids, tot, d_ind, d_st, nc,
                                reinterpret_cast<int32_t *>(w + o_win), u->recount != 0, u->pool_ids,
                                u->pool_len, u->del_ids, u->del_len, keys, n_active, s));
   hs.lap("manager.launch");

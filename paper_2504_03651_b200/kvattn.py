@@ -54,7 +54,7 @@ class ManagerUpdate(ctypes.Structure):
     _fields_ = [("now", ctypes.c_uint32), ("n_chains", ctypes.c_int32), ("chain_indptr", ctypes.c_void_p),
                 ("chain_ids", ctypes.c_void_p), ("chain_state", ctypes.c_void_p), ("recount", ctypes.c_int32),
                 ("pool_ids", ctypes.c_void_p), ("pool_len", ctypes.c_int64), ("del_ids", ctypes.c_void_p),
-                ("del_len", ctypes.c_int64)]
+                ("del_len", ctypes.c_int64), ("chains_on_device", ctypes.c_int32), ("n_chain_ids", ctypes.c_int64)]
 
 
 class PlanStats(ctypes.Structure):
@@ -73,7 +73,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
            "kva_plan_set_span_buffer",
            "kva_plan_destroy",
-           "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "evict_keys",
+           "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "kv_truncate", "evict_keys",
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
            "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step",
            "kva_prefix_index_create", "kva_prefix_index_destroy", "kva_prefix_insert", "kva_prefix_lookup",
@@ -117,6 +117,7 @@ def load(build_if_missing: bool = True):
         "kva_plan_set_timing_events": ([P, P, P, P, P], ctypes.c_int),
         "kva_plan_set_span_buffer": ([P, P], ctypes.c_int),
         "kv_release_blocks": ([P, P, i64, P], ctypes.c_int),
+        "kv_truncate": ([P, P, P, P], ctypes.c_int),
         "kva_plan_destroy": ([P], ctypes.c_int),
         "kva_plan_get_stats": ([P, P], ctypes.c_int),
         "hybrid_attention": ([P, P, P, i64, i64, P, i64, i64, i32, P, P, sz, P], ctypes.c_int),
@@ -188,7 +189,7 @@ class Pool:
         _check(load().kv_pool_resync(self.handle))
 
     def sync(self, stream=None):
-        """kv_pool_sync: order `stream` after the pool's side-stream kv_append writes."""
+        """kv_pool_sync (a no-op: every kv_append write is on the caller's stream)."""
         _check(load().kv_pool_sync(self.handle, _stream(stream)))
 
     def set_threshold(self, threshold_blocks: int):
@@ -348,8 +349,10 @@ class Plan:
                                                  h(decode_begin), h(decode_end)))
 
     def set_span_buffer(self, span: torch.Tensor | None):
-        """kva_plan_set_span_buffer: int64 device tensor [4] (decode start/end, tile start/end ns;
-        initialise [0], [2] to -1 (= UINT64_MAX bits) and [1], [3] to 0)."""
+        """kva_plan_set_span_buffer: int64 device tensor [6] (decode, tile, merge start/end ns;
+        initialise [0], [2], [4] to -1 (= UINT64_MAX bits) and [1], [3], [5] to 0)."""
+        if span is not None and span.numel() < 6:
+            raise KvaError(ERR_INVALID, "span buffer needs 6 entries")
         _check(load().kva_plan_set_span_buffer(self.handle, _ptr(span) if span is not None else None))
 
     def launch_count(self, phases: int = PHASE_ALL) -> int:
@@ -385,6 +388,15 @@ def hybrid_attention(pool: Pool, batch: Batch, q: torch.Tensor, out: torch.Tenso
     return out
 
 
+def kv_truncate(pool: Pool, batch: Batch, keep_len, stream=None):
+    """Shorten request i to its first keep_len[i] tokens (-1: untouched): its blocks past that
+    are released and their table entries reset to -1 (host mirror and device table)."""
+    a = np.ascontiguousarray(keep_len, np.int32)
+    if a.size != batch.num_reqs:
+        raise KvaError(ERR_INVALID, "keep_len must have num_reqs entries")
+    _check(load().kv_truncate(pool.handle, ctypes.byref(batch.desc()), a.ctypes.data, _stream(stream)))
+
+
 def kv_release_blocks(pool: Pool, ids, stream=None):
     """Return blocks (host int32 ids) to the free pool (recompute-mode release)."""
     a = np.ascontiguousarray(ids, np.int32)
@@ -415,6 +427,15 @@ class ManagerStep:
         self.ws = torch.empty(256, dtype=torch.uint8, device=state.device)
 
     @staticmethod
+    def chains_to_device(csr, device):
+        """A chains_csr() tuple as device tensors (kva_manager_update.chains_on_device): the
+        call then uploads nothing and the ids are range-checked on the device."""
+        ci, cids, cst = csr
+        return (torch.from_numpy(np.ascontiguousarray(ci, np.int32)).to(device),
+                torch.from_numpy(np.ascontiguousarray(cids[: int(ci[-1])], np.int32)).to(device),
+                torch.from_numpy(np.ascontiguousarray(cst, np.uint8)).to(device))
+
+    @staticmethod
     def chains_csr(chains):
         """[(state, ids-array), ...] -> host CSR (indptr, ids, states) for __call__."""
         ci = np.zeros(len(chains) + 1, np.int32)
@@ -433,15 +454,20 @@ class ManagerStep:
         ci, cids, cst = chains if isinstance(chains, tuple) else self.chains_csr(chains)
         plen = pool_ids.numel() if pool_ids is not None else 0
         dlen = del_ids.numel() if del_ids is not None else 0
+        on_dev = isinstance(ci, torch.Tensor)  # device CSR (chains_to_device): no upload
         L = load()
         # the marshalled update is reused while the same arrays / tensors are passed (the cache
         # holds references, so an identity cannot be recycled while cached); in-place edits of
         # the arrays keep their addresses
-        key = (ci, cids, cst, pool_ids, del_ids, plen, dlen, int(ci[-1]) if len(ci) else 0)
+        n_ids = (int(cids.numel()) if on_dev else (int(ci[-1]) if len(ci) else 0))
+        key = (ci, cids, cst, pool_ids, del_ids, plen, dlen, n_ids)
         c = getattr(self, "_ucache", None)
         if (c is None or any(a is not b for a, b in zip(c[0][:5], key[:5])) or c[0][5:] != key[5:]):
-            u = ManagerUpdate(0, len(ci) - 1, ci.ctypes.data, cids.ctypes.data, cst.ctypes.data, 0,
-                              _ptr(pool_ids) if plen else None, plen, _ptr(del_ids) if dlen else None, dlen)
+            ptr = _ptr if on_dev else (lambda a: a.ctypes.data)
+            nch = (ci.numel() if on_dev else len(ci)) - 1
+            u = ManagerUpdate(0, nch, ptr(ci), ptr(cids), ptr(cst), 0,
+                              _ptr(pool_ids) if plen else None, plen, _ptr(del_ids) if dlen else None, dlen,
+                              1 if on_dev else 0, n_ids)
             need = ctypes.c_size_t()
             _check(L.kv_manager_step_workspace_size(ctypes.byref(self.meta), ctypes.byref(u), ctypes.byref(need)))
             c = self._ucache = (key, u, need.value)

@@ -18,7 +18,7 @@ def main():
     dump_all = "--all" in sys.argv
     if e2e:  # profile the pipelined end-to-end loop (host copies) instead of the device-only one
         os.environ["KVA_BENCH_E2E_IN_PROFILE"] = "1"
-    sys.argv = [sys.argv[0], "--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+    sys.argv = [sys.argv[0], "--config", cfg, "--steps", "6", "--warmup", "3", "--no-cpu-baseline",
                 "--profile"] + ([] if e2e else ["--no-e2e"])
     import bench
     from torch.profiler import ProfilerActivity, profile
@@ -31,7 +31,7 @@ def main():
             evs.append((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)))
     evs.sort()
     mine = [x for x in evs if any(k in x[2] for k in ("kva::", "decode_", "tile_", "merge_kernel",
-                                                      "append_kernel", "alloc_write", "evict_", "release_ids",
+                                                      "append_kernel", "manager_", "evict_", "release_ids",
                                                       "Memcpy", "Memset", "elementwise", "copy"))]
     if dump_all:  # every CUDA event of the run (relative to the first)
         t00 = mine[0][0]
@@ -49,7 +49,7 @@ def main():
             json.dump(allrows, open(out, "w"), indent=0)
         return
     # last step = kernels after the last append_kernel's preceding evict_keys
-    starts = [i for i, x in enumerate(mine) if "manager_apply" in x[2]] or [0]
+    starts = [i for i, x in enumerate(mine) if "manager_kernel" in x[2]] or [0]
     last = mine[starts[-1]:]
     t0 = last[0][0]
     rows = [{"kernel": n.split("(")[0][-40:], "stream": s, "start_us": round(a - t0, 1),

@@ -217,3 +217,32 @@ def test_select_small_odd_and_unaligned(n):
             s, ref = oracle.evict_select(kk, k)
             assert nsel == len(ref)
             assert np.array_equal(ids.cpu().numpy(), ref), (off, k)
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "qwen14b"])
+def test_truncate_rollback_matches_oracle(cfg):
+    """kv_truncate: after kv_append, truncating every request to its pre-append length
+    gives the oracle's table (host mirror AND device table) and free bitmap — the pristine
+    ones — and the next kv_append re-allocates exactly the same ids (smallest free first)."""
+    import paper_2504_03651_b200 as K
+    wl = W.make_workload(cfg)
+    dev = "cuda"
+    fb = K.free_bits_tensor(wl.free_bits, dev)
+    pool = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), fb)
+    batch = K.Batch(wl.batch, dev)
+    n0 = pool.free_count()
+    K.kv_append(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+    after = batch.table_host.copy()
+    keep = (wl.batch["ctx_len"] - np.diff(wl.batch["q_indptr"])).astype(np.int32)
+    s, fb_ref, bt_ref = oracle.truncate(dict(wl.batch, block_table=after), fb.cpu().numpy().view(np.uint32), keep)
+    assert s == oracle.OK
+    K.kv_truncate(pool, batch, keep)
+    torch.cuda.synchronize()
+    assert np.array_equal(batch.table_host, bt_ref) and np.array_equal(bt_ref, wl.batch["block_table"])
+    assert np.array_equal(batch.table_dev.cpu().numpy(), bt_ref)
+    assert np.array_equal(fb.cpu().numpy().view(np.uint32), fb_ref)
+    assert pool.free_count() == n0
+    K.kv_append(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+    assert np.array_equal(batch.table_host, after)
+    with pytest.raises(K.KvaError):  # keep > ctx
+        K.kv_truncate(pool, batch, wl.batch["ctx_len"] + 1)

@@ -151,3 +151,34 @@ def test_threshold_parity():
     for t, expect in [(W.ONLINE_PREFILL, K.OK), (W.OFFLINE_PREFILL, K.NEEDS_EVICTION)]:
         w = _thr_workload([t], [64], [64])
         assert _append(w, 1, 1)[0] == expect
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_manager_device_resident_chains(seed):
+    """kva_manager_update.chains_on_device: the same CSR passed as device arrays gives the
+    oracle's state / rc / lat / keys / active count bit-exactly (last chain wins on the device);
+    ids outside [0, n) are skipped, i.e. the result equals the oracle on the chains without
+    them."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(100, 5000))
+    state = rng.integers(0, 6, n).astype(np.uint8)
+    lat = rng.integers(0, 100, n).astype(np.uint32)
+    depth = rng.integers(0, 8, n).astype(np.uint16)
+    rc = np.zeros(n, np.uint32)
+    d_state, d_lat, d_rc = _dev(state, np.uint8), _dev(lat, np.int32), _dev(rc, np.int32)
+    mgr = K.ManagerStep(d_state, d_rc, d_lat, _dev(depth, np.int16))
+    chains = [(int(rng.integers(0, 6)), rng.choice(n, int(rng.integers(1, 40)), replace=False))
+              for _ in range(int(rng.integers(1, 12)))]
+    bad = [(int(rng.integers(0, 6)), np.concatenate([c[1], [n + 5, -3]])) for c in chains[:1]]
+    pool = [rng.choice(n, int(rng.integers(1, 60)), replace=False) for _ in range(int(rng.integers(1, 30)))]
+    pool_ids = torch.from_numpy(np.concatenate(pool).astype(np.int32)).cuda()
+    csr = K.ManagerStep.chains_to_device(K.ManagerStep.chains_csr(bad + chains), "cuda")
+    keys = mgr(77, csr, pool_ids)
+    torch.cuda.synchronize()
+    clean = [(bad[0][0], bad[0][1][:-2])] + chains
+    st, state, rc, lat, rkeys, nact = oracle.manager_step(state, rc, lat, depth, 77, clean, pool)
+    assert st == oracle.OK
+    assert np.array_equal(d_state.cpu().numpy(), state)
+    assert np.array_equal(_u32(d_rc), rc) and np.array_equal(_u32(d_lat), lat)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), rkeys)
+    assert int(mgr.n_active.item()) == nact

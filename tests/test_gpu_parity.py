@@ -342,9 +342,9 @@ def test_many_requests_uploaded_lists():
     assert st["n_tile_items"] > 560 and st["n_cascade_items"] > 0, st
 
 
-def test_append_side_stream_ordering():
-    """kv_append writes the tile-path rows on the pool's side stream (include/kvattn.h
-    "Ordering"): after kv_pool_sync, work on the caller's stream sees the complete pool,
+def test_append_on_a_side_stream_matches_oracle():
+    """kv_append on a non-default stream (include/kvattn.h "Ordering": both of its kernels run
+    on the caller's stream): work following it on that stream sees the complete pool,
     bit-identical to the oracle's kv_append (reading #13)."""
     import paper_2504_03651_b200 as K
     wl = W.make_workload("tiny")

@@ -190,3 +190,41 @@ def test_release_blocks_oracle():
         assert s == oracle.INVALID and np.array_equal(fb3, fb), bad
     s, fb4 = oracle.release_blocks(fb, n, [])
     assert s == oracle.OK and np.array_equal(fb4, fb)
+
+
+def test_truncate_oracle_roundtrip_and_errors():
+    """kv_truncate's oracle (P:448 release of a victim's KV): after kv_append, truncating every
+    request to its pre-append length restores the pristine table and free bitmap exactly (the
+    inverse of the append's allocation); keep = ctx is a no-op; keep = 0 on an ungrouped
+    request frees its whole row; a cut inside a group prefix is GROUP, keep > ctx INVALID,
+    and neither changes anything."""
+    import workloads as W
+    wl = W.make_workload("tiny")
+    b = wl.batch
+    s, _, _, _, bt, fb = oracle.kv_append(b, wl.k_pool, wl.v_pool, wl.free_bits, wl.k_new, wl.v_new)
+    assert s == oracle.OK
+    b2 = dict(b, block_table=bt)
+    ql = np.diff(b["q_indptr"])
+    keep = (b["ctx_len"] - ql).astype(np.int32)
+    s, fb_t, bt_t = oracle.truncate(b2, fb, keep)
+    assert s == oracle.OK
+    assert np.array_equal(bt_t, b["block_table"]) and np.array_equal(fb_t, wl.free_bits)
+    s, fb_n, bt_n = oracle.truncate(b2, fb, b["ctx_len"])
+    assert s == oracle.OK and np.array_equal(bt_n, bt) and np.array_equal(fb_n, fb)
+    n = b["num_blocks"]
+    gof = b["group_of"]
+    i = int(np.nonzero(gof < 0)[0][0])
+    keep0 = np.full(len(keep), -1, np.int32)
+    keep0[i] = 0
+    s, fb0, bt0 = oracle.truncate(b2, fb, keep0)
+    row = {int(x) for x in bt[i] if x >= 0}
+    assert s == oracle.OK and _bits_of(fb0, n) == _bits_of(fb, n) | row and (bt0[i] == -1).all()
+    assert np.array_equal(np.delete(bt0, i, 0), np.delete(bt, i, 0))
+    j = int(np.nonzero(gof >= 0)[0][0])
+    bad = np.full(len(keep), -1, np.int32)
+    bad[j] = 16 * (int(b["group_prefix_blocks"][gof[j]]) - 1)  # releases the last prefix block
+    s, fbx, btx = oracle.truncate(b2, fb, bad)
+    assert s == oracle.GROUP and np.array_equal(fbx, fb) and np.array_equal(btx, bt)
+    bad[j] = int(b["ctx_len"][j]) + 1
+    s, fbx, btx = oracle.truncate(b2, fb, bad)
+    assert s == oracle.INVALID and np.array_equal(fbx, fb) and np.array_equal(btx, bt)
