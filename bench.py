@@ -28,7 +28,10 @@ import torch  # noqa: E402
 
 WORKLOAD_NAMES = {"llama7b": "llama7b (BASELINE.json configs[1])", "tiny": "tiny (BASELINE.json configs[0])",
                   "qwen14b": "qwen14b (BASELINE.json configs[2])", "llama70b": "llama70b (BASELINE.json configs[4])",
-                  "qwen14b-p": "qwen14b-p (configs[2] variant: shared-prefix prefill, SURVEY NEXT-4)"}
+                  "qwen14b-p": "qwen14b-p (configs[2] variant: shared-prefix prefill, SURVEY NEXT-4)",
+                  "llama7b-u": "llama7b-u (control: configs[1] with the prefix duplicated per request, no sharing)",
+                  "qwen14b-u": "qwen14b-u (control: configs[2] with the prefix duplicated per request, no sharing)",
+                  "qwen14b-pu": "qwen14b-pu (control: qwen14b-p without sharing)"}
 METRIC = "mixed-batch attention tokens/s and HBM GB/s (% of B200 roofline) at 1/2/4/8 GPUs"
 UNIT = "tokens/s"
 
@@ -42,6 +45,9 @@ def parse():
     ap.add_argument("--config", default="llama7b")
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--l2-rotate", type=int, default=4,
+                    help="replicas of every per-step input (pool, tables, Q/K/V, manager metadata) "
+                         "cycled step by step so no step finds the previous one's data in L2 (1 = off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -215,6 +221,30 @@ def run_ours(args, rank, world, local):
         ev["ids"] = torch.empty(ev["k"], dtype=torch.int32, device=dev)
         ev["ws"] = torch.empty(K.evict_select_workspace_size(ev["n"], ev["k"]), dtype=torch.uint8, device=dev)
 
+    # L2 hygiene (H8): R replicas of every per-step input, step i uses replica i % R — the hot
+    # small parts (shared prefix, Q, workspaces, manager metadata and keys) would otherwise be
+    # re-read from the 126 MB L2 by the next step (the decode stream is marked evict-first and
+    # does not displace them).  Replica 0 is the original; the others are device copies.
+    R = max(1, args.l2_rotate)
+    reps = [dict(pool=pool, batch=batch, ws_app=ws_app, ws_att=ws_att, q=q, k_new=k_new, v_new=v_new,
+                 out=out, lse=lse, ev=ev)]
+    for r in range(1, R):
+        b_r = K.Batch(wl.batch, dev)
+        rp = dict(pool=K.Pool(wl.k_pool.clone(), wl.v_pool.clone(), K.free_bits_tensor(wl.free_bits, dev)),
+                  batch=b_r, ws_app=torch.empty_like(ws_app), ws_att=torch.empty_like(ws_att),
+                  q=q.clone(), k_new=k_new.clone(), v_new=v_new.clone(), out=torch.empty_like(out),
+                  lse=torch.empty_like(lse), ev=None)
+        if ev is not None:
+            e2 = dict(ev)
+            for kname in ("state", "rc", "lat", "depth"):
+                e2[kname] = ev[kname].clone()
+            e2["mgr"] = K.ManagerStep(e2["state"], e2["rc"], e2["lat"], e2["depth"])
+            e2["ids"] = torch.empty_like(ev["ids"])
+            e2["ws"] = torch.empty_like(ev["ws"])
+            rp["ev"] = e2
+        reps.append(rp)
+    rot = {"on": True, "i": 0}
+
     # e2e host buffers (pinned): inputs in, output out, every step
     h_q = q.cpu().pin_memory()
     h_k = k_new.cpu().pin_memory()
@@ -251,6 +281,10 @@ def run_ours(args, rank, world, local):
     gather_on = {"v": True}
 
     def step(time_idx=None):
+        rp = reps[rot["i"] % R] if rot["on"] else reps[0]
+        rot["i"] += 1
+        pool, batch, ev = rp["pool"], rp["batch"], rp["ev"]
+        q, out, lse = rp["q"], rp["out"], rp["lse"]
         n = 0
         if ev is not None:
             # the manager's eviction selection has no data dependency on this layer's attention:
@@ -268,8 +302,8 @@ def run_ours(args, rank, world, local):
             n += 3
         if ev is not None and gate_attn:  # before the append: the attention pair follows it directly
             stream.wait_event(ev_keys)
-        K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream)
-        plan = K.Plan(pool, batch, ws_att, stream=stream)
+        K.kv_append(pool, batch, rp["k_new"], rp["v_new"], rp["ws_app"], stream=stream)
+        plan = K.Plan(pool, batch, rp["ws_att"], stream=stream)
         if plan_launches["n"] is None:  # the same descriptor every step: count once
             plan_launches["n"] = plan.launch_count()
         n += 2 + plan_launches["n"]
@@ -423,12 +457,13 @@ def run_ours(args, rank, world, local):
             ms = t.item()
         return ms
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, R)):  # every replica warmed
         step()
     barrier()
     # the rollback restores the pristine table on both sides (every step starts identically)
-    assert np.array_equal(batch.table_host, pristine_host), "host table != pristine after kv_truncate"
-    assert np.array_equal(batch.table_dev.cpu().numpy(), pristine_host), "device table != pristine"
+    for rp in reps:
+        assert np.array_equal(rp["batch"].table_host, pristine_host), "host table != pristine after kv_truncate"
+        assert np.array_equal(rp["batch"].table_dev.cpu().numpy(), pristine_host), "device table != pristine"
     plan0 = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
     stats = plan0.stats()
     plan0.close()
@@ -437,9 +472,15 @@ def run_ours(args, rank, world, local):
     if not args.profile:
         clocks.start()
     launches["n"] = 0
+    rot["i"] = 0
     ms = timed(args.steps, time_kernels=True)
     gpu_launches = launches["n"]
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+    ms_same = None
+    if R > 1 and not args.profile:  # the same steps on replica 0 only (the delta L2 reuse buys)
+        rot["on"] = False
+        ms_same = timed(args.steps)
+        rot["on"] = True
     sp = spans.cpu().numpy().view(np.uint64)
     dec_ms = [float(sp[i, 1] - sp[i, 0]) * 1e-6 for i in span_used
               if stats["n_decode_items"] > 0 and sp[i, 1] > 0 and sp[i, 1] >= sp[i, 0]]
@@ -525,7 +566,11 @@ def run_ours(args, rank, world, local):
                            ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)" +
                             (" [eviction pass pipelined: issued after the previous step's selection]" if (ev is not None and evict_pipeline) else "")) +
                            "+kv_truncate(rollback of the step's allocations)",
-                   "l2": "no flush: KV working set (%.2f GB/rank) >> 126 MB L2" % (stats["kv_bytes_algorithmic"] / 1e9),
+                   "l2": (f"{R} replicas of every per-step input (pool, tables, Q/K/V, workspaces, manager "
+                          f"metadata, keys) cycled step by step (KV working set %.2f GB/rank per replica)"
+                          % (stats["kv_bytes_algorithmic"] / 1e9)) if R > 1 else
+                         "no rotation (--l2-rotate 1): KV working set %.2f GB/rank" % (stats["kv_bytes_algorithmic"] / 1e9),
+                   "ms_per_step_without_l2_rotation": ms_same,
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
@@ -593,7 +638,42 @@ def _post_append_batch(K, wl, dev):
 
 
 # ------------------------------------------------------------------------------------------
-def oracle_sample(wl, seconds, seed=0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def evict_cpu_timings():
+    """The eviction selection on the host (the `evict` config: 2^20 keys, top-64k): the fp64
+    oracle's full std::sort by (key, id), and a numpy argpartition + sort of the k smallest
+    ("fast CPU" line; not the oracle)."""
+    import oracle
+    import workloads as W
+    ev = W.make_evict()
+    _, keys = oracle.evict_keys(ev.state, ev.rc, ev.lat, ev.depth)
+    t0 = time.perf_counter()
+    s, ids = oracle.evict_select(keys, ev.k)
+    t1 = time.perf_counter()
+    ev_mask = keys != np.uint64(0xFFFFFFFFFFFFFFFF)
+    cand = np.nonzero(ev_mask)[0]
+    kk = keys[cand]
+    part = np.argpartition(kk, ev.k - 1)[:ev.k]   # the k smallest keys (ties at the boundary: then exact sort)
+    thr = kk[part].max()
+    sel = cand[kk <= thr]
+    order = np.lexsort((sel, keys[sel]))[:ev.k]
+    fast = sel[order]
+    t2 = time.perf_counter()
+    assert np.array_equal(fast, ids), "numpy selection disagrees with the oracle"
+    return {"keys": int(len(keys)), "k": int(ev.k), "oracle_std_sort_ms": (t1 - t0) * 1e3,
+            "numpy_argpartition_sort_ms": (t2 - t1) * 1e3, "threads": 1}
+
+
+def oracle_sample(wl, seconds, seed=0, nthreads=None):
     """Time the fp64 oracle on a bounded random sample of (row, head) pairs of the batch."""
     import oracle
     import workloads as W  # noqa: F401
@@ -603,7 +683,7 @@ def oracle_sample(wl, seconds, seed=0):
     b = dict(cpu.batch, block_table=bt)
     Hq = b["num_q_heads"]
     rng = np.random.default_rng(seed)
-    nthreads = os.cpu_count() or 1
+    nthreads = nthreads or os.cpu_count() or 1
     n = max(nthreads, 16)
     while True:
         rows = rng.integers(0, cpu.total_q, n).astype(np.int32)
@@ -649,9 +729,9 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": args.config, "q_tokens": wl.total_q, "Hq": cfg.Hq, "Hkv": cfg.Hkv,
+        "config": {"workload": WORKLOAD_NAMES.get(args.config, args.config), "q_tokens": wl.total_q, "Hq": cfg.Hq, "Hkv": cfg.Hkv,
                    "head_dim": cfg.d},
-        "cpu_baseline": dict(last, value=v),
+        "cpu_baseline": dict(last, value=v, cpu_model=cpu_model()),
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -721,6 +801,11 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline and not args.profile and world == 1:
             res["cpu_baseline"] = oracle_sample(wl, args.cpu_seconds)
+            res["cpu_baseline"]["cpu_model"] = cpu_model()
+            one = oracle_sample(wl, 3.0, seed=7, nthreads=1)
+            res["cpu_baseline"]["one_thread"] = {"value": one["value"], "unit": UNIT, "sample": one["sample"]}
+            if not args.no_evict:
+                res["cpu_baseline"]["evict_select"] = evict_cpu_timings()
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist
