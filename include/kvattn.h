@@ -382,6 +382,20 @@ kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t num_reqs, const 
                                   int32_t *group_of, int32_t *group_prefix_blocks,
                                   int32_t *group_parent, int32_t *num_groups);
 
+/* ---- tuning and diagnostics options (process-wide; read by every later call) ----
+ *   "tile_ctas"   persistent CTAs of the tile kernel while it overlaps the decode kernel
+ *                 (0 = the planner's split from measured rates, default)
+ *   "overlap"     1 = tile kernel concurrent with decode (default), 0 = decode then tile
+ *   "pdl"         1 = decode launched as a programmatic dependent of the tile kernel on one
+ *                 stream (default), 0 = the two kernels on two streams (events)
+ *   "evict_ctas"  CTAs of the cooperative evict_select kernel (0 = #SMs / 2, default)
+ *   "host_prof"   1 = accumulate host section times (printed at process exit)
+ *   "debug_flags" tile-kernel diagnostics, WRONG RESULTS: 1 = softmax skipped, 2 = PV MMAs not
+ *                 issued, 4 = QK MMAs not issued (pipeline studies)
+ *   "debug_ts"    device address of a role-timestamp buffer (builds with -DKVA_TILE_TIMESTAMPS)
+ * Unknown name -> KVA_ERR_INVALID.  Not synchronised with calls in flight on other threads. */
+kva_status kva_set_option(const char *name, int64_t value);
+kva_status kva_get_option(const char *name, int64_t *value);
 /* ---- diagnostics (not part of the hot path) ----
  * kva_diag_occupy: enqueue n_ctas CTAs that each hold smem_bytes of shared memory and spin
  * for ns nanoseconds on `stream`; a kernel launched right after on another stream then runs on

@@ -10,5 +10,5 @@ from .kvattn import (  # noqa: F401
     PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL,
     kv_append_workspace_size, last_error, load, validate_batch, version,
     OK, ERR_INVALID, ERR_UNSUPPORTED, NEEDS_EVICTION, ERR_CAPACITY, EVICTION_SHORT, ERR_GROUP,
-    ERR_CUDA, OUT_BF16, OUT_F32, diag_occupy, ManagerStep, PrefixIndex,
+    ERR_CUDA, OUT_BF16, OUT_F32, diag_occupy, ManagerStep, PrefixIndex, set_option, get_option, options,
 )

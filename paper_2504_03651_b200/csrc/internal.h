@@ -19,10 +19,14 @@ cudaError_t smem_attrs_once(const void *kern, int smem);
 // multiprocessor count of the current device (cached)
 int sm_count();
 
+// Tuning / diagnostics options (kva_set_option; process-wide, read at each call)
+enum Opt : int { kOptTileCtas = 0, kOptOverlap, kOptPdl, kOptEvictCtas, kOptHostProf, kOptDebugFlags, kOptDebugTs,
+                 kOptCount };
+int64_t opt(Opt o);
+
 constexpr int kBlock = 16;        // tokens per KV block (reading #5)
 constexpr int kSplitKeys = 512;   // fixed split-KV length (depends only on ctx, H9)
 constexpr int kDecodeRows = 16;   // rows (q tokens x g heads) one decode warp handles
-constexpr int kTileMMma = 64;     // rows per legacy mma.sync tile CTA (4 warps x 16)
 constexpr int kTileMTc = 128;     // rows per tcgen05 tile CTA (UMMA M = TMEM lanes)
 constexpr int kTileN = 64;        // keys per tile-kernel pipeline stage (4 blocks)
 
@@ -111,10 +115,6 @@ struct AttnParams {
 cudaError_t launch_decode(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                           const ReqList<DecodeReq> &reqs, int n_units, cudaStream_t s, bool pdl = false,
                           const void *tmap_k3 = nullptr, const void *tmap_v3 = nullptr);
-cudaError_t launch_tile(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                        const TileItem *items, int n_items, cudaStream_t s);
-cudaError_t launch_tile_tc(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                           const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 // Tile items of the tcgen05 kernel: kernel parameter when n <= kInlineTiles (no upload, so the
 // tile kernel is not ordered behind a host->device copy and claims its SMs first), else uploaded.
 constexpr int kInlineTiles = 560;
@@ -126,8 +126,6 @@ struct TileList {
 cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmap_k, const void *tmap_v,
                             const TileList &items, int max_ctas, cudaStream_t s,
                             const void *tmap_v3 = nullptr, const void *tmap_k3 = nullptr);
-cudaError_t launch_tile_tc3(const AttnParams &p, const void *tmap_k, const void *tmap_v,
-                            const TileItem *items, int n_items, int max_ctas, cudaStream_t s);
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &reqs, int n_units, cudaStream_t s);
 // Newly allocated blocks (table entry index, block id): kernel parameter when n <= kInlineAlloc,
 // else uploaded (tbl_ptr / ids_ptr set).

@@ -27,274 +27,11 @@
 namespace kva {
 using namespace dev;
 
-template <int D, int NST, int PF>
-__global__ void __launch_bounds__(128, 2)
-    decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tmk,
-                  const __grid_constant__ CUtensorMap tmv, const __grid_constant__ ReqList<DecodeReq> L,
-                  int n_units) {
-  constexpr int HALVES = D / 64;
-  constexpr int KBYTES = 16 * D * 2;  // K (or V) of one block for one head
-  constexpr int STAGE = 2 * KBYTES;
-  constexpr int KT = D / 16;          // k-steps of the QK^T contraction
-  constexpr int NT = D / 8;           // n-tiles of the PV output
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[4][NST];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x * 4 + warp;  // (item, kv head), head fastest
-  if (unit >= n_units) return;             // no CTA-wide barrier below
-  const int item = unit / p.Hkv, kv_head = unit - item * p.Hkv;  // item = (request, split)
-  const DecodeReq *reqs = L.ptr ? L.ptr : L.req;
-  const int32_t *pre = L.ptr ? L.pre_ptr : L.pre;
-  int lo = 0, hi = L.n - 1;  // request: pre[lo] <= item < pre[lo + 1] (warp-uniform search)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= item) lo = mid;
-    else hi = mid - 1;
-  }
-  const DecodeReq rq = reqs[lo];
-  const int split = item - pre[lo];
-  struct {
-    int q_row0, n_tok, table_row, k0, k1, pos0;
-  } it;
-  it.q_row0 = rq.q_row0;
-  it.n_tok = rq.n_tok;
-  it.table_row = rq.table_row;
-  it.k0 = rq.kb + split * kSplitKeys;
-  it.k1 = min(rq.ctx, it.k0 + kSplitKeys);
-  it.pos0 = rq.ctx - rq.n_tok;
-  const int slot = rq.slot < 0 ? -1 : rq.slot + (kv_head * rq.nsplit + split) * (rq.n_tok * p.g);
-  uint8_t *sbase = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
-  uint8_t *ws = sbase + warp * NST * STAGE;
-  uint64_t *bar = bars[warp];
-  const int g = p.g;
-  const int n_rows = it.n_tok * g;
-
-  if (lane == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-
-  const int b0 = it.k0 / kBlock;
-  const int nblk = (it.k1 + kBlock - 1) / kBlock - b0;  // <= 32
-  const int32_t *trow = p.block_table + (int64_t)it.table_row * p.max_blocks + b0;
-  const int my_id = lane < nblk ? __ldg(trow + lane) : 0;
-  const int row_base = kv_head * kBlock;  // + id*Hkv*16
-
-  auto issue = [&](int st, int id) {  // lane 0 only
-    uint64_t *b = &bar[st];
-    mbar_arrive_expect_tx(b, STAGE);
-    const int row = id * p.Hkv * kBlock + row_base;
-    uint8_t *dst = ws + st * STAGE;
-#pragma unroll
-    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + h * 2048, &tmk, b, h * 64, row);
-#pragma unroll
-    for (int h = 0; h < HALVES; ++h) tma_load_2d(dst + KBYTES + h * 2048, &tmv, b, h * 64, row);
-  };
-
-  // L2 prefetch PF blocks beyond the TMA ring: keeps more HBM requests in flight per SM than
-  // shared memory could hold, so the stream saturates HBM on fewer SMs (co-running kernels)
-  auto prefetch = [&](int id) {  // lane 0 only
-    const int row = id * p.Hkv * kBlock + row_base;
-#pragma unroll
-    for (int h = 0; h < HALVES; ++h) {
-      tma_prefetch_2d(&tmk, h * 64, row);
-      tma_prefetch_2d(&tmv, h * 64, row);
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < NST; ++s) {
-    const int id = __shfl_sync(0xffffffffu, my_id, s);
-    if (lane == 0 && s < nblk) issue(s, id);
-  }
-#pragma unroll
-  for (int s = NST; s < NST + PF; ++s) {
-    const int id = __shfl_sync(0xffffffffu, my_id, s & 31);
-    if (lane == 0 && s < nblk) prefetch(id);
-  }
-
-  // Q fragments (A operand, rows = tok*g + hh)
-  const int r_lo = lane >> 2, r_hi = r_lo + 8;
-  const int cq = (lane & 3) * 2;
-  uint32_t qa[KT][4];
-  {
-    const uint32_t *qlo = nullptr, *qhi = nullptr;
-    if (r_lo < n_rows)
-      qlo = reinterpret_cast<const uint32_t *>(
-          p.q + (int64_t)(it.q_row0 + r_lo / g) * p.q_stride_tok +
-          (int64_t)(kv_head * g + r_lo % g) * p.q_stride_head);
-    if (r_hi < n_rows)
-      qhi = reinterpret_cast<const uint32_t *>(
-          p.q + (int64_t)(it.q_row0 + r_hi / g) * p.q_stride_tok +
-          (int64_t)(kv_head * g + r_hi % g) * p.q_stride_head);
-#pragma unroll
-    for (int kk = 0; kk < KT; ++kk) {
-      const int c = kk * 16 + cq;
-      qa[kk][0] = qlo ? __ldg(qlo + c / 2) : 0u;
-      qa[kk][1] = qhi ? __ldg(qhi + c / 2) : 0u;
-      qa[kk][2] = qlo ? __ldg(qlo + (c + 8) / 2) : 0u;
-      qa[kk][3] = qhi ? __ldg(qhi + (c + 8) / 2) : 0u;
-    }
-  }
-  const int pos_lo = it.pos0 + r_lo / g, pos_hi = it.pos0 + r_hi / g;
-
-  float o[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m_lo = -CUDART_INF_F, m_hi = -CUDART_INF_F, l_lo = 0.f, l_hi = 0.f;
-  const float sl2 = p.scale_log2;
-
-  for (int j = 0; j < nblk; ++j) {
-    const int st = j % NST;
-    const int next_id = __shfl_sync(0xffffffffu, my_id, (j + NST) & 31);
-    const int pf_id = __shfl_sync(0xffffffffu, my_id, (j + NST + PF) & 31);
-    mbar_wait(&bar[st], (j / NST) & 1);
-    const uint32_t kb = smem_u32(ws + st * STAGE), vb = kb + KBYTES;
-    const int key0 = (b0 + j) * kBlock;
-    if (key0 + kBlock > it.k1) {
-      // never-written slots of the last block are NaN-poisoned: zero those V rows
-      const int vr = it.k1 - key0;  // valid rows
-      uint8_t *vp = ws + st * STAGE + KBYTES;
-      for (int c = lane; c < (16 - vr) * HALVES * 8; c += 32) {
-        const int h = c / ((16 - vr) * 8), rem = c % ((16 - vr) * 8);
-        const int row = vr + rem / 8, ch = rem % 8;
-        *reinterpret_cast<uint4 *>(vp + h * 2048 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
-      }
-      __syncwarp();
-    }
-    // S = Q K^T  (16 rows x 16 keys)
-    float s[2][4];
-#pragma unroll
-    for (int n = 0; n < 2; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-    {
-      const int key = (lane >> 4) * 8 + (lane & 7);
-      const int csub = ((lane >> 3) & 1) * 8;
-#pragma unroll
-      for (int kk = 0; kk < KT; ++kk) {
-        const int col = kk * 16 + csub;
-        uint32_t r0, r1, r2, r3;
-        ldsm_x4(kb + (col >> 6) * 2048 + sw128(key, col & 63), r0, r1, r2, r3);
-        mma_bf16(s[0], qa[kk], r0, r1);
-        mma_bf16(s[1], qa[kk], r2, r3);
-      }
-    }
-    // mask + scale (log2 domain)
-    float mx_lo = -CUDART_INF_F, mx_hi = -CUDART_INF_F;
-#pragma unroll
-    for (int n = 0; n < 2; ++n) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = key0 + n * 8 + cq + (e & 1);
-        const int pos = (e >> 1) ? pos_hi : pos_lo;
-        const bool ok = key >= it.k0 && key < it.k1 && key <= pos;
-        s[n][e] = ok ? s[n][e] * sl2 : -CUDART_INF_F;
-      }
-      mx_lo = fmaxf(mx_lo, fmaxf(s[n][0], s[n][1]));
-      mx_hi = fmaxf(mx_hi, fmaxf(s[n][2], s[n][3]));
-    }
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-    const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
-    const float base_lo = mn_lo == -CUDART_INF_F ? 0.f : mn_lo;
-    const float base_hi = mn_hi == -CUDART_INF_F ? 0.f : mn_hi;
-    const float a_lo = fast_exp2(m_lo - base_lo), a_hi = fast_exp2(m_hi - base_hi);
-    m_lo = mn_lo;
-    m_hi = mn_hi;
-    float ps_lo = 0.f, ps_hi = 0.f;
-#pragma unroll
-    for (int n = 0; n < 2; ++n) {
-      s[n][0] = fast_exp2(s[n][0] - base_lo);
-      s[n][1] = fast_exp2(s[n][1] - base_lo);
-      s[n][2] = fast_exp2(s[n][2] - base_hi);
-      s[n][3] = fast_exp2(s[n][3] - base_hi);
-      ps_lo += s[n][0] + s[n][1];
-      ps_hi += s[n][2] + s[n][3];
-    }
-    l_lo = l_lo * a_lo + ps_lo;
-    l_hi = l_hi * a_hi + ps_hi;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      o[n][0] *= a_lo;
-      o[n][1] *= a_lo;
-      o[n][2] *= a_hi;
-      o[n][3] *= a_hi;
-    }
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
-    // O += P V
-    {
-      const int key = (lane & 7) + ((lane >> 3) & 1) * 8;
-      const int csub = (lane >> 4) * 8;
-#pragma unroll
-      for (int c16 = 0; c16 < D / 16; ++c16) {
-        const int col = c16 * 16 + csub;
-        uint32_t r0, r1, r2, r3;
-        ldsm_x4_t(vb + (col >> 6) * 2048 + sw128(key, col & 63), r0, r1, r2, r3);
-        mma_bf16(o[2 * c16], pa, r0, r1);
-        mma_bf16(o[2 * c16 + 1], pa, r2, r3);
-      }
-    }
-    __syncwarp();
-    if (lane == 0 && j + NST < nblk) {
-      fence_proxy_async();
-      issue(st, next_id);
-      if (j + NST + PF < nblk) prefetch(pf_id);
-    }
-  }
-  // row sums across the quad
-  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
-  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
-  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
-  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
-
-  constexpr float kLn2 = 0.6931471805599453f;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int r = half ? r_hi : r_lo;
-    if (r >= n_rows) continue;
-    const float l = half ? l_hi : l_lo, m = half ? m_hi : m_lo;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const float lse = l > 0.f ? (m + __log2f(l)) * kLn2 : -CUDART_INF_F;
-    const int tok = r / g, hq = kv_head * g + r % g;
-    if (slot < 0) {
-      const int64_t qrow = it.q_row0 + tok;
-      if (p.out_f32) {
-        float *dst = reinterpret_cast<float *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<float2 *>(dst + n * 8 + cq) =
-              make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
-      } else {
-        uint16_t *dst =
-            reinterpret_cast<uint16_t *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<uint32_t *>(dst + n * 8 + cq) =
-              pack_bf16(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
-      }
-      if (p.lse && (lane & 3) == 0) p.lse[qrow * p.Hq + hq] = lse;
-    } else {
-      float *dst = p.part_o + (int64_t)(slot + r) * D;
-#pragma unroll
-      for (int n = 0; n < NT; ++n)
-        *reinterpret_cast<float2 *>(dst + n * 8 + cq) =
-            make_float2(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
-      if ((lane & 3) == 0) p.part_lse[slot + r] = lse;
-    }
-  }
-}
-
 // ------------------------------------------------------------------------------------------
-// v2 (default): keys along the MMA M dimension.  For decode the rows (q_len x g <= 16) are few,
-// so S^T = K Q^T (M = 16 keys, N = 8 rows, K = d) and O^T = V^T P^T (M = 16 dims, N = 8 rows,
-// K = 16 keys) waste at most the N padding instead of 15/16 of M: half the MMAs of v1 and half
-// its accumulator registers.  P^T goes from the S^T accumulator layout to the B-operand layout
+// Keys along the MMA M dimension.  For decode the rows (q_len x g <= 16) are few, so
+// S^T = K Q^T (M = 16 keys, N = 8 rows, K = d) and O^T = V^T P^T (M = 16 dims, N = 8 rows,
+// K = 16 keys) waste at most the N padding instead of 15/16 of M (the rows-along-M layout of
+// round 1: twice the MMAs and accumulator registers).  P^T goes from the S^T accumulator layout to the B-operand layout
 // with two movmatrix transposes.  The running max is updated lazily (only when it grows by more
 // than 2^8 for some row of the warp, FA4-style), so the O rescale is skipped on almost every
 // block; masking runs only on blocks that reach the causal diagonal or the split end.  Fewer
@@ -653,65 +390,23 @@ static cudaError_t launch_decode_kt(const AttnParams &p, const void *tmk, const 
   return cudaLaunchKernelEx(&cfg, kern, p, mk, mv, L, n);
 }
 
-template <int D, int NST, int PF>
-static cudaError_t launch_decode_t(const AttnParams &p, const void *tmk, const void *tmv,
-                                   const ReqList<DecodeReq> &L, int n, cudaStream_t s) {
-  const size_t smem = 4 * NST * (2 * 16 * D * 2) + 1024;  // + alignment slack
-  auto kern = decode_kernel<D, NST, PF>;
-  // max dynamic smem + full carveout (CTAs of concurrently running kernels share SMs), once
-  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(kern), (int)smem);
-  if (e != cudaSuccess) return e;
-  const CUtensorMap &mk = *reinterpret_cast<const CUtensorMap *>(tmk);
-  const CUtensorMap &mv = *reinterpret_cast<const CUtensorMap *>(tmv);
-  kern<<<(n + 3) / 4, 128, smem, s>>>(p, mk, mv, L, n);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_decode(const AttnParams &p, const void *tmk, const void *tmv,
                           const ReqList<DecodeReq> &L, int n, cudaStream_t s, bool pdl,
                           const void *tmk3, const void *tmv3) {
   if (n <= 0) return cudaSuccess;
-  // KVA_DECODE_IMPL=v1: the M = rows kernel (cross-check); default v2 (keys along M).
-  // KVA_DECODE_CFG: 0 = 3 stages x 2 CTAs/SM (default), 1 = 2 stages x 3 CTAs/SM.
-  static const int impl = [] {
-    const char *e = getenv("KVA_DECODE_IMPL");
-    return e && std::string(e) == "v1" ? 1 : 2;
-  }();
-  static const int cfg = [] {
-    const char *e = getenv("KVA_DECODE_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  if (impl == 2) {
-    int max_rows = 0;
-    const DecodeReq *reqs = L.ptr ? nullptr : L.req;
-    if (reqs)
-      for (int i = 0; i < L.n; ++i) max_rows = std::max(max_rows, reqs[i].n_tok * p.g);
-    else
-      max_rows = kDecodeRows;
-    const bool nr1 = max_rows <= 8;
-    if (p.d == 128) {
-      if (cfg == 1) return nr1 ? launch_decode_kt<128, 1, 2, 3>(p, tmk, tmv, L, n, s, pdl)
-                               : launch_decode_kt<128, 2, 2, 3>(p, tmk, tmv, L, n, s, pdl);
-      if (tmk3 && tmv3)  // one 3-D TMA box per block-head (half the TMA operations)
-        return nr1 ? launch_decode_kt<128, 1, 3, 4, true>(p, tmk3, tmv3, L, n, s, pdl)
-                   : launch_decode_kt<128, 2, 3, 2, true>(p, tmk3, tmv3, L, n, s, pdl);
-      return nr1 ? launch_decode_kt<128, 1, 3, 4>(p, tmk, tmv, L, n, s, pdl)
-                 : launch_decode_kt<128, 2, 3, 2>(p, tmk, tmv, L, n, s, pdl);
-    }
-    return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s, pdl)
-               : launch_decode_kt<64, 2, 4, 2>(p, tmk, tmv, L, n, s, pdl);
-  }
-  static const int pf = [] {
-    const char *e = getenv("KVA_DECODE_PF");
-    return e ? atoi(e) : 0;  // L2 prefetch measured counter-productive
-  }();
-  if (p.d == 128) {
-    if (pf <= 0) return launch_decode_t<128, 3, 0>(p, tmk, tmv, L, n, s);
-    if (pf <= 4) return launch_decode_t<128, 3, 4>(p, tmk, tmv, L, n, s);
-    if (pf <= 6) return launch_decode_t<128, 3, 6>(p, tmk, tmv, L, n, s);
-    return launch_decode_t<128, 3, 10>(p, tmk, tmv, L, n, s);
-  }
-  return launch_decode_t<64, 4, 6>(p, tmk, tmv, L, n, s);
+  int max_rows = 0;
+  const DecodeReq *reqs = L.ptr ? nullptr : L.req;
+  if (reqs)
+    for (int i = 0; i < L.n; ++i) max_rows = std::max(max_rows, reqs[i].n_tok * p.g);
+  else
+    max_rows = kDecodeRows;
+  const bool nr1 = max_rows <= 8;  // one 8-row MMA N tile
+  if (p.d == 128 && tmk3 && tmv3)  // one 3-D TMA box per block-head
+    return nr1 ? launch_decode_kt<128, 1, 3, 4, true>(p, tmk3, tmv3, L, n, s, pdl)
+               : launch_decode_kt<128, 2, 3, 2, true>(p, tmk3, tmv3, L, n, s, pdl);
+  if (p.d == 128) return cudaErrorInvalidValue;  // the pool always has the 3-D maps for d = 128
+  return nr1 ? launch_decode_kt<64, 1, 4, 2>(p, tmk, tmv, L, n, s, pdl)
+             : launch_decode_kt<64, 2, 4, 2>(p, tmk, tmv, L, n, s, pdl);
 }
 
 }  // namespace kva

@@ -630,29 +630,14 @@ cudaError_t launch_tile_tc2(const AttnParams &p, const void *tmk, const void *tm
                             const TileList &items, int max_ctas, cudaStream_t s, const void *tmv3,
                             const void *tmk3) {
   if (items.n <= 0) return cudaSuccess;
-  // KVA_POLY: column pairs (of 16) with exp2 on the FMA pipe: 0 (default), 4 or 6.  Measured
-  // (profiles/poly.sh): 0 is fastest — this softmax is issue/latency-bound, not MUFU-bound
-  // (llama7b tile 102 / 109 / 116 us, llama70b 962 / 887 / 856 TFLOP/s for 0 / 4 / 6).
-  static const int pp = [] {
-    const char *e = getenv("KVA_POLY");
-    return e ? atoi(e) : 0;
-  }();
+  // the exp2 of the softmax stays on MUFU (round 1: moving 4 or 6 of 16 column pairs to an FMA-pipe
+  // polynomial was slower, profiles/r01b/poly.log — this softmax is issue/latency-bound); K tiles by
+  // one 4-D box per block and V by one 3-D box for d = 128 (llama70b 7.35 -> 7.21 ms vs 2-D boxes)
   if (p.d == 128) {
-    // K tiles by one 4-D box per block (N = 128 QK over a 2 KB group stride; default):
-    // llama70b 7.35 -> 7.21 ms, qwen14b-p 2.36 -> 2.25 ms.  KVA_TILE_K3=0: 2-D boxes.
-    static const bool k3 = [] {
-      const char *e = getenv("KVA_TILE_K3");
-      return !(e && std::string(e) == "0");
-    }();
-    if (pp <= 0 && tmv3 && tmk3 && k3)
-      return launch_tile_tc2_t<128, 0, true, true>(p, tmk, tmv, items, max_ctas, s, tmv3, tmk3);
-    if (pp <= 0 && tmv3) return launch_tile_tc2_t<128, 0, true>(p, tmk, tmv, items, max_ctas, s, tmv3);
-    if (pp <= 0) return launch_tile_tc2_t<128, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
-    if (pp <= 4) return launch_tile_tc2_t<128, 4>(p, tmk, tmv, items, max_ctas, s, tmv3);
-    return launch_tile_tc2_t<128, 6>(p, tmk, tmv, items, max_ctas, s, tmv3);
+    if (!tmv3 || !tmk3) return cudaErrorInvalidValue;  // the pool always has them for d = 128
+    return launch_tile_tc2_t<128, 0, true, true>(p, tmk, tmv, items, max_ctas, s, tmv3, tmk3);
   }
-  if (pp <= 0) return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
-  return launch_tile_tc2_t<64, 4>(p, tmk, tmv, items, max_ctas, s, tmv3);
+  return launch_tile_tc2_t<64, 0>(p, tmk, tmv, items, max_ctas, s, tmv3);
 }
 
 }  // namespace kva

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -20,18 +21,13 @@
 using namespace kva;
 
 // ------------------------------------------------------------------------------------------
-// host-side section timer (diagnostics): KVA_HOST_PROF=1 accumulates steady-clock time per
-// labelled section and prints the per-call means at exit
+// host-side section timer (diagnostics): option "host_prof" = 1 accumulates steady-clock time
+// per labelled section and prints the per-call medians / means at exit
 // ------------------------------------------------------------------------------------------
 namespace {
 struct HostProf {
-  bool on = false;
   std::mutex mu;
   std::vector<std::pair<std::string, std::vector<double>>> acc;
-  HostProf() {
-    const char *e = getenv("KVA_HOST_PROF");
-    on = e && e[0] == '1';
-  }
   void add(const char *name, double us) {
     std::lock_guard<std::mutex> g(mu);
     for (auto &a : acc)
@@ -42,7 +38,7 @@ struct HostProf {
     acc.push_back({name, {us}});
   }
   ~HostProf() {  // median and mean per label (first calls include lazy module loading)
-    if (!on) return;
+    if (acc.empty()) return;
     for (auto &a : acc) {
       std::vector<double> v = a.second;
       std::sort(v.begin(), v.end());
@@ -57,7 +53,7 @@ HostProf g_hprof;
 struct HSection {  // HSection t; ... t.lap("label");
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   void lap(const char *name) {
-    if (!g_hprof.on) return;
+    if (!opt(kOptHostProf)) return;
     const auto n = std::chrono::steady_clock::now();
     g_hprof.add(name, std::chrono::duration<double, std::micro>(n - t).count());
     t = n;
@@ -122,7 +118,36 @@ int sm_count() {
   if (dev >= 0 && dev < 64) cached[dev] = n;
   return n;
 }
+namespace {
+struct OptDef {
+  const char *name;
+  int64_t def;
+};
+// defaults = the measured best
+constexpr OptDef kOptDefs[kOptCount] = {{"tile_ctas", 0}, {"overlap", 1}, {"pdl", 1},   {"evict_ctas", 0},
+                                        {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0}};
+std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}};
+int opt_index(const char *name) {
+  if (!name) return -1;
+  for (int i = 0; i < kOptCount; ++i)
+    if (std::strcmp(kOptDefs[i].name, name) == 0) return i;
+  return -1;
+}
+}  // namespace
+int64_t opt(Opt o) { return g_opt[o].load(std::memory_order_relaxed); }
 }  // namespace kva
+extern "C" kva_status kva_set_option(const char *name, int64_t value) {
+  const int i = kva::opt_index(name);
+  if (i < 0) return fail(KVA_ERR_INVALID, "unknown option '%s'", name ? name : "(null)");
+  kva::g_opt[i].store(value, std::memory_order_relaxed);
+  return KVA_OK;
+}
+extern "C" kva_status kva_get_option(const char *name, int64_t *value) {
+  const int i = kva::opt_index(name);
+  if (i < 0 || !value) return fail(KVA_ERR_INVALID, "unknown option '%s' or null value", name ? name : "(null)");
+  *value = kva::g_opt[i].load(std::memory_order_relaxed);
+  return KVA_OK;
+}
 extern "C" const char *kva_version(void) {
   return "kvattn 0.1 (sm_100a; decode split-KV TMA+mma.sync, tile attention, radix top-k)";
 }
@@ -339,14 +364,11 @@ extern "C" kva_status kv_pool_create(const kva_pool_desc *d, kva_pool **out) {
   const int64_t rows = (int64_t)d->num_blocks * d->num_kv_heads * kBlock;
   kva_status st = make_pool_map(&p->tmk, d->k_pool, rows, d->head_dim);
   if (st == KVA_OK) st = make_pool_map(&p->tmv, d->v_pool, rows, d->head_dim);
-  if (st == KVA_OK && d->head_dim == 128) {
-    const char *e3 = getenv("KVA_TMA3D");  // KVA_TMA3D=0: 2-D boxes only (cross-check)
-    if (!(e3 && std::string(e3) == "0")) {
-      st = make_pool_map_3d(&p->tmk3, d->k_pool, rows, d->head_dim);
-      if (st == KVA_OK) st = make_pool_map_4d(&p->tmk4, d->k_pool, rows, d->head_dim);
-      if (st == KVA_OK) st = make_pool_map_3d(&p->tmv3, d->v_pool, rows, d->head_dim);
-      p->has3d = st == KVA_OK;
-    }
+  if (st == KVA_OK && d->head_dim == 128) {  // one box per block-head (d = 128 kernels)
+    st = make_pool_map_3d(&p->tmk3, d->k_pool, rows, d->head_dim);
+    if (st == KVA_OK) st = make_pool_map_4d(&p->tmk4, d->k_pool, rows, d->head_dim);
+    if (st == KVA_OK) st = make_pool_map_3d(&p->tmv3, d->v_pool, rows, d->head_dim);
+    p->has3d = st == KVA_OK;
   }
   if (st != KVA_OK) {
     delete p;
@@ -678,7 +700,6 @@ struct kva_plan {
   bool has3d = false;
   ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
   ReqList<MergeReq> mrg;                   // merged requests (idem)
-  const TileItem *d_tile = nullptr;
   TileList tiles;                          // tcgen05 tile items (inline kernel parameter or uploaded)
   int n_dec = 0, n_tile = 0, n_mrows = 0;  // work units: decode (split, head), tiles, merge (row, head)
   // the plan arrays are uploaded on the pool's side stream (ordered after `stream`'s prior work
@@ -688,8 +709,6 @@ struct kva_plan {
   bool uploaded = false;
   kva_pool *pool = nullptr;  // for the side-stream append event (the pool outlives its plans)
   int device = 0;
-  bool tile_tc = true;
-  int tile_impl = 2;
   int tile_ctas = 0;              // persistent tile-kernel grid (0 = all SMs)
   bool overlap = true;            // tile kernel on the side stream, concurrent with decode
   cudaStream_t aux = nullptr;
@@ -711,30 +730,8 @@ struct PlanBuild {
   kva_plan_stats stats{};
 };
 
-// Tile kernel: tcgen05/TMEM (128-row tiles, default) or the legacy mma.sync kernel (64-row
-// tiles) kept as an independent cross-check (KVA_TILE_IMPL=mma).
-// 0 = legacy mma.sync (64-row tiles), 1 = tcgen05 one-Q-tile (128 rows), 2 = tcgen05
-// two-Q-tile (256 rows, default).  KVA_TILE_IMPL=mma|tc1|tc2 selects one (cross-checks).
-static int tile_impl() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("KVA_TILE_IMPL");
-    const std::string s = e ? e : "";
-    v = s == "mma" ? 0 : s == "tc1" ? 1 : s == "tc3" ? 3 : 2;
-  }
-  return v;
-}
-static bool tile_use_tc() { return tile_impl() != 0; }
-
-// effective implementation for a descriptor (the CTA-pair kernel is head_dim 128 only)
-static int tile_impl_for(const kva_batch_desc *b) {
-  const int v = tile_impl();
-  return (v == 3 && b->head_dim != 128) ? 2 : v;
-}
-
 static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
-  const int impl = tile_impl_for(b);
-  const int kTileM = impl == 3 ? 4 * kTileMTc : impl == 2 ? 2 * kTileMTc : impl == 1 ? kTileMTc : kTileMMma;
+  const int kTileM = 2 * kTileMTc;  // rows per tile item: the tcgen05 kernel's two Q tiles
   const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
   const int d = b->head_dim;
   const int G = b->group_of ? std::max(b->num_groups, 0) : 0;
@@ -970,8 +967,7 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     std::copy(pb.mrg.begin(), pb.mrg.end(), pl->mrg.req);
     std::copy(pb.mrg_pre.begin(), pb.mrg_pre.end(), pl->mrg.pre);
   }
-  const int impl = tile_impl_for(b);
-  const bool tile_inline = impl == 2 && pb.tile.size() <= (size_t)kInlineTiles;
+  const bool tile_inline = pb.tile.size() <= (size_t)kInlineTiles;
   pl->tiles.n = (int32_t)pb.tile.size();
   pl->tiles.ptr = nullptr;
   if (tile_inline) std::copy(pb.tile.begin(), pb.tile.end(), pl->tiles.item);
@@ -993,8 +989,8 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
       off += align256(std::max<size_t>(n, 4));
       return dws + o;
     };
-    pl->d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), tile_inline ? 0 : sizeof(TileItem) * pb.tile.size()));
-    if (!tile_inline) pl->tiles.ptr = pl->d_tile;
+    const TileItem *d_tile = reinterpret_cast<const TileItem *>(put(pb.tile.data(), tile_inline ? 0 : sizeof(TileItem) * pb.tile.size()));
+    if (!tile_inline) pl->tiles.ptr = d_tile;
     pl->p.row_list = reinterpret_cast<const int32_t *>(put(pb.row_list.data(), 4 * pb.row_list.size()));
     if (!dec_inline) {
       pl->dec.ptr = reinterpret_cast<const DecodeReq *>(put(pb.dec.data(), sizeof(DecodeReq) * pb.dec.size()));
@@ -1020,8 +1016,6 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
     pl->uploaded = true;
   }
   hs.lap("plan.upload");
-  pl->tile_tc = tile_use_tc();
-  pl->tile_impl = tile_impl_for(b);
   pl->aux = p->aux;
   pl->pool = p;
   pl->ev_fork = p->ev_fork;
@@ -1029,15 +1023,14 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->desc.device);
-    const char *e = getenv("KVA_TILE_CTAS");
-    const char *o = getenv("KVA_OVERLAP");
-    pl->overlap = !(o && std::string(o) == "0");
+    const int64_t tc_opt = opt(kOptTileCtas);
+    pl->overlap = opt(kOptOverlap) != 0;
     // standalone time estimates from measured rates: ~3.9 TFLOP/s per SM for
     // the tcgen05 tile kernel, 6.7 TB/s for the decode stream
     const double t_tile = (double)pb.tile_flops / (nsm * 3.9e12);
     const double t_dec = (double)pb.stats.decode_kv_bytes / 6.7e12;
-    if (e) {
-      pl->tile_ctas = atoi(e);
+    if (tc_opt > 0) {
+      pl->tile_ctas = (int)std::min<int64_t>(tc_opt, nsm);
     } else if (pb.dec.empty() || pb.tile.empty() || !pl->overlap || t_tile > 1.5 * t_dec) {
       // tile-dominated batches (e.g. 8k chunks): run the tile kernel on every SM, then decode
       pl->overlap = false;
@@ -1116,12 +1109,11 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.lse = lse;
   p.dbg = nullptr;
   p.span = pl->span;
-  p.debug_flags = 0;
-  if (const char *e = getenv("KVA_DEBUG_FLAGS")) p.debug_flags = atoi(e);
-  if (const char *e = getenv("KVA_DEBUG_TS")) p.dbg = reinterpret_cast<unsigned long long *>(strtoull(e, nullptr, 0));
+  p.debug_flags = (int32_t)opt(kOptDebugFlags);
+  if (const int64_t ts_addr = opt(kOptDebugTs)) p.dbg = reinterpret_cast<unsigned long long *>(ts_addr);
   const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
   const bool do_dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
-  const bool fork = do_tile && do_dec && pl->overlap && pl->tile_tc;
+  const bool fork = do_tile && do_dec && pl->overlap;
   cudaStream_t ts = s;
   if (fork) {  // tile kernel first on the high-priority side stream, then decode on `s`
     CUDA_TRY(cudaEventRecord(pl->ev_fork, s));
@@ -1143,15 +1135,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (ts == s && wait_upload(true) != KVA_OK) return KVA_ERR_CUDA;
     if (ts == s && wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], ts));
-    if (pl->tile_impl == 3) CUDA_TRY(launch_tile_tc3(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
-                                                     fork ? pl->tile_ctas : 0, ts));
-    else if (pl->tile_impl == 2) CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles,
-                                                          fork ? pl->tile_ctas : 0, ts,
-                                                          pl->has3d ? &pl->tmv3 : nullptr,
-                                                          pl->has3d ? &pl->tmk4 : nullptr));
-    else if (pl->tile_tc) CUDA_TRY(launch_tile_tc(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile,
-                                                  fork ? pl->tile_ctas : 0, ts));
-    else CUDA_TRY(launch_tile(p, &pl->tmk, &pl->tmv, pl->d_tile, pl->n_tile, ts));
+    CUDA_TRY(launch_tile_tc2(p, &pl->tmk, &pl->tmv, pl->tiles, fork ? pl->tile_ctas : 0, ts,
+                             pl->has3d ? &pl->tmv3 : nullptr, pl->has3d ? &pl->tmk4 : nullptr));
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], ts));
     return KVA_OK;
   };
@@ -1171,11 +1156,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   // the decode kernel (programmatic dependent launch) start on the remaining SMs.  This fixes
   // the SM split: with two streams the decode kernel's 2-CTA/SM grid could be dispatched first
   // and hold every SM until its first wave retired.  Timing events bracket the pair.
-  static const bool pdl_mode = [] {
-    const char *e = getenv("KVA_PDL");
-    return !(e && std::string(e) == "0");
-  }();
-  if (fork && pdl_mode && pl->tile_impl == 2) {
+  const bool pdl_mode = opt(kOptPdl) != 0;
+  if (fork && pdl_mode) {
     if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
     if (pl->t_ev[2]) CUDA_TRY(cudaEventRecord(pl->t_ev[2], s));
@@ -1490,7 +1472,7 @@ extern "C" kva_status evict_select(const uint64_t *keys, int64_t n, int64_t k, i
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t *w = static_cast<uint8_t *>(ws);
   int64_t *d_count = reinterpret_cast<int64_t *>(w);
-  static const int ctas = [] { const char *e = getenv("KVA_EVICT_CTAS"); return e ? atoi(e) : 0; }();
+  const int ctas = (int)opt(kOptEvictCtas);
   CUDA_TRY(launch_evict_select(keys, n, k, out_ids, d_count, apply ? pool->desc.free_bits : nullptr, w + 256,
                                ws_bytes - 256, ctas, s));
   if (!n_selected) return KVA_OK;  // asynchronous mode: count stays on the device

@@ -77,7 +77,8 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
            "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step",
            "kva_prefix_index_create", "kva_prefix_index_destroy", "kva_prefix_insert", "kva_prefix_lookup",
-           "kva_prefix_remove", "kva_prefix_size", "kva_group_batch", "kva_group_batch_nested"]
+           "kva_prefix_remove", "kva_prefix_size", "kva_group_batch", "kva_group_batch_nested",
+           "kva_set_option", "kva_get_option"]
 PHASE_TILE, PHASE_DECODE, PHASE_MERGE, PHASE_ALL = 1, 2, 4, 7
 
 _lib = None
@@ -137,6 +138,8 @@ def load(build_if_missing: bool = True):
         "kva_prefix_size": ([P, P], ctypes.c_int),
         "kva_group_batch": ([P, i32, P, P, P, i32, P, P, P], ctypes.c_int),
         "kva_group_batch_nested": ([P, i32, P, P, P, i32, P, P, P, P, P], ctypes.c_int),
+        "kva_set_option": ([ctypes.c_char_p, i64], ctypes.c_int),
+        "kva_get_option": ([ctypes.c_char_p, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -511,6 +514,34 @@ def evict_select(keys: torch.Tensor, k: int, out_ids: torch.Tensor | None = None
         return out_ids[: nsel.value], nsel.value
     _check(st)
     return out_ids[: nsel.value], nsel.value
+
+
+def set_option(name: str, value: int):
+    """kva_set_option (include/kvattn.h): process-wide tuning / diagnostics option."""
+    _check(load().kva_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    _check(load().kva_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: `with options(tile_ctas=40, overlap=1): ...` restores the old values."""
+
+    def __init__(self, **kw):
+        self.kw, self.old = kw, {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
 
 
 def free_bits_tensor(free_bits_np: np.ndarray, device) -> torch.Tensor:

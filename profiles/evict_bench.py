@@ -1,7 +1,7 @@
 """evict_select alone on the `evict` config (2^20 keys, top-64k) and its straddle variant:
 CUDA-event time per call (keys L2-resident from the previous call, as in the serving step),
-phase timestamps of CTA 0, for a list of cooperative grid sizes (KVA_EVICT_CTAS is read once
-per process, so each size runs in its own process).
+phase timestamps of CTA 0, for a list of cooperative grid sizes (option evict_ctas; each size
+in its own process).
 
 usage: python profiles/evict_bench.py [ctas ...]
 """
@@ -16,6 +16,7 @@ CHILD = r"""
 import json, sys, numpy as np, torch
 sys.path.insert(0, %r)
 import workloads as W, paper_2504_03651_b200 as K
+K.set_option("evict_ctas", int(sys.argv[1]))
 dev = torch.device("cuda", 0)
 res = {}
 for straddle in (False, True):
@@ -63,10 +64,7 @@ print("RESULT " + json.dumps(res))
 def main():
     sizes = sys.argv[1:] or ["0"]
     for c in sizes:
-        env = dict(os.environ)
-        if c != "0":
-            env["KVA_EVICT_CTAS"] = c
-        r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=900)
+        r = subprocess.run([sys.executable, "-c", CHILD, c], capture_output=True, text=True, timeout=900)
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")]
         if r.returncode != 0 or not line:
             print(json.dumps({"ctas": c, "error": (r.stdout + r.stderr)[-3000:]}))
