@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--config", default="llama7b")
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--evict-thread", type=int, default=0,
+                    help="1: the KV manager's per-step calls (kv_manager_step + evict_select) are "
+                         "enqueued by a second host thread, concurrently with the attention calls")
     ap.add_argument("--l2-rotate", type=int, default=4,
                     help="replicas of every per-step input (pool, tables, Q/K/V, manager metadata) "
                          "cycled step by step so no step finds the previous one's data in L2 (1 = off)")
@@ -280,6 +283,39 @@ def run_ours(args, rank, world, local):
     fork_next = {"v": True}
     gather_on = {"v": True}
 
+    # The KV manager's per-step enqueue on its own host thread (a serving engine's scheduler /
+    # KV-manager bookkeeping runs beside the model runner): the main thread hands it the step's
+    # replica and waits for "enqueued" only right before ordering the step's end after the
+    # selection (ev_join).  ctypes releases the GIL inside the library calls.
+    import queue
+    jobs, done = queue.SimpleQueue(), queue.SimpleQueue()
+
+    def evict_enqueue(ev, fork):
+        if fork:
+            ev_stream.wait_event(ev_fork)
+        keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
+                         stream=ev_stream)
+        ev_keys.record(ev_stream)
+        K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream, sync=False)
+        ev_join.record(ev_stream)
+
+    def evict_worker():
+        torch.cuda.set_device(dev)
+        while True:
+            job = jobs.get()
+            if job is None:
+                return
+            try:
+                evict_enqueue(*job)
+                done.put(None)
+            except BaseException as exc:  # surfaced on the main thread
+                done.put(exc)
+
+    threaded = bool(args.evict_thread) and ev is not None
+    if threaded:
+        worker = threading.Thread(target=evict_worker, daemon=True)
+        worker.start()
+
     def step(time_idx=None):
         rp = reps[rot["i"] % R] if rot["on"] else reps[0]
         rot["i"] += 1
@@ -289,18 +325,16 @@ def run_ours(args, rank, world, local):
         if ev is not None:
             # the manager's eviction selection has no data dependency on this layer's attention:
             # it runs on its own stream, concurrently (its CTAs leave room for decode CTAs)
-            if fork_next["v"] or not evict_pipeline:
+            fork = fork_next["v"] or not evict_pipeline
+            if fork:
                 ev_fork.record(stream)
-                ev_stream.wait_event(ev_fork)
                 fork_next["v"] = False
-            keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
-                             stream=ev_stream)
-            ev_keys.record(ev_stream)
-            K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
-                           sync=False)
-            ev_join.record(ev_stream)
-            n += 3
-        if ev is not None and gate_attn:  # before the append: the attention pair follows it directly
+            if threaded:
+                jobs.put((ev, fork))
+            else:
+                evict_enqueue(ev, fork)
+            n += 2
+        if ev is not None and gate_attn and not threaded:  # the attention pair follows the key pass
             stream.wait_event(ev_keys)
         K.kv_append(pool, batch, rp["k_new"], rp["v_new"], rp["ws_app"], stream=stream)
         plan = K.Plan(pool, batch, rp["ws_att"], stream=stream)
@@ -314,6 +348,10 @@ def run_ours(args, rank, world, local):
         if world > 1 and gather_on["v"]:
             kdist.gather_outputs(out, gbuf)
         if ev is not None:
+            if threaded:
+                exc = done.get()
+                if exc is not None:
+                    raise exc
             stream.wait_event(ev_join)
         K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
@@ -374,21 +412,19 @@ def run_ours(args, rank, world, local):
             b["v"].copy_(h_v, non_blocking=True)
             ev_in[i % 2].record(cs_in)
         if ev is not None:
-            if fork_next["v"] or not evict_pipeline:
+            fork = fork_next["v"] or not evict_pipeline
+            if fork:
                 ev_fork.record(stream)
-                ev_stream.wait_event(ev_fork)
                 fork_next["v"] = False
-            keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
-                             stream=ev_stream)
-            ev_keys.record(ev_stream)
-            K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream,
-                           sync=False)
-            ev_join.record(ev_stream)
-            n += 3
+            if threaded:
+                jobs.put((ev, fork))
+            else:
+                evict_enqueue(ev, fork)
+            n += 2
         stream.wait_event(ev_in[i % 2])
         if i >= 2:
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done
-        if ev is not None and gate_attn:
+        if ev is not None and gate_attn and not threaded:
             stream.wait_event(ev_keys)
         K.kv_append(pool, batch, b["k"], b["v"], ws_app, stream=stream)
         plan = K.Plan(pool, batch, ws_att, stream=stream)
@@ -406,6 +442,10 @@ def run_ours(args, rank, world, local):
             h_out.copy_(res_t, non_blocking=True)
             ev_out[i % 2].record(cs_out)
         if ev is not None:
+            if threaded:
+                exc = done.get()
+                if exc is not None:
+                    raise exc
             stream.wait_event(ev_join)
         K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
@@ -574,7 +614,10 @@ def run_ours(args, rank, world, local):
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
-                   "overlap": "tile (tcgen05) on a side stream concurrent with decode; eviction selection on a third stream concurrent with the attention"},
+                   "overlap": "tile (tcgen05) kernel and decode kernel concurrent (programmatic dependent launch); "
+                              "KV-manager pass + eviction selection on a second stream concurrent with the attention"
+                              + (", enqueued by a second host thread" if threaded else ""),
+                   "host_threads": 2 if threaded else 1},
         "roofline": {"bound": "hbm", "kernel": "decode_kt_kernel (split-KV)", "achieved": achieved,
                      "timing": "in-kernel %globaltimer span per timed step (first CTA start -> last CTA end)",
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,

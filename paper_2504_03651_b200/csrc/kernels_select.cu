@@ -36,7 +36,11 @@ namespace cg = cooperative_groups;
 namespace kva {
 namespace {
 
-constexpr int kT = 512;              // threads per CTA
+#ifndef KVA_SEL_THREADS
+#define KVA_SEL_THREADS 512
+#endif
+constexpr int kT = KVA_SEL_THREADS;  // threads per CTA
+constexpr int kPer = (1 << 11) / kT;  // histogram bins per thread in the scans
 constexpr int kNW = kT / 32;
 constexpr int kDig = 11;             // radix digit bits
 constexpr int kBins = 1 << kDig;
@@ -159,6 +163,56 @@ __device__ __forceinline__ unsigned bin_claim(unsigned *cur, int d) {
   base = __shfl_sync(0xffffffffu, base, leader);
   if (d == d0) return base + __popc(same & lanemask_lt());
   return d >= 0 ? atomicAdd(&cur[d], 1u) : 0u;
+}
+
+// Batched forms for NK keys per lane (the input passes): the lanes' keys that share the
+// warp's dominant digit (the first valid one; neighbouring blocks of a chain share their
+// class and LAT) are counted / claimed with ONE shared atomic for all NK keys — the hot bin
+// otherwise takes one same-address atomic per warp per key, serialised across the CTA's warps.
+template <int NK>
+__device__ __forceinline__ int dominant(const int (&d)[NK]) {
+  int D = -1;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const unsigned v = __ballot_sync(0xffffffffu, d[k] >= 0);
+    if (D < 0 && v) D = __shfl_sync(0xffffffffu, d[k], __ffs(v) - 1);
+  }
+  return D;
+}
+template <int NK>
+__device__ __forceinline__ void hist_batch(unsigned *h, const int (&d)[NK]) {
+  const int D = dominant(d);
+  if (D < 0) return;
+  unsigned tot = 0;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) tot += __popc(__ballot_sync(0xffffffffu, d[k] == D));
+  if ((threadIdx.x & 31) == 0) atomicAdd(&h[D], tot);
+#pragma unroll
+  for (int k = 0; k < NK; ++k)
+    if (d[k] >= 0 && d[k] != D) atomicAdd(&h[d[k]], 1u);
+}
+template <int NK>
+__device__ __forceinline__ void claim_batch(unsigned *cur, const int (&d)[NK], unsigned (&pos)[NK]) {
+  const int D = dominant(d);
+  if (D < 0) return;
+  unsigned same[NK], tot = 0;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    same[k] = __ballot_sync(0xffffffffu, d[k] == D);
+    tot += __popc(same[k]);
+  }
+  unsigned base = 0;
+  if ((threadIdx.x & 31) == 0) base = atomicAdd(&cur[D], tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    if (d[k] == D) pos[k] = base + __popc(same[k] & lt);
+    base += __popc(same[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < NK; ++k)
+    if (d[k] >= 0 && d[k] != D) pos[k] = atomicAdd(&cur[d[k]], 1u);
 }
 
 // Add this CTA's bin counts to the grid's (global) counts; s_off[d] = this CTA's offset in bin d.
@@ -309,7 +363,10 @@ __device__ __forceinline__ void sort_bucket(const SelArgs &a, const uint64_t *sk
   }
 }
 
-__global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_constant__ SelArgs a) {
+#ifndef KVA_SEL_MAXREG
+#define KVA_SEL_MAXREG 80  // measured: 1M keys alone 70 us (74 CTAs), co-runs with the attention
+#endif
+__global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_constant__ SelArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ __align__(16) unsigned char s_buf[kCap * 12];  // 24 KB: two bin arrays | a sort buffer
   __shared__ unsigned s_w[kNW];
@@ -336,32 +393,49 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
   const bool vec = (reinterpret_cast<uintptr_t>(a.keys) & 15) == 0;
 
   // Walk this CTA's slice of the input keys: f(key, id), 2 x 4 keys in flight per thread.
+  // Walk this CTA's slice of the input keys, 4 keys per lane per call: f(key[4], id[4]) (kInf =
+  // no key); a 4-deep register pipeline of 16-B loads (2 per call)
   auto for_slice = [&](auto &&f) {
+    uint64_t k4[4];
+    int32_t i4[4];
     if (vec) {
       const int64_t v0 = lo >> 1, v1 = hi >> 1;  // lo even
       const uint4 *src = reinterpret_cast<const uint4 *>(a.keys);
-      // 4-deep register pipeline of 16-B loads; the body (f) appears twice in the code
       auto ld = [&](int64_t i) { return i < v1 ? __ldcg(src + i) : make_uint4(~0u, ~0u, ~0u, ~0u); };
       uint4 q0 = ld(v0 + tid), q1 = ld(v0 + kT + tid), q2 = ld(v0 + 2 * kT + tid), q3 = ld(v0 + 3 * kT + tid);
 #pragma unroll 1
-      for (int64_t b = v0; b < v1; b += kT) {
-        const uint4 v = q0;
-        q0 = q1;
-        q1 = q2;
-        q2 = q3;
-        q3 = ld(b + 4 * kT + tid);
-        const int64_t i = b + tid;
-        f(((uint64_t)v.y << 32) | v.x, (int32_t)(2 * i));
-        f(((uint64_t)v.w << 32) | v.z, (int32_t)(2 * i + 1));
+      for (int64_t b = v0; b < v1; b += 2 * kT) {
+        const uint4 x = q0, y = q1;
+        q0 = q2;
+        q1 = q3;
+        q2 = ld(b + 4 * kT + tid);
+        q3 = ld(b + 5 * kT + tid);
+        const int64_t i = b + tid, j = b + kT + tid;
+        k4[0] = ((uint64_t)x.y << 32) | x.x;
+        k4[1] = ((uint64_t)x.w << 32) | x.z;
+        k4[2] = ((uint64_t)y.y << 32) | y.x;
+        k4[3] = ((uint64_t)y.w << 32) | y.z;
+        i4[0] = (int32_t)(2 * i);
+        i4[1] = (int32_t)(2 * i + 1);
+        i4[2] = (int32_t)(2 * j);
+        i4[3] = (int32_t)(2 * j + 1);
+        f(k4, i4);
       }
       if ((hi & 1) && hi > lo) {  // odd tail of the last slice: thread 0 of a full warp pass
-        const uint64_t kk = tid == 0 ? a.keys[hi - 1] : kInf;
-        f(kk, (int32_t)(hi - 1));
+        k4[0] = tid == 0 ? a.keys[hi - 1] : kInf;
+        k4[1] = k4[2] = k4[3] = kInf;
+        i4[0] = i4[1] = i4[2] = i4[3] = (int32_t)(hi - 1);
+        f(k4, i4);
       }
     } else {
-      for (int64_t b = lo; b < hi; b += kT) {
-        const int64_t i = b + tid;
-        f(i < hi ? a.keys[i] : kInf, (int32_t)i);
+      for (int64_t b = lo; b < hi; b += 4 * kT) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = b + u * kT + tid;
+          k4[u] = i < hi ? a.keys[i] : kInf;
+          i4[u] = (int32_t)i;
+        }
+        f(k4, i4);
       }
     }
   };
@@ -369,12 +443,14 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
   // ---------------- phase 0: which bits vary among the evictable keys, how many ----------------
   {
     unsigned long long o = 0, an = 0, cn = 0;
-    for_slice([&](uint64_t key, int32_t) {
-      if (key != kInf) {
-        o |= key;
-        an |= ~key;
-        ++cn;
-      }
+    for_slice([&](const uint64_t (&k4)[4], const int32_t (&)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k4[u] != kInf) {
+          o |= k4[u];
+          an |= ~k4[u];
+          ++cn;
+        }
     });
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
@@ -471,7 +547,12 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
     const DigSel ds0 = dig_sel(cp, 0);
     __syncthreads();
     stamp();
-    for_slice([&](uint64_t key, int32_t id) { hist_add(s_cnt, key != kInf ? digit(ds0, compress(cr, key), id) : -1); });
+    for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
+      int d4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d4[u] = k4[u] != kInf ? digit(ds0, compress(cr, k4[u]), i4[u]) : -1;
+      hist_batch<4>(s_cnt, d4);
+    });
     __syncthreads();
     stamp();
     flush_counts(s_cnt, s_off, a.hist);
@@ -494,22 +575,22 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
       unsigned *Hz = a.hist + ((r + 2) % 3) * kBins;
       for (int i = c * kT + tid; i < kBins; i += C * kT) Hz[i] = 0u;
     }
-    unsigned h[4], ex[4];
+    unsigned h[kPer], ex[kPer];
     unsigned sum = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      h[u] = __ldcg(Hr + 4 * tid + u);
+    for (int u = 0; u < kPer; ++u) {
+      h[u] = __ldcg(Hr + kPer * tid + u);
       sum += h[u];
     }
     unsigned tot;
     unsigned run = block_scan(sum, s_w, tot);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { ex[u] = run; run += h[u]; }
+    for (int u = 0; u < kPer; ++u) { ex[u] = run; run += h[u]; }
     if (!full) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kPer; ++u)
         if ((unsigned long long)ex[u] < need && need <= (unsigned long long)ex[u] + h[u]) {
-          s_bnd[0] = 4 * tid + u;
+          s_bnd[0] = kPer * tid + u;
           s_bnd[1] = ex[u];
           s_bnd[2] = h[u];
         }
@@ -538,8 +619,8 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
     // singleton bin, emitted directly); the next segment -> wk/wi from 0
     unsigned nrec = 0;  // this thread's level-0 bucket records: small count | large count << 16
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int d = 4 * tid + u;
+    for (int u = 0; u < kPer; ++u) {
+      const int d = kPer * tid + u;
       const bool tk = d < sure_end || (fin && d == b);
       if (tk) s_off[d] += (out_base + ex[u]) | (h[u] == 1u && d < sure_end ? 0x80000000u : 0u);
       if (tk && h[u] >= 2u) nrec += h[u] <= (unsigned)kWarpMax ? 1u : 0x10000u;
@@ -549,8 +630,8 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
       unsigned at = block_scan(nrec, s_w, tot_rec);
       unsigned at_s = rec_small + (at & 0xFFFFu), at_l = rec_large + (at >> 16);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int d = 4 * tid + u;
+      for (int u = 0; u < kPer; ++u) {
+        const int d = kPer * tid + u;
         if ((d < sure_end || (fin && d == b)) && h[u] >= 2u) {
           const unsigned take = d < sure_end ? h[u] : (unsigned)need_b;
           const uint4 rec = make_uint4(out_base + ex[u], h[u], take, (unsigned)(r + 1));
@@ -575,24 +656,35 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
     stamp();
     const int wsrc = r & 1, wdst = (r + 1) & 1;
     const DigSel dsr = dig_sel(cp, r), dsn = dig_sel(cp, r + 1);
-    auto place = [&](uint64_t key, int32_t id, bool valid) {  // key: compressed
-      int d = valid ? digit(dsr, key, id) : -1;
-      const bool taken = d >= 0 && (d < sure_end || (fin && d == b));
-      const bool seg = nxt && d == b;
-      if (!taken && !seg) d = -1;
-      const unsigned pos = bin_claim(s_off, d);
-      if (taken) {
-        if (pos & 0x80000000u) {
-          emit(a, pos & 0x7FFFFFFFu, id);
-        } else {
-          a.sk[0][pos] = key;
-          a.si[0][pos] = id;
-        }
-      } else if (seg) {
-        a.wk[wdst][pos] = key;
-        a.wi[wdst][pos] = id;
+    // NK (compressed key, id) pairs per lane: digit, category, batched position claim, store,
+    // and the next segment's digit-(r+1) count
+    auto place = [&](auto nkc, const uint64_t *key, const int32_t *id, const bool *valid) {
+      constexpr int NK = decltype(nkc)::value;
+      int d[NK], dn[NK];
+      unsigned pos[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        d[k] = valid[k] ? digit(dsr, key[k], id[k]) : -1;
+        const bool taken = d[k] >= 0 && (d[k] < sure_end || (fin && d[k] == b));
+        const bool seg = nxt && d[k] == b;
+        if (!taken && !seg) d[k] = -1;
+        dn[k] = seg && d[k] >= 0 ? digit(dsn, key[k], id[k]) : -1;
       }
-      hist_add(s_cnt, seg ? digit(dsn, key, id) : -1);
+      claim_batch<NK>(s_off, d, pos);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        if (d[k] < 0) continue;
+        if (nxt && d[k] == b) {
+          a.wk[wdst][pos[k]] = key[k];
+          a.wi[wdst][pos[k]] = id[k];
+        } else if (pos[k] & 0x80000000u) {
+          emit(a, pos[k] & 0x7FFFFFFFu, id[k]);
+        } else {
+          a.sk[0][pos[k]] = key[k];
+          a.si[0][pos[k]] = id[k];
+        }
+      }
+      hist_batch<NK>(s_cnt, dn);
     };
     if (r == 0) {
       // keys above bin b are dropped before compressing: digit > b <=> key >= t_hi (compress is
@@ -608,9 +700,15 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
           t_hi = t;
         }
       }
-      for_slice([&](uint64_t key, int32_t id) {
-        const bool v = key < t_hi;  // also excludes kInf
-        place(v ? compress(cr, key) : 0ull, id, v);
+      for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
+        uint64_t c4[4];
+        bool v4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v4[u] = k4[u] < t_hi;  // also excludes kInf
+          c4[u] = v4[u] ? compress(cr, k4[u]) : 0ull;
+        }
+        place(std::integral_constant<int, 4>{}, c4, i4, v4);
       });
     } else {
       const uint64_t *xk = a.wk[wsrc];
@@ -618,10 +716,10 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
       for (unsigned base = 0; base < m_cnt; base += 2 * kT) {
         const unsigned i0 = base + tid, i1 = base + kT + tid;
         const bool v0 = i0 < m_cnt, v1 = i1 < m_cnt;
-        const uint64_t k0 = v0 ? __ldcg(xk + m_lo + i0) : kInf, k1 = v1 ? __ldcg(xk + m_lo + i1) : kInf;
-        const int32_t d0 = v0 ? __ldcg(xi + m_lo + i0) : 0, d1 = v1 ? __ldcg(xi + m_lo + i1) : 0;
-        place(k0, d0, v0);
-        place(k1, d1, v1);
+        const uint64_t k2[2] = {v0 ? __ldcg(xk + m_lo + i0) : kInf, v1 ? __ldcg(xk + m_lo + i1) : kInf};
+        const int32_t d2[2] = {v0 ? __ldcg(xi + m_lo + i0) : 0, v1 ? __ldcg(xi + m_lo + i1) : 0};
+        const bool b2[2] = {v0, v1};
+        place(std::integral_constant<int, 2>{}, k2, d2, b2);
       }
     }
     stamp();
@@ -654,9 +752,13 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
       const uint64_t *xk = a.sk[src];
       const int32_t *xi = a.si[src];
       if (size <= (unsigned)kCap) {  // the CTA: registers + shared-memory exchanges
-        if (size <= (unsigned)kT) sort_bucket<1, kT>(a, xk, xi, off, size, take, sbk, sbi);
-        else if (size <= 2u * kT) sort_bucket<2, kT>(a, xk, xi, off, size, take, sbk, sbi);
-        else sort_bucket<4, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        if (size <= (unsigned)kT) {
+          sort_bucket<1, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        } else if (size <= 2u * kT) {
+          sort_bucket<2, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        } else {
+          if constexpr (kCap > 2 * kT) sort_bucket<kCap / kT, kT>(a, xk, xi, off, size, take, sbk, sbi);
+        }
         __syncthreads();
       } else {  // partition by the next digit into the other staging buffer -> next level
         uint64_t *yk = a.sk[src ^ 1];
@@ -669,14 +771,14 @@ __global__ void __launch_bounds__(kT, 2) evict_select_kernel(const __grid_consta
           hist_add(s_cnt, i < size ? digit(dsp, __ldcg(xk + off + i), __ldcg(xi + off + i)) : -1);
         }
         __syncthreads();
-        unsigned hh[4], sm = 0;
+        unsigned hh[kPer], sm = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { hh[u] = s_cnt[4 * tid + u]; sm += hh[u]; }
+        for (int u = 0; u < kPer; ++u) { hh[u] = s_cnt[kPer * tid + u]; sm += hh[u]; }
         unsigned tt;
         unsigned rr = block_scan(sm, s_w, tt);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int d = 4 * tid + u;
+        for (int u = 0; u < kPer; ++u) {
+          const int d = kPer * tid + u;
           s_off[d] = (off + rr) | (hh[u] == 1u ? 0x80000000u : 0u);
           if (hh[u] >= 2u) {
             const uint4 r2 = make_uint4(off + rr, hh[u], hh[u], (unsigned)(dg + 1) | ((src ^ 1u) << 8));
@@ -751,10 +853,15 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
     a.rl[i] = reinterpret_cast<uint4 *>(p + L.rl[i]);
   }
   const int nsm = sm_count();
-  int C = ctas > 0 ? ctas : nsm / 2;
-  C = std::max(1, std::min(C, std::min(kMaxC, 2 * nsm)));
   cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(evict_select_kernel), 0);
   if (e != cudaSuccess) return e;
+  static const int per_sm = [] {  // co-resident CTAs per SM (cooperative launch bound)
+    int v = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, evict_select_kernel, kT, 0);
+    return std::max(1, v);
+  }();
+  int C = ctas > 0 ? ctas : nsm / 2;
+  C = std::max(1, std::min(C, std::min(kMaxC, per_sm * nsm)));
   void *args[] = {(void *)&a};
   return cudaLaunchCooperativeKernel((void *)evict_select_kernel, dim3(C), dim3(kT), args, 0, s);
 }
