@@ -17,7 +17,7 @@ using namespace dev;
 // splits.
 // ---------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
+__global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
                                                     const __grid_constant__ ReqList<MergeReq> RL,
                                                     int n_units) {
   constexpr int V = D / 32;  // 4 (d=128) or 2 (d=64)
@@ -27,16 +27,28 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     atomicMin(&p.span[4], t0);
   }
-  if (w >= n_units) return;
-  const int m = w / p.Hkv, h = w - m * p.Hkv;  // m = (request, row)
   const MergeReq *reqs = RL.ptr ? RL.ptr : RL.req;
   const int32_t *pre = RL.ptr ? RL.pre_ptr : RL.pre;
-  int lo = 0, hi = RL.n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= m) lo = mid;
-    else hi = mid - 1;
+  // the request of the CTA's first unit by one binary search (warp 0), shared; each warp walks
+  // forward from it (its units are at most 7 warps further: usually the same request)
+  __shared__ int s_req0;
+  __shared__ unsigned s_fin;
+  if (threadIdx.x == 0) s_fin = 0u;
+  if (threadIdx.x < 32) {
+    const int m0 = min(blockIdx.x * 8, n_units - 1) / p.Hkv;
+    int lo = 0, hi = RL.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pre[mid] <= m0) lo = mid;
+      else hi = mid - 1;
+    }
+    if (threadIdx.x == 0) s_req0 = lo;
   }
+  __syncthreads();
+  if (w >= n_units) return;
+  const int m = w / p.Hkv, h = w - m * p.Hkv;  // m = (request, row)
+  int lo = s_req0;
+  while (lo + 1 < RL.n && pre[lo + 1] <= m) ++lo;
   const MergeReq &mq = reqs[lo];  // (a reference: dynamic casc_slot[i] indexing without a stack copy)
   const int r = m - pre[lo];
   const int nc = mq.n_casc;
@@ -45,24 +57,18 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
   auto slot_of = [&](int i) {
     return i < nc ? mq.casc_slot[i] + h * mq.casc_hstride[i] + r : split0 + (i - nc) * mq.rows;
   };
-  // every partial's lse and O vector requested before any is used (one L2 round trip each for
-  // up to kBatch partials): lane i < n loads lse_i, the warp max + weights by shuffles
-  constexpr int kBatch = 8;
-  float L = -CUDART_INF_F;
-  for (int i = lane; i < n; i += 32) L = fmaxf(L, __ldg(p.part_lse + slot_of(i)));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xffffffffu, L, o));
+  // one memory round trip for up to kBatch partials: lane j < n loads lse_j and every lane its
+  // channels of all O_j together, before the max (the loads do not depend on it); the weights
+  // e^(lse_j - max) then reach the lanes by shuffles.  More partials: further batches rescaled
+  // by the running max (exact: sum and acc carry the same factor)
+  constexpr int kBatch = 6;
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
-  float sum = 0.f;
+  float sum = 0.f, L = -CUDART_INF_F;
   for (int i0 = 0; i0 < n; i0 += kBatch) {
     const int nb = min(kBatch, n - i0);
-    float my_w = 0.f;  // lane j < nb: weight of partial i0 + j
-    if (lane < nb) {
-      const float lj = __ldg(p.part_lse + slot_of(i0 + lane));
-      my_w = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
-    }
+    const float lj = lane < nb ? __ldg(p.part_lse + slot_of(i0 + lane)) : -CUDART_INF_F;
     float xs[kBatch][V];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
@@ -77,6 +83,18 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
         }
       }
     }
+    float bm = lj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    const float Ln = fmaxf(L, bm);
+    if (Ln != L && L != -CUDART_INF_F) {  // a later batch raised the max (n > kBatch only)
+      const float c = __expf(L - Ln);
+      sum *= c;
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] *= c;
+    }
+    L = Ln;
+    const float my_w = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
       const float wgt = __shfl_sync(0xffffffffu, my_w, j);
@@ -105,10 +123,15 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnParams p,
       *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
   }
   if (p.lse && lane == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
-  if (p.span && lane == 0) {  // instrumentation: warp end
-    unsigned long long t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    atomicMax(&p.span[5], t1);
+  if (p.span) {  // instrumentation: the CTA's last warp to finish records the end
+    if (lane == 0) {
+      const unsigned active = min(8, n_units - (int)blockIdx.x * 8);
+      if (atomicAdd(&s_fin, 1u) + 1 == active) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        atomicMax(&p.span[5], t1);
+      }
+    }
   }
 }
 
