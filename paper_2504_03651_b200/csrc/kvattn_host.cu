@@ -890,6 +890,24 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   pb.tile_flops = pb.stats.tile_flops;
   std::stable_sort(pb.tile.begin(), pb.tile.end(),
                    [](const TileItem &a, const TileItem &c) { return a.k1 - a.k0 > c.k1 - c.k0; });
+  // decode requests longest first (LPT): the decode grid runs ~1.7 waves (2 CTAs/SM by shared
+  // memory), and a short request's CTAs then fill the tail instead of a long one's; each
+  // request keeps its partial slots, so the order changes no arithmetic
+  {
+    std::vector<int> ord(pb.dec.size());
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      return pb.dec[x].ctx - pb.dec[x].kb > pb.dec[y].ctx - pb.dec[y].kb;
+    });
+    std::vector<DecodeReq> dec(pb.dec.size());
+    std::vector<int32_t> pre(pb.dec.size() + 1, 0);
+    for (size_t i = 0; i < ord.size(); ++i) {
+      dec[i] = pb.dec[ord[i]];
+      pre[i + 1] = pre[i] + dec[i].nsplit;
+    }
+    pb.dec.swap(dec);
+    pb.dec_pre.swap(pre);
+  }
   pb.stats.n_decode_items = (int64_t)pb.dec_pre.back() * Hkv;  // (split, head) units
   pb.stats.n_tile_items = (int64_t)pb.tile.size();
   pb.stats.n_merge_rows = (int64_t)pb.mrg_pre.back() * Hkv;
