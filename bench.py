@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch + process group + max-over-ranks only (no GPU; CPU tests)")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="N>1: NCCL all-gather after the attention (default), or the epilogues "
+                         "storing into the peers' symmetric-memory buffers (kva_plan_set_outputs)")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (default); gloo only to smoke-test the N>1 code path on one GPU")
     return ap.parse_args()
@@ -200,6 +203,13 @@ def run_ours(args, rank, world, local):
     out = torch.empty((T, Hl, d), dtype=out_dtype, device=dev)
     lse = torch.empty((T, Hl), dtype=torch.float32, device=dev)
     gbuf = torch.empty((world, T, Hl, d), dtype=out_dtype, device=dev) if world > 1 else None
+    fused = None
+    if world > 1 and args.gather == "fused":
+        # a7 fused into the epilogues: out = this rank's slot of a symmetric gathered buffer,
+        # the peers' slots are extra destinations of every run (include/kvattn.h)
+        fused = kdist.FusedGather((T, Hl, d), out_dtype, dev)
+        out = fused.out_local
+        gbuf = fused.buf
 
     ev = None
     if not args.no_evict:
@@ -247,6 +257,9 @@ def run_ours(args, rank, world, local):
             rp["ev"] = e2
         reps.append(rp)
     rot = {"on": True, "i": 0}
+    if fused is not None:  # every replica writes into the symmetric gathered buffer
+        for rp in reps:
+            rp["out"] = fused.out_local
 
     # e2e host buffers (pinned): inputs in, output out, every step
     h_q = q.cpu().pin_memory()
@@ -344,9 +357,14 @@ def run_ours(args, rank, world, local):
         if time_idx is not None:
             plan.set_span_buffer(spans[time_idx])
             span_used.append(time_idx)
+        if fused is not None and gather_on["v"]:
+            fused.attach(plan)
         plan.run(q, out, lse, stream=stream)
         if world > 1 and gather_on["v"]:
-            kdist.gather_outputs(out, gbuf)
+            if fused is not None:
+                fused.barrier()
+            else:
+                kdist.gather_outputs(out, gbuf)
         if ev is not None:
             if threaded:
                 exc = done.get()
@@ -565,7 +583,10 @@ def run_ours(args, rank, world, local):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            kdist.gather_outputs(out, gbuf)
+            if fused is not None:  # the fused gather's only separate cost: the cross-rank barrier
+                fused.barrier()
+            else:
+                kdist.gather_outputs(out, gbuf)
         b.record(stream)
         barrier()
         g_ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
@@ -577,8 +598,12 @@ def run_ours(args, rank, world, local):
         gather = {"ms": g_ms.item(), "bytes_received_per_rank": recv,
                   "GBps_per_rank": recv / (g_ms.item() * 1e-3) / 1e9,
                   "ms_per_step_without_gather": ms_ng, "ms_per_step_with_gather": ms,
-                  "backend": dist.get_backend(), "timing": "CUDA events around K back-to-back "
-                  "all_gather_into_tensor calls on the bench stream, max over ranks"}
+                  "backend": dist.get_backend(), "mode": args.gather,
+                  "timing": ("CUDA events around K back-to-back all_gather_into_tensor calls on the bench "
+                             "stream, max over ranks") if fused is None else
+                            ("fused into the epilogues (peer stores over NVLink while the attention runs): "
+                             "'ms' = K back-to-back symmetric-memory barriers alone; the transfer itself "
+                             "is inside ms_per_step_with_gather")}
     ms_e2e = None
     if not args.no_e2e and (not args.profile or os.environ.get("KVA_BENCH_E2E_IN_PROFILE") == "1"):
         ms_e2e = timed_e2e_pipelined(args.steps)

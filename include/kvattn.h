@@ -202,6 +202,15 @@ kva_status hybrid_attention_run_phases(const kva_plan *plan, const void *q, int6
  * to 0).  Unlike timing events this does not break the programmatic-dependent-launch chain of
  * the run.  NULL disables it. */
 kva_status kva_plan_set_span_buffer(kva_plan *plan, unsigned long long *dev_span);
+/* The output all-gather (a7; H5) fused into the attention epilogues: every
+ * later run of this plan stores each final output row not only into `out` but also, at the
+ * same element offset (same strides), into outs[0, n) — with kv-head sharding these are the
+ * peers' gathered output buffers shifted to this rank's head block, mapped into this process
+ * (CUDA IPC / symmetric memory over NVLink), so the gather overlaps the attention tile by tile
+ * instead of following it.  Rows that go through partials are stored by the merge kernel.  The
+ * caller orders the peers' reads after every rank's run (a cross-rank barrier on the stream).
+ * n <= 7 device pointers, 16-byte aligned; n = 0 clears.  lse is written locally only. */
+kva_status kva_plan_set_outputs(kva_plan *plan, int32_t n, void *const *outs);
 kva_status kva_plan_set_timing_events(kva_plan *plan, void *tile_begin, void *tile_end,
                                       void *decode_begin, void *decode_end);
 /* Number of kernel launches hybrid_attention_run_phases(plan, phases) enqueues. */

@@ -29,6 +29,7 @@ constexpr int kSplitKeys = 512;   // fixed split-KV length (depends only on ctx,
 constexpr int kDecodeRows = 16;   // rows (q tokens x g heads) one decode warp handles
 constexpr int kTileMTc = 128;     // rows per tcgen05 tile CTA (UMMA M = TMEM lanes)
 constexpr int kTileN = 64;        // keys per tile-kernel pipeline stage (4 blocks)
+constexpr int kMaxOutExtra = 7;   // extra output destinations (peers of an 8-GPU node)
 
 // One decode warp: <= 16 rows (tok*g + hh) of one request and kv-head over keys [k0, k1).
 // One decode-class request: keys [kb, ctx) are cut into nsplit splits of
@@ -97,6 +98,10 @@ struct AttnParams {
   int64_t q_stride_tok, q_stride_head;
   void *out;
   int64_t o_stride_tok, o_stride_head;
+  // a7 fused into the epilogues: every output row is also stored at the same element offset in
+  // out_extra[0, n_out_extra) — peers' gathered buffers over NVLink (kva_plan_set_outputs)
+  int32_t n_out_extra;
+  void *out_extra[kMaxOutExtra];
   int32_t out_f32;
   float *lse;             // nullable [total_q][Hq]
   // workspace

@@ -335,14 +335,18 @@ __global__ void __launch_bounds__(128, MINB)
     if (slot < 0) {
       const int64_t qrow = q_row0 + r / g;
       const int hq = kv_head * g + r % g;
-      if (p.out_f32) {
-        float *dst = reinterpret_cast<float *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+      const int64_t off = qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+      for (int o = 0; o <= p.n_out_extra; ++o) {  // own output, then the peers' (fused a7)
+        void *base = o == 0 ? p.out : p.out_extra[o - 1];
+        if (p.out_f32) {
+          float *dst = reinterpret_cast<float *>(base) + off;
 #pragma unroll
-        for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
-      } else {
-        uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+          for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
+        } else {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(base) + off;
 #pragma unroll
-        for (int i = 0; i < V; i += 2) *reinterpret_cast<uint32_t *>(dst + i) = pack_bf16(v[i], v[i + 1]);
+          for (int i = 0; i < V; i += 2) *reinterpret_cast<uint32_t *>(dst + i) = pack_bf16(v[i], v[i + 1]);
+        }
       }
     } else {
       float *dst = p.part_o + (int64_t)(slot + r) * D + lane * V;

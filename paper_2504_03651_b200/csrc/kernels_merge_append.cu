@@ -108,19 +108,22 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
   const float inv = 1.f / sum;
   const int q_head = h * p.g + r % p.g, q_row = mq.q_row0 + r / p.g;
   const int64_t off = (int64_t)q_row * p.o_stride_tok + (int64_t)q_head * p.o_stride_head + lane * V;
-  if (p.out_f32) {
-    float *dst = reinterpret_cast<float *>(p.out) + off;
-    if constexpr (V == 4)
-      *reinterpret_cast<float4 *>(dst) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    else
-      *reinterpret_cast<float2 *>(dst) = make_float2(acc[0] * inv, acc[1] * inv);
-  } else {
-    uint16_t *dst = reinterpret_cast<uint16_t *>(p.out) + off;
-    if constexpr (V == 4)
-      *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
-                                                   pack_bf16(acc[2] * inv, acc[3] * inv));
-    else
-      *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
+  for (int o = 0; o <= p.n_out_extra; ++o) {  // own output, then the peers' (fused a7)
+    void *base = o == 0 ? p.out : p.out_extra[o - 1];
+    if (p.out_f32) {
+      float *dst = reinterpret_cast<float *>(base) + off;
+      if constexpr (V == 4)
+        *reinterpret_cast<float4 *>(dst) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      else
+        *reinterpret_cast<float2 *>(dst) = make_float2(acc[0] * inv, acc[1] * inv);
+    } else {
+      uint16_t *dst = reinterpret_cast<uint16_t *>(base) + off;
+      if constexpr (V == 4)
+        *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
+                                                     pack_bf16(acc[2] * inv, acc[3] * inv));
+      else
+        *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
+    }
   }
   if (p.lse && lane == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
   if (p.span) {  // instrumentation: the CTA's last warp to finish records the end

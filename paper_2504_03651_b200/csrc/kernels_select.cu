@@ -40,10 +40,13 @@ namespace {
 #define KVA_SEL_THREADS 512
 #endif
 constexpr int kT = KVA_SEL_THREADS;  // threads per CTA
-constexpr int kPer = (1 << 11) / kT;  // histogram bins per thread in the scans
 constexpr int kNW = kT / 32;
-constexpr int kDig = 11;             // radix digit bits
+#ifndef KVA_SEL_DIGIT
+#define KVA_SEL_DIGIT 11
+#endif
+constexpr int kDig = KVA_SEL_DIGIT;  // radix digit bits
 constexpr int kBins = 1 << kDig;
+constexpr int kPer = kBins / kT;      // histogram bins per thread in the scans
 constexpr int kCap = 2048;           // pairs one CTA sorts in shared memory (24 KB)
 constexpr int kWarpMax = 256;        // pairs one warp sorts in registers (8 per lane)
 constexpr int kMaxRuns = 8;          // runs of varying key bits kept apart (more are merged)
@@ -368,7 +371,8 @@ __device__ __forceinline__ void sort_bucket(const SelArgs &a, const uint64_t *sk
 #endif
 __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_constant__ SelArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ __align__(16) unsigned char s_buf[kCap * 12];  // 24 KB: two bin arrays | a sort buffer
+  constexpr int kBufBytes = kCap * 12 > 8 * kBins ? kCap * 12 : 8 * kBins;
+  __shared__ __align__(16) unsigned char s_buf[kBufBytes];  // two bin arrays | a sort buffer (24 KB at 11 bits)
   __shared__ unsigned s_w[kNW];
   __shared__ unsigned long long s_red[3][kNW];
   __shared__ Comp s_comp;

@@ -561,18 +561,22 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           float4 *dst = reinterpret_cast<float4 *>(p.part_o + (int64_t)(it.slot + (r - it.r0)) * D + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-        } else if (p.out_f32) {
-          float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(p.out) + (int64_t)qrow * p.o_stride_tok +
-                                                   (int64_t)hq * p.o_stride_head + c * 32);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         } else {
-          uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(p.out) + (int64_t)qrow * p.o_stride_tok +
-                                                 (int64_t)hq * p.o_stride_head + c * 32);
+          const int64_t off = (int64_t)qrow * p.o_stride_tok + (int64_t)hq * p.o_stride_head + c * 32;
+          for (int oi = 0; oi <= p.n_out_extra; ++oi) {  // own output, then the peers' (fused a7)
+            void *base = oi == 0 ? p.out : p.out_extra[oi - 1];
+            if (p.out_f32) {
+              float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(base) + off);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
-                                pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
+              for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+            } else {
+              uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(base) + off);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                dst[i] = make_uint4(pack_bf16(o[8 * i], o[8 * i + 1]), pack_bf16(o[8 * i + 2], o[8 * i + 3]),
+                                    pack_bf16(o[8 * i + 4], o[8 * i + 5]), pack_bf16(o[8 * i + 6], o[8 * i + 7]));
+            }
+          }
         }
       }
       if (valid) {

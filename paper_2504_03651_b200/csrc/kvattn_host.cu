@@ -715,6 +715,8 @@ struct kva_plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t t_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events
   unsigned long long *span = nullptr;                           // optional in-kernel spans
+  int n_out_extra = 0;                                          // fused a7: peer destinations
+  void *out_extra[kMaxOutExtra] = {};
   kva_plan_stats stats{};
 };
 
@@ -1127,6 +1129,8 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   p.lse = lse;
   p.dbg = nullptr;
   p.span = pl->span;
+  p.n_out_extra = pl->n_out_extra;
+  for (int i = 0; i < kMaxOutExtra; ++i) p.out_extra[i] = pl->out_extra[i];
   p.debug_flags = (int32_t)opt(kOptDebugFlags);
   if (const int64_t ts_addr = opt(kOptDebugTs)) p.dbg = reinterpret_cast<unsigned long long *>(ts_addr);
   const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
@@ -1220,6 +1224,17 @@ extern "C" kva_status hybrid_attention_run(const kva_plan *pl, const void *q, in
                                            int32_t out_dtype, float *lse, kva_stream_t stream) {
   return hybrid_attention_run_phases(pl, q, q_st, q_sh, out, o_st, o_sh, out_dtype, lse,
                                      KVA_PHASE_ALL, stream);
+}
+
+extern "C" kva_status kva_plan_set_outputs(kva_plan *pl, int32_t n, void *const *outs) {
+  if (!pl || n < 0 || n > kMaxOutExtra || (n > 0 && !outs))
+    return fail(KVA_ERR_INVALID, "n must be in [0, %d] with a pointer array", kMaxOutExtra);
+  for (int i = 0; i < n; ++i)
+    if (!outs[i] || (reinterpret_cast<uintptr_t>(outs[i]) & 15))
+      return fail(KVA_ERR_INVALID, "extra output %d is null or not 16-byte aligned", i);
+  pl->n_out_extra = n;
+  for (int i = 0; i < kMaxOutExtra; ++i) pl->out_extra[i] = i < n ? outs[i] : nullptr;
+  return KVA_OK;
 }
 
 extern "C" kva_status kva_plan_set_span_buffer(kva_plan *pl, unsigned long long *dev_span) {

@@ -38,3 +38,36 @@ def token_major(gbuf: torch.Tensor) -> torch.Tensor:
     """[G][T][Hl][d] -> [T][G*Hl][d] (a copy; for checks and for consumers needing it)."""
     G, T, Hl, d = gbuf.shape
     return gbuf.permute(1, 0, 2, 3).reshape(T, G * Hl, d)
+
+
+class FusedGather:
+    """a7 fused into the attention epilogues (include/kvattn.h kva_plan_set_outputs, H5): a
+    symmetric-memory buffer gbuf [G][T][Hq/G][d] on every rank (torch symmetric memory, NVLink
+    peer mappings); this rank's merge / tile / decode epilogues store its head block into slot
+    `rank` of EVERY peer's gbuf while the attention runs, instead of an all-gather after it.
+    barrier() (a device-side cross-rank barrier on the current stream) then orders the peers'
+    reads.  The NCCL all_gather_into_tensor of gather_outputs() is the correctness baseline."""
+
+    def __init__(self, local_shape, dtype, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        gname = (group or dist.group.WORLD).group_name
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            symm_mem.enable_symm_mem_for_group(gname)
+        self.buf = symm_mem.empty((self.world,) + tuple(local_shape), dtype=dtype, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, gname)
+        self.out_local = self.buf[self.rank]          # this rank's own slot (the plan's `out`)
+        slot_bytes = self.out_local.numel() * self.out_local.element_size()
+        self.peer_ptrs = [int(self.hdl.buffer_ptrs[p]) + self.rank * slot_bytes
+                          for p in range(self.world) if p != self.rank]
+
+    def attach(self, plan):
+        """Every later run of `plan` also stores into the peers' slots of this rank."""
+        plan.set_extra_outputs(self.peer_ptrs)
+
+    def barrier(self):
+        """Device-side: every rank's stores issued before this point are visible after it."""
+        self.hdl.barrier(channel=0)
+        return self.buf

@@ -71,7 +71,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "kv_pool_free_count", "kv_pool_resync", "kv_pool_sync", "kv_append_workspace_size", "kv_append",
            "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
-           "kva_plan_set_span_buffer",
+           "kva_plan_set_span_buffer", "kva_plan_set_outputs",
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "kv_truncate", "evict_keys",
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
@@ -117,6 +117,7 @@ def load(build_if_missing: bool = True):
         "kva_plan_launch_count": ([P, i32, P], ctypes.c_int),
         "kva_plan_set_timing_events": ([P, P, P, P, P], ctypes.c_int),
         "kva_plan_set_span_buffer": ([P, P], ctypes.c_int),
+        "kva_plan_set_outputs": ([P, i32, P], ctypes.c_int),
         "kv_release_blocks": ([P, P, i64, P], ctypes.c_int),
         "kv_truncate": ([P, P, P, P], ctypes.c_int),
         "kva_plan_destroy": ([P], ctypes.c_int),
@@ -350,6 +351,14 @@ class Plan:
         h = lambda e: None if e is None else ctypes.c_void_p(e.cuda_event)
         _check(load().kva_plan_set_timing_events(self.handle, h(tile_begin), h(tile_end),
                                                  h(decode_begin), h(decode_end)))
+
+    def set_extra_outputs(self, outs):
+        """kva_plan_set_outputs: every output row is also stored into each of `outs` (device
+        tensors or raw device addresses with out's strides) — the fused all-gather epilogue."""
+        ptrs = [o if isinstance(o, int) else o.data_ptr() for o in (outs or [])]
+        self._extra_refs = list(outs or [])  # keep tensors alive while the plan may run
+        arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+        _check(load().kva_plan_set_outputs(self.handle, len(ptrs), arr))
 
     def set_span_buffer(self, span: torch.Tensor | None):
         """kva_plan_set_span_buffer: int64 device tensor [6] (decode, tile, merge start/end ns;

@@ -30,3 +30,32 @@ def test_shards_concatenate_to_g1_bitexact(name, worlds):
             torch.cuda.empty_cache()
         assert torch.equal(torch.cat(outs, dim=1), ref), G
         assert torch.equal(torch.cat(lses, dim=1), ref_lse), G
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_fused_gather_epilogue_stores_every_destination(out_dtype):
+    """kva_plan_set_outputs (a7 fused into the epilogues): with kv-head shards G = 2 on one GPU
+    and each shard's plan given the OTHER shard's slot of a second gathered buffer as an extra
+    destination (what the peers' NVLink mappings are on a node), both gathered buffers end up
+    bit-identical to the concatenation of the shards' own outputs — decode-direct, tile-direct
+    and merged rows alike (tiny: online decodes, chunks, a shared-prefix group)."""
+    import paper_2504_03651_b200 as K
+    G = 2
+    outs = []
+    wl0 = W.make_workload("tiny", rank=0, world=G)
+    T, Hl, d = wl0.q.shape
+    gbufs = [torch.full((G, T, Hl, d), float("nan"), dtype=out_dtype, device="cuda") for _ in range(G)]
+    for r in range(G):
+        wl = W.make_workload("tiny", rank=r, world=G)
+        g = gpu_step(wl, out_dtype=out_dtype)
+        outs.append(g["out"])
+        # rank r's run again, now storing into its slot of BOTH gathered buffers
+        plan = g["plan"]
+        plan.set_extra_outputs([gbufs[1 - r][r]])
+        plan.run(g["q"], gbufs[r][r])
+        torch.cuda.synchronize()
+    for p in range(G):
+        for r in range(G):
+            a = gbufs[p][r].cpu().view(torch.int16 if out_dtype == torch.bfloat16 else torch.int32)
+            b = outs[r].cpu().view(torch.int16 if out_dtype == torch.bfloat16 else torch.int32)
+            assert torch.equal(a, b), (p, r)
