@@ -562,6 +562,7 @@ def run_ours(args, rank, world, local):
     # standalone decode-kernel timing (same plan, no co-running kernels): context for the
     # in-step roofline above, which is measured while the tile kernel shares the GPU
     dec_alone = None
+    extra_alone = {}
     if not args.profile and stats["n_decode_items"] > 0:
         plan_s = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
         ts_ = []
@@ -573,8 +574,40 @@ def run_ours(args, rank, world, local):
             b.synchronize()
             if i >= 3:
                 ts_.append(a.elapsed_time(b))
-        plan_s.close()
         dec_alone = statistics.median(ts_)
+        # kv_append and evict_select alone: each call is preceded by a
+        # decode run so the GPU is still busy while the host enqueues it, then bracketed by two
+        # events — device time of that call alone, without its host enqueue
+        def alone(fn, after=None, n=6):
+            ts2 = []
+            for i in range(n + 2):
+                plan_s.run(q, out, lse, stream=stream, phases=K.PHASE_DECODE)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                if after is not None:
+                    after()
+                b.synchronize()
+                if i >= 2:
+                    ts2.append(a.elapsed_time(b))
+            return statistics.median(ts2)
+        new_rows = int(sum(int(x) for x in np.diff(batch.q_indptr)))
+        app_bytes = 2 * 2 * new_rows * k_new.shape[1] * d * 2  # K and V rows: read once, written once
+        app_ms = alone(lambda: K.kv_append(pool, batch, k_new, v_new, ws_app, stream=stream),
+                       after=lambda: K.kv_truncate(pool, batch, keep_len, stream=stream))
+        extra_alone["kv_append"] = {"us": app_ms * 1e3, "bytes": app_bytes,
+                                    "GBps": app_bytes / (app_ms * 1e-3) / 1e9}
+        if ev is not None:
+            ev_ms = alone(lambda: K.evict_select(ev["mgr"].keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"],
+                                                 stream=stream, sync=False))
+            extra_alone["evict_select"] = {"us": ev_ms * 1e3, "keys": ev["n"], "k": ev["k"],
+                                           "GBps_keys_once": ev["n"] * 8 / (ev_ms * 1e-3) / 1e9,
+                                           "note": "1M u64 keys (8.4 MB, read 3x from L2), top-64k sorted"}
+            mg_ms = alone(lambda: ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"],
+                                            recount=False, stream=stream))
+            extra_alone["kv_manager_step"] = {"us": mg_ms * 1e3, "blocks": ev["n"]}
+        plan_s.close()
     gather = None
     if world > 1:
         # a7 reported on its own: the all-gather alone, and the step without it
@@ -672,6 +705,8 @@ def run_ours(args, rank, world, local):
         res["step_period_ms"] = {"p10": pct(period_ms, 0.1), "median": pct(period_ms, 0.5),
                                  "p90": pct(period_ms, 0.9),
                                  "timing": "device time between consecutive steps' last merge CTA end"}
+    if extra_alone:
+        res["config"]["alone"] = extra_alone
     if dec_alone:
         a = dec_bytes / (dec_alone * 1e-3) / 1e9
         res["config"]["decode_kernel_standalone"] = {"ms": dec_alone, "GBps": a, "frac_of_peak": a / peak,
