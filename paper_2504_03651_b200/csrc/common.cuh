@@ -2,6 +2,7 @@
 // legacy mma.sync bf16, fast exp2.  Product code; shares nothing with oracle/.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 namespace kva {
@@ -41,8 +42,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+#ifdef KVA_MBAR_DEBUG  // diagnostics build: report a wait that never completes, then trap
+  long long spins = 0;
+  while (!mbar_try_wait(bar, phase)) {
+    if (++spins == (1ll << 22) && (threadIdx.x & 31) == 0) {
+      printf("mbar_wait stuck: block %d thread %d bar smem 0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             smem_u32(bar), phase);
+    }
+    if (spins == (1ll << 24)) __trap();
+  }
+#else
   while (!mbar_try_wait(bar, phase)) {
   }
+#endif
 }
 
 // ---------------- TMA ----------------
