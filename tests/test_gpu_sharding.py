@@ -59,3 +59,38 @@ def test_fused_gather_epilogue_stores_every_destination(out_dtype):
             a = gbufs[p][r].cpu().view(torch.int16 if out_dtype == torch.bfloat16 else torch.int32)
             b = outs[r].cpu().view(torch.int16 if out_dtype == torch.bfloat16 else torch.int32)
             assert torch.equal(a, b), (p, r)
+
+
+def test_fused_gather_symmetric_memory_one_rank():
+    """dist.FusedGather through torch symmetric memory on a 1-rank NCCL group (the API path a
+    multi-GPU node uses: allocation, rendezvous, peer pointers, device-side barrier): the
+    gathered buffer holds exactly the plan's output."""
+    import os
+    import socket
+    import torch.distributed as dist
+    import paper_2504_03651_b200 as K
+    from paper_2504_03651_b200 import dist as kdist
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        wl = W.make_workload("tiny")
+        g = gpu_step(wl, out_dtype=torch.bfloat16)
+        T, Hl, d = g["out"].shape
+        try:
+            fg = kdist.FusedGather((T, Hl, d), torch.bfloat16, torch.device("cuda", 0))
+        except Exception as e:  # symmetric memory unavailable in this build / driver
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        assert fg.peer_ptrs == [] and fg.buf.shape == (1, T, Hl, d)
+        fg.attach(g["plan"])
+        g["plan"].run(g["q"], fg.out_local)
+        fg.barrier()
+        torch.cuda.synchronize()
+        assert torch.equal(fg.buf[0].view(torch.int16), g["out"].view(torch.int16))
+    finally:
+        dist.destroy_process_group()
