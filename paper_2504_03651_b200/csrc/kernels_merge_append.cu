@@ -12,16 +12,20 @@ using namespace dev;
 // ---------------------------------------------------------------------------------------
 // a6: for each output (row, q-head) with partials {(O_j, lse_j)}:
 //   lse = ln sum_j e^{lse_j},  O = sum_j e^{lse_j - lse} O_j.
-// One warp per (request row, kv head); each lane owns D/32 contiguous channels (16-B / 8-B
-// vectors).  Partials in order: the cascade prefix slots (one per nested level), then the key
-// splits.
+// One HALF-warp per (request row, kv head) — two units per warp instruction stream, each lane
+// owning D/16 contiguous channels (2 x 16-B for d = 128).  Partials in order: the cascade
+// prefix slots (one per nested level), then the key splits.  lse and O of up to kBatch
+// partials are loaded in one memory round trip, before the max (which they do not need).
 // ---------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
+__global__ void __launch_bounds__(256, 4) merge_kernel(const AttnParams p,
                                                     const __grid_constant__ ReqList<MergeReq> RL,
                                                     int n_units) {
-  constexpr int V = D / 32;  // 4 (d=128) or 2 (d=64)
-  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  constexpr int V = D / 16;  // channels per lane: 8 (d=128) or 4 (d=64)
+  constexpr int kUnitsPerCta = 16;
+  const int lane = threadIdx.x & 31, hl = lane & 15;  // lane within the half-warp
+  const unsigned hmask = (lane < 16) ? 0x0000FFFFu : 0xFFFF0000u;
+  const int w = blockIdx.x * kUnitsPerCta + (threadIdx.x >> 4);  // this half-warp's unit
   if (p.span && threadIdx.x == 0) {  // instrumentation: CTA start
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -29,13 +33,13 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
   }
   const MergeReq *reqs = RL.ptr ? RL.ptr : RL.req;
   const int32_t *pre = RL.ptr ? RL.pre_ptr : RL.pre;
-  // the request of the CTA's first unit by one binary search (warp 0), shared; each warp walks
-  // forward from it (its units are at most 7 warps further: usually the same request)
+  // the request of the CTA's first unit by one binary search (warp 0), shared; each half-warp
+  // walks forward from it (its unit is at most 15 further: usually the same request)
   __shared__ int s_req0;
   __shared__ unsigned s_fin;
   if (threadIdx.x == 0) s_fin = 0u;
   if (threadIdx.x < 32) {
-    const int m0 = min(blockIdx.x * 8, n_units - 1) / p.Hkv;
+    const int m0 = min(blockIdx.x * kUnitsPerCta, n_units - 1) / p.Hkv;
     int lo = 0, hi = RL.n - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -45,7 +49,7 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
     if (threadIdx.x == 0) s_req0 = lo;
   }
   __syncthreads();
-  if (w >= n_units) return;
+  if (w >= n_units) return;  // whole half-warps leave (n_units is a per-half-warp bound)
   const int m = w / p.Hkv, h = w - m * p.Hkv;  // m = (request, row)
   int lo = s_req0;
   while (lo + 1 < RL.n && pre[lo + 1] <= m) ++lo;
@@ -57,35 +61,29 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
   auto slot_of = [&](int i) {
     return i < nc ? mq.casc_slot[i] + h * mq.casc_hstride[i] + r : split0 + (i - nc) * mq.rows;
   };
-  // one memory round trip for up to kBatch partials: lane j < n loads lse_j and every lane its
-  // channels of all O_j together, before the max (the loads do not depend on it); the weights
-  // e^(lse_j - max) then reach the lanes by shuffles.  More partials: further batches rescaled
-  // by the running max (exact: sum and acc carry the same factor)
-  constexpr int kBatch = 6;
+  constexpr int kBatch = 4;
   float acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = 0.f;
   float sum = 0.f, L = -CUDART_INF_F;
-  for (int i0 = 0; i0 < n; i0 += kBatch) {
+  for (int i0 = 0; i0 < n; i0 += kBatch) {  // (the two half-warps may run different counts)
     const int nb = min(kBatch, n - i0);
-    const float lj = lane < nb ? __ldg(p.part_lse + slot_of(i0 + lane)) : -CUDART_INF_F;
+    const float lj = hl < nb ? __ldg(p.part_lse + slot_of(i0 + hl)) : -CUDART_INF_F;
     float xs[kBatch][V];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
       if (j < nb) {
-        const float *src = p.part_o + (int64_t)slot_of(i0 + j) * D + lane * V;
-        if constexpr (V == 4) {
-          const float4 x = __ldg(reinterpret_cast<const float4 *>(src));
-          xs[j][0] = x.x; xs[j][1] = x.y; xs[j][2] = x.z; xs[j][3] = x.w;
-        } else {
-          const float2 x = __ldg(reinterpret_cast<const float2 *>(src));
-          xs[j][0] = x.x; xs[j][1] = x.y;
+        const float4 *src = reinterpret_cast<const float4 *>(p.part_o + (int64_t)slot_of(i0 + j) * D + hl * V);
+#pragma unroll
+        for (int v4 = 0; v4 < V / 4; ++v4) {
+          const float4 x = __ldg(src + v4);
+          xs[j][4 * v4] = x.x; xs[j][4 * v4 + 1] = x.y; xs[j][4 * v4 + 2] = x.z; xs[j][4 * v4 + 3] = x.w;
         }
       }
     }
     float bm = lj;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+    for (int o = 8; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(hmask, bm, o, 16));
     const float Ln = fmaxf(L, bm);
     if (Ln != L && L != -CUDART_INF_F) {  // a later batch raised the max (n > kBatch only)
       const float c = __expf(L - Ln);
@@ -97,7 +95,7 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
     const float my_w = lj == -CUDART_INF_F ? 0.f : __expf(lj - L);
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      const float wgt = __shfl_sync(0xffffffffu, my_w, j);
+      const float wgt = __shfl_sync(hmask, my_w, j, 16);
       if (j < nb) {
         sum += wgt;
 #pragma unroll
@@ -107,28 +105,28 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
   }
   const float inv = 1.f / sum;
   const int q_head = h * p.g + r % p.g, q_row = mq.q_row0 + r / p.g;
-  const int64_t off = (int64_t)q_row * p.o_stride_tok + (int64_t)q_head * p.o_stride_head + lane * V;
+  const int64_t off = (int64_t)q_row * p.o_stride_tok + (int64_t)q_head * p.o_stride_head + hl * V;
   for (int o = 0; o <= p.n_out_extra; ++o) {  // own output, then the peers' (fused a7)
     void *base = o == 0 ? p.out : p.out_extra[o - 1];
     if (p.out_f32) {
-      float *dst = reinterpret_cast<float *>(base) + off;
-      if constexpr (V == 4)
-        *reinterpret_cast<float4 *>(dst) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-      else
-        *reinterpret_cast<float2 *>(dst) = make_float2(acc[0] * inv, acc[1] * inv);
+      float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(base) + off);
+#pragma unroll
+      for (int v4 = 0; v4 < V / 4; ++v4)
+        dst[v4] = make_float4(acc[4 * v4] * inv, acc[4 * v4 + 1] * inv, acc[4 * v4 + 2] * inv, acc[4 * v4 + 3] * inv);
     } else {
       uint16_t *dst = reinterpret_cast<uint16_t *>(base) + off;
-      if constexpr (V == 4)
-        *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
-                                                     pack_bf16(acc[2] * inv, acc[3] * inv));
-      else
-        *reinterpret_cast<uint32_t *>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
+      if constexpr (V == 8) {
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                                                     pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+      } else {
+        *reinterpret_cast<uint2 *>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+      }
     }
   }
-  if (p.lse && lane == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
-  if (p.span) {  // instrumentation: the CTA's last warp to finish records the end
-    if (lane == 0) {
-      const unsigned active = min(8, n_units - (int)blockIdx.x * 8);
+  if (p.lse && hl == 0) p.lse[(int64_t)q_row * p.Hq + q_head] = L + __logf(sum);
+  if (p.span) {  // instrumentation: the CTA's last unit to finish records the end
+    if (hl == 0) {
+      const unsigned active = min(kUnitsPerCta, n_units - (int)blockIdx.x * kUnitsPerCta);
       if (atomicAdd(&s_fin, 1u) + 1 == active) {
         unsigned long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -140,7 +138,7 @@ __global__ void __launch_bounds__(256, 6) merge_kernel(const AttnParams p,
 
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n_units, cudaStream_t s) {
   if (n_units <= 0) return cudaSuccess;
-  const int grid = (n_units + 7) / 8;
+  const int grid = (n_units + 15) / 16;  // 16 units (half-warps) per 256-thread CTA
   if (p.d == 128)
     merge_kernel<128><<<grid, 256, 0, s>>>(p, RL, n_units);
   else
