@@ -47,7 +47,10 @@ constexpr int kNW = kT / 32;
 constexpr int kDig = KVA_SEL_DIGIT;  // radix digit bits
 constexpr int kBins = 1 << kDig;
 constexpr int kPer = kBins / kT;      // histogram bins per thread in the scans
-constexpr int kCap = 2048;           // pairs one CTA sorts in shared memory (24 KB)
+#ifndef KVA_SEL_CAP
+#define KVA_SEL_CAP 2048
+#endif
+constexpr int kCap = KVA_SEL_CAP;    // pairs one CTA sorts in shared memory (24 KB at 2048)
 constexpr int kWarpMax = 256;        // pairs one warp sorts in registers (8 per lane)
 constexpr int kMaxRuns = 8;          // runs of varying key bits kept apart (more are merged)
 constexpr int kMaxLevels = 16;
@@ -240,6 +243,11 @@ struct Comp {
   unsigned long long cst;  // the key bits outside the runs (equal in every evictable key)
   unsigned long long mask[kMaxRuns];
   int sh[kMaxRuns];
+  // digit 0 straight from the raw key when it lies within the key bits (n0 >= 0): the sum of
+  // (key & m0[i]) >> s0[i] over the n0 runs that reach into its window; n0 < 0: via compress
+  int n0;
+  unsigned long long m0[kMaxRuns];
+  int s0[kMaxRuns];
 };
 // the first 4 runs in registers (the `evict` keys have 3: priority code, LAT, depth), the
 // rest read from shared memory
@@ -249,6 +257,27 @@ struct CompR {
   int s0, s1, s2, s3;
   const Comp *c;
 };
+// digit 0 from the raw key (Comp::n0 >= 0): the first two contributing runs in registers
+struct Dig0R {
+  int n0;
+  unsigned long long m0, m1;
+  int s0, s1;
+  const Comp *c;
+};
+__device__ __forceinline__ Dig0R dig0_regs(const Comp &c) {
+  Dig0R r;
+  r.n0 = c.n0;
+  r.m0 = c.m0[0]; r.m1 = c.n0 > 1 ? c.m0[1] : 0ull;
+  r.s0 = c.s0[0]; r.s1 = c.n0 > 1 ? c.s0[1] : 0;
+  r.c = &c;
+  return r;
+}
+__device__ __forceinline__ int digit0_raw(const Dig0R &r, uint64_t key) {
+  uint32_t d = (uint32_t)((key & r.m0) >> r.s0) | (uint32_t)((key & r.m1) >> r.s1);
+  if (r.n0 > 2)
+    for (int i = 2; i < r.n0; ++i) d |= (uint32_t)((key & r.c->m0[i]) >> r.c->s0[i]);
+  return (int)d;
+}
 __device__ __forceinline__ CompR comp_regs(const Comp &c) {
   CompR r;
   r.nr = c.nr;
@@ -536,6 +565,24 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       cp.idb = idb;
       cp.B = bits + idb;
       cp.nd = cp.B > 0 ? (cp.B + kDig - 1) / kDig : 1;
+      {  // digit-0 window [lo, lo + w) of the composite -> [wl, wh) of the compressed key
+        const int lo0 = cp.B > kDig ? cp.B - kDig : 0;
+        cp.n0 = -1;
+        if (lo0 >= idb) {
+          const int wl = lo0 - idb, wh = cp.B - idb;
+          cp.n0 = 0;
+          for (int i = 0; i < nr; ++i) {  // run i: key bit j -> compressed bit j - sh[i]
+            const int jl = wl + cp.sh[i], jh = wh + cp.sh[i];  // key bits [jl, jh) land in the window
+            if (jl >= 64) continue;
+            const uint64_t win = (jh >= 64 ? ~0ull : ((1ull << jh) - 1ull)) & ~((1ull << jl) - 1ull);
+            if (cp.mask[i] & win) {
+              cp.m0[cp.n0] = cp.mask[i] & win;
+              cp.s0[cp.n0] = jl;
+              ++cp.n0;
+            }
+          }
+        }
+      }
       s_comp = cp;
       s_red[2][0] = N;
       if (c == 0) *a.d_count = (int64_t)std::min<unsigned long long>(N, (unsigned long long)a.k);
@@ -550,11 +597,14 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;
     const DigSel ds0 = dig_sel(cp, 0);
     __syncthreads();
+    const Dig0R d0r = dig0_regs(cp);
+    const bool raw0 = d0r.n0 >= 0;
     stamp();
     for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
       int d4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d4[u] = k4[u] != kInf ? digit(ds0, compress(cr, k4[u]), i4[u]) : -1;
+      for (int u = 0; u < 4; ++u)
+        d4[u] = k4[u] == kInf ? -1 : raw0 ? digit0_raw(d0r, k4[u]) : digit(ds0, compress(cr, k4[u]), i4[u]);
       hist_batch<4>(s_cnt, d4);
     });
     __syncthreads();
@@ -655,6 +705,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     }
     if (nxt)
       for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;  // digit-(r+1) counts of the next segment
+    if (tid == 0) s_bnd[3] = 0u;  // round 0: this CTA's compacted pair count
     __syncthreads();
 
     stamp();
@@ -690,6 +741,22 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       }
       hist_batch<NK>(s_cnt, dn);
     };
+    // place a segment [xk, xk + cnt) of (compressed key, id) pairs, 2 per lane per pass
+    // (raw: the pairs hold input keys, compressed here)
+    auto seg_loop = [&](const uint64_t *xk, const int32_t *xi, unsigned cnt, bool raw) {
+      for (unsigned base = 0; base < cnt; base += 2 * kT) {
+        const unsigned i0 = base + tid, i1 = base + kT + tid;
+        const bool v0 = i0 < cnt, v1 = i1 < cnt;
+        uint64_t k2[2] = {v0 ? __ldcg(xk + i0) : kInf, v1 ? __ldcg(xk + i1) : kInf};
+        if (raw) {
+          k2[0] = v0 ? compress(cr, k2[0]) : kInf;
+          k2[1] = v1 ? compress(cr, k2[1]) : kInf;
+        }
+        const int32_t d2[2] = {v0 ? __ldcg(xi + i0) : 0, v1 ? __ldcg(xi + i1) : 0};
+        const bool b2[2] = {v0, v1};
+        place(std::integral_constant<int, 2>{}, k2, d2, b2);
+      }
+    };
     if (r == 0) {
       // keys above bin b are dropped before compressing: digit > b <=> key >= t_hi (compress is
       // an order isomorphism on keys that agree outside the runs; t_hi = the smallest such key
@@ -704,27 +771,43 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
           t_hi = t;
         }
       }
+      // filter, then place: the keys below t_hi (typically a small fraction) are compacted
+      // (raw; compressed when placed) into this CTA's own range of wk[0] (one shared atomic per warp pass, ballot
+      // ranks); the dropped keys cost a compare and a ballot.  The CTA then places its compacted
+      // pairs like a later round's segment: every lane busy, no grid barrier in between (the
+      // pairs stay with the CTA that counted them, so its bin reservations still hold).
+      uint64_t *ck = a.wk[0] + lo;
+      int32_t *ci = a.wi[0] + lo;
+      const unsigned lt = lanemask_lt();
       for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
-        uint64_t c4[4];
-        bool v4[4];
+        bool v[4];
+        unsigned m[4], tot = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          v4[u] = k4[u] < t_hi;  // also excludes kInf
-          c4[u] = v4[u] ? compress(cr, k4[u]) : 0ull;
+          v[u] = k4[u] < t_hi;  // also excludes kInf
+          m[u] = __ballot_sync(0xffffffffu, v[u]);
+          tot += __popc(m[u]);
         }
-        place(std::integral_constant<int, 4>{}, c4, i4, v4);
+        if (tot == 0u) return;
+        unsigned at = 0;
+        if (lane == 0) at = atomicAdd(&s_bnd[3], tot);
+        at = __shfl_sync(0xffffffffu, at, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (v[u]) {
+            const unsigned p = at + __popc(m[u] & lt);
+            ck[p] = k4[u];
+            ci[p] = i4[u];
+          }
+          at += __popc(m[u]);
+        }
       });
+      stamp();
+      __syncthreads();
+      seg_loop(ck, ci, s_bnd[3], true);
     } else {
-      const uint64_t *xk = a.wk[wsrc];
-      const int32_t *xi = a.wi[wsrc];
-      for (unsigned base = 0; base < m_cnt; base += 2 * kT) {
-        const unsigned i0 = base + tid, i1 = base + kT + tid;
-        const bool v0 = i0 < m_cnt, v1 = i1 < m_cnt;
-        const uint64_t k2[2] = {v0 ? __ldcg(xk + m_lo + i0) : kInf, v1 ? __ldcg(xk + m_lo + i1) : kInf};
-        const int32_t d2[2] = {v0 ? __ldcg(xi + m_lo + i0) : 0, v1 ? __ldcg(xi + m_lo + i1) : 0};
-        const bool b2[2] = {v0, v1};
-        place(std::integral_constant<int, 2>{}, k2, d2, b2);
-      }
+      stamp();  // (keeps the stamp count per round equal)
+      seg_loop(a.wk[wsrc] + m_lo, a.wi[wsrc] + m_lo, m_cnt, false);
     }
     stamp();
     if (nxt) {  // reserve this CTA's ranges in the next segment's digit bins
@@ -811,7 +894,9 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       }
     }
     stamp();
-    for (unsigned ri = (unsigned)(c * kNW + w); ri < ns; ri += (unsigned)(C * kNW)) {
+    // small buckets from the LAST CTA's warps down, large ones (above) from CTA 0 up: with fewer
+    // large buckets than CTAs the two kinds run side by side
+    for (unsigned ri = (unsigned)((C - 1 - c) * kNW + w); ri < ns; ri += (unsigned)(C * kNW)) {
       const uint4 rec = __ldcg(a.rs[L] + ri);
       const unsigned off = rec.x, size = rec.y, take = rec.z, src = rec.w >> 8;
       if (size <= 32) sort_bucket<1, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);

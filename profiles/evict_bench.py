@@ -43,7 +43,8 @@ for straddle in (False, True):
     times.sort()
     res["straddle" if straddle else "evict"] = {
         "us_median": times[len(times) // 2], "us_p10": times[len(times) // 10], "us_p90": times[9 * len(times) // 10],
-        "phase_us": [round(float(x), 1) for x in np.diff(ts) / 1e3], "rounds": int(ctl[48]), "levels": int(ctl[49])}
+        "phase_us": [round(float(x), 1) for x in np.diff(ts) / 1e3], "rounds": int(ctl[48]), "levels": int(ctl[49]),
+        "records_small_large_big": [[int(ctl[l]), int(ctl[16 + l]), int(ctl[32 + l])] for l in range(int(ctl[49]) + 1)]}
 # launch + teardown cost: a call with nothing evictable returns after phase 0 and one barrier
 keys1 = torch.full((1 << 20,), -1, dtype=torch.int64, device=dev)
 ws1 = torch.zeros(K.evict_select_workspace_size(1 << 20, 1), dtype=torch.uint8, device=dev)
