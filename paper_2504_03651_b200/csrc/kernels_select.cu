@@ -395,13 +395,178 @@ __device__ __forceinline__ void sort_bucket(const SelArgs &a, const uint64_t *sk
   }
 }
 
+// CTA bucket of <= E * kT pairs: one more MSD digit (the bucket's next digit ds) in shared
+// memory, then each pair's rank inside its sub-bin by counting (the composite is unique, so the
+// rank is the position): pairs land at off + sub-bin start + rank.  Sub-bins are ~1-3 pairs on
+// spread keys; when one holds more than kSub the bucket is sorted by the bitonic network
+// instead.  s_st = kBins + 1 counters (sub-bin slots, then their exclusive starts).
+constexpr int kSub = 48;
+template <int E>
+__device__ __forceinline__ void radix_bucket(const SelArgs &a, const uint64_t *sk, const int32_t *si, unsigned off,
+                                             unsigned size, unsigned take, const DigSel &ds, uint64_t *sbk,
+                                             int32_t *sbi, unsigned *s_st, unsigned *s_w) {
+  const int t = (int)threadIdx.x;
+  uint64_t x[E];
+  int32_t y[E];
+  int d[E];
+  unsigned slot[E];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) s_st[kPer * t + u] = 0u;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(kT * j + t);
+    x[j] = i < size ? __ldcg(sk + off + i) : kInf;
+    y[j] = i < size ? __ldcg(si + off + i) : INT32_MAX;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(kT * j + t);
+    d[j] = i < size ? digit(ds, x[j], y[j]) : 0;
+    slot[j] = i < size ? atomicAdd(&s_st[d[j]], 1u) : 0u;
+  }
+  __syncthreads();
+  unsigned h[kPer], sum = 0;
+  bool big = false;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    h[u] = s_st[kPer * t + u];
+    sum += h[u];
+    big |= h[u] > (unsigned)kSub;
+  }
+  unsigned tot;
+  unsigned run = block_scan(sum, s_w, tot);  // ends with a barrier: every count read
+  if (__syncthreads_or(big)) {
+    group_sort<E, kT>(x, y, sbk, sbi);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const unsigned i = (unsigned)(kT * j + t);
+      if (i < take) emit(a, (int64_t)off + i, y[j]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) { s_st[kPer * t + u] = run; run += h[u]; }
+  if (t == 0) s_st[kBins] = size;
+  __syncthreads();
+  unsigned lo[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(kT * j + t);
+    lo[j] = s_st[d[j]];
+    if (i < size) { sbk[lo[j] + slot[j]] = x[j]; sbi[lo[j] + slot[j]] = y[j]; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(kT * j + t);
+    if (i >= size) continue;
+    const unsigned hi = s_st[d[j] + 1];
+    unsigned pos = lo[j];
+    if (hi - lo[j] > 1u)
+      for (unsigned q = lo[j]; q < hi; ++q) pos += pair_gt(x[j], y[j], sbk[q], sbi[q]) ? 1u : 0u;
+    if (pos < take) emit(a, (int64_t)off + pos, y[j]);
+  }
+}
+
+// Warp bucket of <= 32 * E pairs (E >= 2), the same scheme as radix_bucket with an 8-bit digit
+// (the top bits of the bucket's next digit) in the warp's own shared-memory area; a sub-bin
+// of more than kSubW pairs sends the bucket to the bitonic network.
+constexpr int kWB = 256;  // warp sub-bins
+constexpr int kSubW = 24;
+struct WarpArea {
+  uint64_t k[kWarpMax];
+  int32_t i[kWarpMax];
+  unsigned h[kWB + 4];
+};
+constexpr int kDynBytes = kNW * (int)sizeof(WarpArea);
+template <int E>
+__device__ __forceinline__ void warp_radix_bucket(const SelArgs &a, const uint64_t *sk, const int32_t *si,
+                                                  unsigned off, unsigned size, unsigned take, DigSel ds,
+                                                  WarpArea *wa) {
+  constexpr int P = kWB / 32;
+  const int lane = (int)(threadIdx.x & 31);
+  if (ds.w > 8) { ds.lo += ds.w - 8; ds.w = 8; }
+  uint64_t x[E];
+  int32_t y[E];
+  int d[E];
+  unsigned slot[E];
+#pragma unroll
+  for (int u = 0; u < P; ++u) wa->h[P * lane + u] = 0u;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(32 * j + lane);
+    x[j] = i < size ? __ldcg(sk + off + i) : kInf;
+    y[j] = i < size ? __ldcg(si + off + i) : INT32_MAX;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(32 * j + lane);
+    d[j] = i < size ? digit(ds, x[j], y[j]) : 0;
+    slot[j] = i < size ? atomicAdd(&wa->h[d[j]], 1u) : 0u;
+  }
+  __syncwarp();
+  unsigned h[P], sum = 0;
+  bool big = false;
+#pragma unroll
+  for (int u = 0; u < P; ++u) {
+    h[u] = wa->h[P * lane + u];
+    sum += h[u];
+    big |= h[u] > (unsigned)kSubW;
+  }
+  if (__any_sync(0xffffffffu, big)) {
+    group_sort<E, 32>(x, y, nullptr, nullptr);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const unsigned i = (unsigned)(32 * j + lane);
+      if (i < take) emit(a, (int64_t)off + i, y[j]);
+    }
+    __syncwarp();
+    return;
+  }
+  unsigned run = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, run, o);
+    if (lane >= o) run += v;
+  }
+  run -= sum;
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < P; ++u) { wa->h[P * lane + u] = run; run += h[u]; }
+  if (lane == 0) wa->h[kWB] = size;
+  __syncwarp();
+  unsigned lo[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(32 * j + lane);
+    lo[j] = wa->h[d[j]];
+    if (i < size) { wa->k[lo[j] + slot[j]] = x[j]; wa->i[lo[j] + slot[j]] = y[j]; }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned i = (unsigned)(32 * j + lane);
+    if (i >= size) continue;
+    const unsigned hi = wa->h[d[j] + 1];
+    unsigned pos = lo[j];
+    if (hi - lo[j] > 1u)
+      for (unsigned q = lo[j]; q < hi; ++q) pos += pair_gt(x[j], y[j], wa->k[q], wa->i[q]) ? 1u : 0u;
+    if (pos < take) emit(a, (int64_t)off + pos, y[j]);
+  }
+  __syncwarp();
+}
+
 #ifndef KVA_SEL_MAXREG
 #define KVA_SEL_MAXREG 80  // measured: 1M keys alone 70 us (74 CTAs), co-runs with the attention
 #endif
 __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_constant__ SelArgs a) {
   cg::grid_group grid = cg::this_grid();
-  constexpr int kBufBytes = kCap * 12 > 8 * kBins ? kCap * 12 : 8 * kBins;
-  __shared__ __align__(16) unsigned char s_buf[kBufBytes];  // two bin arrays | a sort buffer (24 KB at 11 bits)
+  constexpr int kBufBytes = (kCap * 12 > 8 * kBins ? kCap * 12 : 8 * kBins) + 4 * (kBins + 4);
+  // two bin arrays | a sort buffer + sub-bin starts (32 KB at 11 bits)
+  __shared__ __align__(16) unsigned char s_buf[kBufBytes];
+  extern __shared__ __align__(16) unsigned char s_dyn[];  // kNW WarpAreas (small buckets)
   __shared__ unsigned s_w[kNW];
   __shared__ unsigned long long s_red[3][kNW];
   __shared__ Comp s_comp;
@@ -411,6 +576,16 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
   const int C = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   Ctl *ctl = a.ctl;
   int tp = 0;
+  // diagnostics (-DKVA_SEL_SPAN): per-CTA end of the large buckets (part[c].o, thread 0) and
+  // exit (part[c].pad, latest warp), %globaltimer ns
+  auto span_mark = [&](bool at_exit) {
+#ifdef KVA_SEL_SPAN
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!at_exit && tid == 0) a.part[c].o = t;
+    if (at_exit && lane == 0) atomicMax(&a.part[c].pad, t);
+#endif
+  };
   auto stamp = [&]() {
     if (c == 0 && tid == 0 && tp < 32) {
       unsigned long long t;
@@ -829,6 +1004,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
   // ---------------- buckets: sort every taken bin of >= 2 pairs ----------------
   uint64_t *sbk = reinterpret_cast<uint64_t *>(s_buf);
   int32_t *sbi = reinterpret_cast<int32_t *>(s_buf + kCap * 8);
+  unsigned *s_st = reinterpret_cast<unsigned *>(s_buf + kCap * 12);
   for (int lv = 0; lv < kMaxLevels; ++lv) {
     const int L = lv & 1;
     const unsigned nl = __ldcg(&ctl->n_large[lv]), ns = __ldcg(&ctl->n_small[lv]);
@@ -838,13 +1014,14 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       const unsigned off = rec.x, size = rec.y, take = rec.z, dg = rec.w & 0xFF, src = rec.w >> 8;
       const uint64_t *xk = a.sk[src];
       const int32_t *xi = a.si[src];
-      if (size <= (unsigned)kCap) {  // the CTA: registers + shared-memory exchanges
+      if (size <= (unsigned)kCap) {  // the CTA: one more digit in shared memory + sub-bin ranks
+        const DigSel dsb = dig_sel(cp, dg);
         if (size <= (unsigned)kT) {
-          sort_bucket<1, kT>(a, xk, xi, off, size, take, sbk, sbi);
+          radix_bucket<1>(a, xk, xi, off, size, take, dsb, sbk, sbi, s_st, s_w);
         } else if (size <= 2u * kT) {
-          sort_bucket<2, kT>(a, xk, xi, off, size, take, sbk, sbi);
+          radix_bucket<2>(a, xk, xi, off, size, take, dsb, sbk, sbi, s_st, s_w);
         } else {
-          if constexpr (kCap > 2 * kT) sort_bucket<kCap / kT, kT>(a, xk, xi, off, size, take, sbk, sbi);
+          if constexpr (kCap > 2 * kT) radix_bucket<kCap / kT>(a, xk, xi, off, size, take, dsb, sbk, sbi, s_st, s_w);
         }
         __syncthreads();
       } else {  // partition by the next digit into the other staging buffer -> next level
@@ -894,19 +1071,27 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       }
     }
     stamp();
-    // small buckets from the LAST CTA's warps down, large ones (above) from CTA 0 up: with fewer
-    // large buckets than CTAs the two kinds run side by side
-    for (unsigned ri = (unsigned)((C - 1 - c) * kNW + w); ri < ns; ri += (unsigned)(C * kNW)) {
-      const uint4 rec = __ldcg(a.rs[L] + ri);
-      const unsigned off = rec.x, size = rec.y, take = rec.z, src = rec.w >> 8;
-      if (size <= 32) sort_bucket<1, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
-      else if (size <= 64) sort_bucket<2, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
-      else if (size <= 128) sort_bucket<4, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
-      else sort_bucket<8, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+    if (!more) span_mark(false);
+    // small buckets on the CTAs without a large one (all CTAs when every CTA had one), spread
+    // over CTAs first: with fewer large buckets than CTAs the two kinds run side by side
+    {
+      const unsigned nl0 = nl < (unsigned)C ? nl : 0u, Cs = (unsigned)C - nl0;
+      WarpArea *wa = reinterpret_cast<WarpArea *>(s_dyn) + w;
+      if ((unsigned)c >= nl0)
+        for (unsigned ri = (unsigned)w * Cs + ((unsigned)c - nl0); ri < ns; ri += (unsigned)kNW * Cs) {
+          const uint4 rec = __ldcg(a.rs[L] + ri);
+          const unsigned off = rec.x, size = rec.y, take = rec.z, dg = rec.w & 0xFF, src = rec.w >> 8;
+          const DigSel dsb = dig_sel(cp, dg);
+          if (size <= 32) sort_bucket<1, 32>(a, a.sk[src], a.si[src], off, size, take, nullptr, nullptr);
+          else if (size <= 64) warp_radix_bucket<2>(a, a.sk[src], a.si[src], off, size, take, dsb, wa);
+          else if (size <= 128) warp_radix_bucket<4>(a, a.sk[src], a.si[src], off, size, take, dsb, wa);
+          else warp_radix_bucket<8>(a, a.sk[src], a.si[src], off, size, take, dsb, wa);
+        }
     }
     stamp();
     if (!more) {
       if (c == 0 && tid == 0) ctl->levels = (unsigned)(lv + 1);
+      span_mark(true);
       break;
     }
     grid.sync();
@@ -942,17 +1127,17 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
     a.rl[i] = reinterpret_cast<uint4 *>(p + L.rl[i]);
   }
   const int nsm = sm_count();
-  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(evict_select_kernel), 0);
+  cudaError_t e = smem_attrs_once(reinterpret_cast<const void *>(evict_select_kernel), kDynBytes);
   if (e != cudaSuccess) return e;
   static const int per_sm = [] {  // co-resident CTAs per SM (cooperative launch bound)
     int v = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, evict_select_kernel, kT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, evict_select_kernel, kT, kDynBytes);
     return std::max(1, v);
   }();
   int C = ctas > 0 ? ctas : nsm / 2;
   C = std::max(1, std::min(C, std::min(kMaxC, per_sm * nsm)));
   void *args[] = {(void *)&a};
-  return cudaLaunchCooperativeKernel((void *)evict_select_kernel, dim3(C), dim3(kT), args, 0, s);
+  return cudaLaunchCooperativeKernel((void *)evict_select_kernel, dim3(C), dim3(kT), args, kDynBytes, s);
 }
 
 }  // namespace kva

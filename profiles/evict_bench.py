@@ -39,11 +39,19 @@ for straddle in (False, True):
         times.append(a.elapsed_time(b) * 1e3 / 20)
     ts = ws[256:256 + 256].view(torch.int64).cpu().numpy()
     ctl = ws[256 + 256:256 + 256 + 4 * 50].view(torch.int32).cpu().numpy()
+    pt = ws[768:768 + 32 * 512].view(torch.int64).view(-1, 4).cpu().numpy()
+    t_end = None
+    if pt[0, 3] > ts[0]:  # -DKVA_SEL_SPAN build: per-CTA large-bucket end / exit
+        C = int((pt[:, 3] > ts[0]).sum())
+        ex, le = (pt[:C, 3] - ts[0]) / 1e3, (pt[:C, 0] - ts[0]) / 1e3
+        t_end = {"exit_max_us": round(float(ex.max()), 1), "exit_argmax": int(ex.argmax()),
+                 "exit_p50_us": round(float(np.median(ex)), 1), "large_end_max_us": round(float(le.max()), 1),
+                 "exit_top8": [(int(i), round(float(ex[i]), 1)) for i in np.argsort(-ex)[:8]]}
     ts = ts[ts > 0]
     times.sort()
     res["straddle" if straddle else "evict"] = {
         "us_median": times[len(times) // 2], "us_p10": times[len(times) // 10], "us_p90": times[9 * len(times) // 10],
-        "phase_us": [round(float(x), 1) for x in np.diff(ts) / 1e3], "rounds": int(ctl[48]), "levels": int(ctl[49]),
+        "phase_us": [round(float(x), 1) for x in np.diff(ts) / 1e3], "last_cta": t_end, "rounds": int(ctl[48]), "levels": int(ctl[49]),
         "records_small_large_big": [[int(ctl[l]), int(ctl[16 + l]), int(ctl[32 + l])] for l in range(int(ctl[49]) + 1)]}
 # launch + teardown cost: a call with nothing evictable returns after phase 0 and one barrier
 keys1 = torch.full((1 << 20,), -1, dtype=torch.int64, device=dev)
