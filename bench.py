@@ -349,8 +349,8 @@ def run_ours(args, rank, world, local):
             n += 2
         if ev is not None and gate_attn and not threaded:  # the attention pair follows the key pass
             stream.wait_event(ev_keys)
-        K.kv_append(pool, batch, rp["k_new"], rp["v_new"], rp["ws_app"], stream=stream)
-        plan = K.Plan(pool, batch, rp["ws_att"], stream=stream)
+        # kv_append + plan of the same descriptor in one library call (one validation)
+        plan = K.kv_append_plan(pool, batch, rp["k_new"], rp["v_new"], rp["ws_app"], rp["ws_att"], stream=stream)
         if plan_launches["n"] is None:  # the same descriptor every step: count once
             plan_launches["n"] = plan.launch_count()
         n += 2 + plan_launches["n"]
@@ -444,8 +444,7 @@ def run_ours(args, rank, world, local):
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done
         if ev is not None and gate_attn and not threaded:
             stream.wait_event(ev_keys)
-        K.kv_append(pool, batch, b["k"], b["v"], ws_app, stream=stream)
-        plan = K.Plan(pool, batch, ws_att, stream=stream)
+        plan = K.kv_append_plan(pool, batch, b["k"], b["v"], ws_app, ws_att, stream=stream)
         if plan_launches["n"] is None:  # the same descriptor every step: count once
             plan_launches["n"] = plan.launch_count()
         n += 2 + plan_launches["n"]
@@ -531,7 +530,14 @@ def run_ours(args, rank, world, local):
         clocks.start()
     launches["n"] = 0
     rot["i"] = 0
+    ring = None
+    if os.environ.get("KVA_BENCH_SPAN_RING") == "1":  # diagnostics: manager / selection spans
+        ring = torch.zeros(2 * 256 * 2, dtype=torch.int64, device=dev)
+        K.set_option("span_ring", ring.data_ptr())
     ms = timed(args.steps, time_kernels=True)
+    if ring is not None:
+        K.set_option("span_ring", 0)
+        _dump_timeline(ring, spans, span_used)
     gpu_launches = launches["n"]
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
     ms_same = None
@@ -723,6 +729,25 @@ def run_ours(args, rank, world, local):
                                     "stream; double-buffered device buffers; timed from the first input copy "
                                     "to the last result on the host"}
     return res, wl
+
+
+def _dump_timeline(ring, spans, used):
+    """stderr: one line per timed step — attention kernel spans and the manager / selection
+    launches (span_ring) that overlap it, us relative to the first step's first start."""
+    r = ring.cpu().numpy().view(np.uint64).reshape(2, 256, 2)
+    sp = spans.cpu().numpy().view(np.uint64)
+    ev = [("mgr", int(a), int(b)) for a, b in r[0] if a and b] + [("sel", int(a), int(b)) for a, b in r[1] if a and b]
+    att = []
+    for i in used:
+        for nm, j in (("dec", 0), ("tile", 2), ("merge", 4)):
+            if sp[i, j] != np.uint64(0xFFFFFFFFFFFFFFFF) and sp[i, j + 1] > 0:
+                att.append((f"{nm}{i}", int(sp[i, j]), int(sp[i, j + 1])))
+    if not att:
+        return
+    t0, t1 = min(a[1] for a in att), max(a[2] for a in att)
+    rows = sorted([e for e in ev if t0 - 200000 <= e[1] <= t1] + att, key=lambda e: e[1])
+    for nm, a, b in rows:
+        sys.stderr.write(f"[timeline] {nm:8s} {(a - t0) / 1e3:9.1f} {(b - t0) / 1e3:9.1f} {(b - a) / 1e3:7.1f}\n")
 
 
 def _post_append_batch(K, wl, dev):

@@ -21,7 +21,17 @@ int sm_count();
 
 // Tuning / diagnostics options (kva_set_option; process-wide, read at each call)
 enum Opt : int { kOptTileCtas = 0, kOptOverlap, kOptPdl, kOptEvictCtas, kOptHostProf, kOptDebugFlags, kOptDebugTs,
-                 kOptCount };
+                 kOptSpanRing, kOptCount };
+// span_ring (diagnostics): device u64 [2][256][2] — manager (0) / evict_select (1) launch i writes
+// [kind][i % 256] = {CTA 0 start, latest CTA end} (%globaltimer ns)
+unsigned long long *span_ring_slot(int kind);
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 int64_t opt(Opt o);
 
 constexpr int kBlock = 16;        // tokens per KV block (reading #5)

@@ -81,6 +81,7 @@ struct MgrArgs {
   int64_t del_len;
   uint64_t *keys;
   unsigned long long *n_active;
+  unsigned long long *span;  // diagnostics (span_ring): {CTA 0 start, latest CTA end}
 };
 
 __device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t la, uint32_t dp, unsigned &act) {
@@ -95,6 +96,7 @@ __device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t
 __global__ void __launch_bounds__(256) manager_kernel(const __grid_constant__ MgrArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (a.span && t0 == 0) a.span[0] = gtime();
   // phase 0
   if (a.recount) {
     const int64_t n4 = (reinterpret_cast<uintptr_t>(a.rc) & 15) ? 0 : a.n / 4;
@@ -176,6 +178,10 @@ __global__ void __launch_bounds__(256) manager_kernel(const __grid_constant__ Mg
     __syncthreads();
     if (threadIdx.x == 0 && s_act) atomicAdd(a.n_active, (unsigned long long)s_act);
   }
+  if (a.span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(a.span + 1, gtime());
+  }
 }
 
 cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth,
@@ -186,7 +192,7 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 cudaStream_t s) {
   MgrArgs a{state, rc, lat, depth, n, now, tr_ids, n_tr, tr_indptr, tr_state, n_chains, win,
             recount ? 1 : 0, pool_ids, pool_len, del_ids, del_len, keys,
-            reinterpret_cast<unsigned long long *>(n_active)};
+            reinterpret_cast<unsigned long long *>(n_active), span_ring_slot(0)};
   if (n <= 0 && n_active == nullptr) return cudaSuccess;
   // two 256-thread CTAs per SM (co-resident on an idle GPU: cooperative launch); every phase is
   // a grid-stride pass over <= 2^20 elements (a few per thread)

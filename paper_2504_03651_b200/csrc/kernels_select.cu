@@ -64,6 +64,7 @@ struct Ctl {
   unsigned long long t[32];  // phase timestamps of CTA 0 (%globaltimer ns; diagnostics)
   unsigned int n_small[kMaxLevels], n_large[kMaxLevels], n_big[kMaxLevels];
   unsigned int rounds, levels, pad[2];
+  unsigned long long v_prev;  // the varying-bit mask of the last call on this workspace
 };
 
 struct Layout {
@@ -105,6 +106,7 @@ struct SelArgs {
   uint64_t *sk[2];     // output-aligned staging ping-pong, [k + kCap]
   int32_t *si[2];
   uint4 *rs[2], *rl[2];  // bucket records (off, size, take, dig | src << 8): <= 256 / larger
+  unsigned long long *span;  // diagnostics (span_ring): {CTA 0 start, latest CTA end}
 };
 
 __device__ __forceinline__ bool pair_gt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
@@ -239,6 +241,7 @@ __device__ __forceinline__ void flush_counts(const unsigned *s_cnt, unsigned *s_
 // injection on the evictable keys), then idb id bits.  Segments, staging and buckets hold
 // (ck, id); only the input keys are compressed (once per pass over them).
 struct Comp {
+  unsigned long long v;  // the varying-bit mask it was made for
   int nr, idb, B, nd;
   unsigned long long cst;  // the key bits outside the runs (equal in every evictable key)
   unsigned long long mask[kMaxRuns];
@@ -249,6 +252,85 @@ struct Comp {
   unsigned long long m0[kMaxRuns];
   int s0[kMaxRuns];
 };
+// The composite layout for varying-bit mask V (cst is set by the caller): runs of V, most
+// significant first, gaps merged (smallest first) past kMaxRuns; any V gives a valid layout
+// for keys whose varying bits lie inside it.
+__device__ void make_comp(Comp &out, uint64_t V, int64_t n) {
+  // run i = bits [rlo[i], rhi[i]] (i = 0 most significant): the i-th highest of the runs'
+  // top bits (V & ~(V >> 1)) and bottom bits (V & ~(V << 1)); registers in the common case
+  int rlo[kMaxRuns], rhi[kMaxRuns];
+  int nr = __popcll(V & ~(V << 1));
+  if (nr <= kMaxRuns) {
+    uint64_t hs = V & ~(V >> 1), ls = V & ~(V << 1);
+#pragma unroll
+    for (int i = 0; i < kMaxRuns; ++i) {
+      rhi[i] = hs ? 63 - __clzll((long long)hs) : 0;
+      rlo[i] = ls ? 63 - __clzll((long long)ls) : 0;
+      if (hs) { hs &= ~(1ull << rhi[i]); ls &= ~(1ull << rlo[i]); }
+    }
+  } else {  // more runs than kept apart: merge the smallest gaps
+    int xl[32], xh[32], m = 0;
+    for (uint64_t rem = V; rem;) {
+      const int hb = 63 - __clzll((long long)rem);
+      const uint64_t zeros = hb ? (~rem & ((1ull << hb) - 1ull)) : 0ull;  // clear bits below hb
+      const int lb = zeros ? 64 - __clzll((long long)zeros) : 0;            // run = [lb, hb]
+      xh[m] = hb; xl[m] = lb; ++m;
+      rem &= lb ? ((1ull << lb) - 1ull) : 0ull;
+    }
+    while (m > kMaxRuns) {
+      int best = 0, gap = 1 << 30;
+      for (int i = 0; i + 1 < m; ++i) {
+        const int g = xl[i] - xh[i + 1];
+        if (g < gap) { gap = g; best = i; }
+      }
+      xl[best] = xl[best + 1];
+      for (int i = best + 1; i + 1 < m; ++i) { xl[i] = xl[i + 1]; xh[i] = xh[i + 1]; }
+      --m;
+    }
+    nr = m;
+#pragma unroll
+    for (int i = 0; i < kMaxRuns; ++i) { rlo[i] = xl[i]; rhi[i] = xh[i]; }
+  }
+  out.v = V;
+  out.nr = nr;
+  out.cst = 0ull;
+  int bits = 0;
+#pragma unroll
+  for (int i = kMaxRuns - 1; i >= 0; --i) {  // least significant run lands at bit 0
+    const int len = rhi[i] - rlo[i] + 1;
+    out.mask[i] = i < nr ? (len >= 64 ? ~0ull : ((1ull << len) - 1ull)) << rlo[i] : 0ull;
+    out.sh[i] = i < nr ? rlo[i] - bits : 0;
+    bits += i < nr ? len : 0;
+    out.m0[i] = 0ull;
+    out.s0[i] = 0;
+  }
+  const int idb = n <= 1 ? 0 : min(31, 64 - __clzll((long long)(n - 1)));
+  out.idb = idb;
+  const int B = bits + idb;
+  out.B = B;
+  out.nd = B > 0 ? (B + kDig - 1) / kDig : 1;
+  // digit-0 window [lo0, B) of the composite -> [wl, wh) of the compressed key
+  const int lo0 = B > kDig ? B - kDig : 0;
+  int n0 = -1;
+  if (lo0 >= idb) {
+    const int wl = lo0 - idb, wh = B - idb;
+    n0 = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxRuns; ++i) {  // run i: key bit j -> compressed bit j - sh[i]
+      if (i >= nr) break;
+      const int jl = wl + out.sh[i], jh = wh + out.sh[i];  // key bits [jl, jh) land in the window
+      if (jl >= 64) continue;
+      const uint64_t win = (jh >= 64 ? ~0ull : ((1ull << jh) - 1ull)) & ~((1ull << jl) - 1ull);
+      if (out.mask[i] & win) {
+        out.m0[n0] = out.mask[i] & win;
+        out.s0[n0] = jl;
+        ++n0;
+      }
+    }
+  }
+  out.n0 = n0;
+}
+
 // the first 4 runs in registers (the `evict` keys have 3: priority code, LAT, depth), the
 // rest read from shared memory
 struct CompR {
@@ -595,6 +677,13 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     ++tp;
   };
   stamp();
+  if (a.span && c == 0 && tid == 0) a.span[0] = gtime();
+  auto span_end = [&]() {
+    if (a.span) {
+      __syncthreads();
+      if (tid == 0) atomicMax(a.span + 1, gtime());
+    }
+  };
   const int64_t n = a.n;
   const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // even: 16-B aligned slices
   const int64_t lo = std::min<int64_t>(n, c * per), hi = std::min<int64_t>(n, lo + per);
@@ -649,17 +738,34 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
   };
 
   // ---------------- phase 0: which bits vary among the evictable keys, how many ----------------
+  // The pass also counts digit 0 speculatively, with the layout of the varying-bit mask the
+  // previous call on this workspace found (ctl->v_prev; any value is safe: the counts are used
+  // only when it equals this call's mask, else phase 1 counts again).
   {
+    if (tid == 0) make_comp(s_comp, __ldcg(&ctl->v_prev), n);
+    for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;
+    __syncthreads();
+    const Comp &cg0 = s_comp;
+    const Dig0R d0r = dig0_regs(cg0);
+    const CompR cr0 = comp_regs(cg0);
+    const DigSel ds0 = dig_sel(cg0, 0);
+    const bool raw0 = d0r.n0 >= 0;
     unsigned long long o = 0, an = 0, cn = 0;
-    for_slice([&](const uint64_t (&k4)[4], const int32_t (&)[4]) {
+    stamp();
+    for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
+      int d4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 4; ++u) {
         if (k4[u] != kInf) {
           o |= k4[u];
           an |= ~k4[u];
           ++cn;
         }
+        d4[u] = k4[u] == kInf ? -1 : raw0 ? digit0_raw(d0r, k4[u]) : digit(ds0, compress(cr0, k4[u]), i4[u]);
+      }
+      hist_batch<4>(s_cnt, d4);
     });
+    stamp();
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
       o |= __shfl_xor_sync(0xffffffffu, o, s);
@@ -686,6 +792,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
 
   // ---------------- phase 1: composite layout + digit-0 histogram ----------------
   unsigned long long E;
+  bool hit;
   {
     unsigned long long o = 0, an = 0, cn = 0;
     if (tid < C) {
@@ -704,77 +811,34 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       unsigned long long O = 0, A = 0, N = 0;
       for (int i = 0; i < kNW; ++i) { O |= s_red[0][i]; A |= s_red[1][i]; N += s_red[2][i]; }
       const uint64_t V = O & A;  // set in some evictable key and clear in another
-      // runs of set bits of V, most significant first; gaps merged (smallest first) past kMaxRuns
-      int rlo[32], rhi[32], nr = 0;
-      for (uint64_t rem = V; rem;) {
-        const int hb = 63 - __clzll((long long)rem);
-        const uint64_t zeros = hb ? (~rem & ((1ull << hb) - 1ull)) : 0ull;  // clear bits below hb
-        const int lb = zeros ? 64 - __clzll((long long)zeros) : 0;            // run = [lb, hb]
-        rhi[nr] = hb; rlo[nr] = lb; ++nr;
-        rem &= lb ? ((1ull << lb) - 1ull) : 0ull;
-      }
-      while (nr > kMaxRuns) {
-        int best = 0, gap = 1 << 30;
-        for (int i = 0; i + 1 < nr; ++i) {
-          const int g = rlo[i] - rhi[i + 1];
-          if (g < gap) { gap = g; best = i; }
-        }
-        rlo[best] = rlo[best + 1];
-        for (int i = best + 1; i + 1 < nr; ++i) { rlo[i] = rlo[i + 1]; rhi[i] = rhi[i + 1]; }
-        --nr;
-      }
-      Comp cp{};
-      cp.nr = nr;
-      int bits = 0;
-      for (int i = nr - 1; i >= 0; --i) {  // least significant run lands at bit 0
-        const int len = rhi[i] - rlo[i] + 1;
-        cp.mask[i] = (len >= 64 ? ~0ull : ((1ull << len) - 1ull)) << rlo[i];
-        cp.sh[i] = rlo[i] - bits;
-        bits += len;
-      }
+      const bool h = V == s_comp.v;
+      if (!h) make_comp(s_comp, V, n);
       unsigned long long mall = 0;
-      for (int i = 0; i < nr; ++i) mall |= cp.mask[i];
-      cp.cst = O & ~A & ~mall;
-      int idb = 0;
-      while (idb < 31 && ((int64_t)1 << idb) < n) ++idb;
-      cp.idb = idb;
-      cp.B = bits + idb;
-      cp.nd = cp.B > 0 ? (cp.B + kDig - 1) / kDig : 1;
-      {  // digit-0 window [lo, lo + w) of the composite -> [wl, wh) of the compressed key
-        const int lo0 = cp.B > kDig ? cp.B - kDig : 0;
-        cp.n0 = -1;
-        if (lo0 >= idb) {
-          const int wl = lo0 - idb, wh = cp.B - idb;
-          cp.n0 = 0;
-          for (int i = 0; i < nr; ++i) {  // run i: key bit j -> compressed bit j - sh[i]
-            const int jl = wl + cp.sh[i], jh = wh + cp.sh[i];  // key bits [jl, jh) land in the window
-            if (jl >= 64) continue;
-            const uint64_t win = (jh >= 64 ? ~0ull : ((1ull << jh) - 1ull)) & ~((1ull << jl) - 1ull);
-            if (cp.mask[i] & win) {
-              cp.m0[cp.n0] = cp.mask[i] & win;
-              cp.s0[cp.n0] = jl;
-              ++cp.n0;
-            }
-          }
-        }
-      }
-      s_comp = cp;
+      for (int i = 0; i < s_comp.nr; ++i) mall |= s_comp.mask[i];
+      s_comp.cst = O & ~A & ~mall;
       s_red[2][0] = N;
-      if (c == 0) *a.d_count = (int64_t)std::min<unsigned long long>(N, (unsigned long long)a.k);
+      s_red[1][0] = h ? 1ull : 0ull;
+      if (c == 0) {
+        *a.d_count = (int64_t)std::min<unsigned long long>(N, (unsigned long long)a.k);
+        ctl->v_prev = V;  // every CTA read the old value before the barrier
+      }
     }
     __syncthreads();
     E = s_red[2][0];
+    hit = s_red[1][0] != 0ull;
   }
-  if (E == 0) return;  // uniform: nothing evictable (*d_count = 0)
+  if (E == 0) {  // uniform: nothing evictable (*d_count = 0)
+    span_end();
+    return;
+  }
   const Comp &cp = s_comp;
   const CompR cr = comp_regs(cp);
-  {
+  if (!hit) {  // the layout changed: count digit 0 again
     for (int i = tid; i < kBins; i += kT) s_cnt[i] = 0u;
     const DigSel ds0 = dig_sel(cp, 0);
     __syncthreads();
     const Dig0R d0r = dig0_regs(cp);
     const bool raw0 = d0r.n0 >= 0;
-    stamp();
     for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
       int d4[4];
 #pragma unroll
@@ -783,9 +847,9 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
       hist_batch<4>(s_cnt, d4);
     });
     __syncthreads();
-    stamp();
-    flush_counts(s_cnt, s_off, a.hist);
   }
+  stamp();
+  flush_counts(s_cnt, s_off, a.hist);
   stamp();
   grid.sync();
   stamp();
@@ -1092,6 +1156,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     if (!more) {
       if (c == 0 && tid == 0) ctl->levels = (unsigned)(lv + 1);
       span_mark(true);
+      span_end();
       break;
     }
     grid.sync();
@@ -1115,6 +1180,7 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   a.out_ids = out_ids;
   a.d_count = d_count;
   a.free_bits = free_bits;
+  a.span = span_ring_slot(1);
   a.ctl = reinterpret_cast<Ctl *>(p + L.ctl);
   a.part = reinterpret_cast<Part *>(p + L.part);
   a.hist = reinterpret_cast<unsigned int *>(p + L.hist);

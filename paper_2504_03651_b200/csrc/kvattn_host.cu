@@ -125,8 +125,10 @@ struct OptDef {
 };
 // defaults = the measured best
 constexpr OptDef kOptDefs[kOptCount] = {{"tile_ctas", 0}, {"overlap", 1}, {"pdl", 1},   {"evict_ctas", 0},
-                                        {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0}};
-std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}};
+                                        {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0},
+                                        {"span_ring", 0}};
+std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}};
+std::atomic<unsigned> g_span_seq[2] = {{0}, {0}};
 int opt_index(const char *name) {
   if (!name) return -1;
   for (int i = 0; i < kOptCount; ++i)
@@ -135,6 +137,12 @@ int opt_index(const char *name) {
 }
 }  // namespace
 int64_t opt(Opt o) { return g_opt[o].load(std::memory_order_relaxed); }
+unsigned long long *span_ring_slot(int kind) {
+  const int64_t r = opt(kOptSpanRing);
+  if (!r) return nullptr;
+  const unsigned i = g_span_seq[kind].fetch_add(1u, std::memory_order_relaxed) & 255u;
+  return reinterpret_cast<unsigned long long *>(r) + ((size_t)kind * 256 + i) * 2;
+}
 }  // namespace kva
 extern "C" kva_status kva_set_option(const char *name, int64_t value) {
   const int i = kva::opt_index(name);
@@ -941,13 +949,15 @@ extern "C" kva_status hybrid_attention_workspace_size(const kva_batch_desc *b, s
   return KVA_OK;
 }
 
-extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b, void *ws,
-                                            size_t ws_bytes, kva_stream_t stream, kva_plan **out) {
+// validated = the caller has just validated the descriptor for attention (kv_append_plan:
+// kv_append checked the resident part and filled every new position's entry itself)
+static kva_status plan_impl(kva_pool *p, const kva_batch_desc *b, void *ws, size_t ws_bytes,
+                            kva_stream_t stream, kva_plan **out, bool validated) {
   if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
   *out = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   HSection hs;
-  kva_status st = validate_desc(p, b, 0);
+  kva_status st = validated ? KVA_OK : validate_desc(p, b, 0);
   hs.lap("plan.validate");
   if (st != KVA_OK) return st;
   const auto t1 = std::chrono::steady_clock::now();
@@ -1088,6 +1098,21 @@ extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b
   ap.part_lse = reinterpret_cast<float *>(dws + arrays + align256((size_t)pb.n_slots * b->head_dim * 4));
   *out = pl;
   return KVA_OK;
+}
+
+extern "C" kva_status hybrid_attention_plan(kva_pool *p, const kva_batch_desc *b, void *ws,
+                                            size_t ws_bytes, kva_stream_t stream, kva_plan **out) {
+  return plan_impl(p, b, ws, ws_bytes, stream, out, false);
+}
+
+extern "C" kva_status kv_append_plan(kva_pool *p, kva_batch_desc *b, const void *k_new, const void *v_new,
+                                     int64_t stride_tok, int32_t *deficit, void *ws_append, size_t ws_append_bytes,
+                                     void *ws_attn, size_t ws_attn_bytes, kva_stream_t stream, kva_plan **out) {
+  if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
+  *out = nullptr;
+  kva_status st = kv_append(p, b, k_new, v_new, stride_tok, deficit, ws_append, ws_append_bytes, stream);
+  if (st != KVA_OK) return st;
+  return plan_impl(p, b, ws_attn, ws_attn_bytes, stream, out, true);
 }
 
 extern "C" kva_status kva_plan_destroy(kva_plan *pl) {

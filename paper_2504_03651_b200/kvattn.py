@@ -69,7 +69,7 @@ class PlanStats(ctypes.Structure):
 
 EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_create", "kv_pool_destroy",
            "kv_pool_free_count", "kv_pool_resync", "kv_pool_sync", "kv_append_workspace_size", "kv_append",
-           "hybrid_attention_workspace_size", "hybrid_attention_plan", "hybrid_attention_run",
+           "hybrid_attention_workspace_size", "hybrid_attention_plan", "kv_append_plan", "hybrid_attention_run",
            "hybrid_attention_run_phases", "kva_plan_launch_count", "kva_plan_set_timing_events",
            "kva_plan_set_span_buffer", "kva_plan_set_outputs",
            "kva_plan_destroy",
@@ -113,6 +113,7 @@ def load(build_if_missing: bool = True):
         "hybrid_attention_workspace_size": ([P, P], ctypes.c_int),
         "hybrid_attention_plan": ([P, P, P, sz, P, P], ctypes.c_int),
         "hybrid_attention_run": ([P, P, i64, i64, P, i64, i64, i32, P, P], ctypes.c_int),
+        "kv_append_plan": ([P, P, P, P, i64, P, P, sz, P, sz, P, P], ctypes.c_int),
         "hybrid_attention_run_phases": ([P, P, i64, i64, P, i64, i64, i32, P, i32, P], ctypes.c_int),
         "kva_plan_launch_count": ([P, i32, P], ctypes.c_int),
         "kva_plan_set_timing_events": ([P, P, P, P, P], ctypes.c_int),
@@ -309,6 +310,26 @@ def kv_append(pool: Pool, batch: Batch, k_new: torch.Tensor, v_new: torch.Tensor
     return workspace
 
 
+def kv_append_plan(pool: Pool, batch: Batch, k_new: torch.Tensor, v_new: torch.Tensor,
+                   append_workspace: torch.Tensor | None = None, attn_workspace: torch.Tensor | None = None,
+                   stream=None) -> "Plan":
+    """kv_append + hybrid_attention_plan of the same descriptor in one library call (one
+    validation); returns the Plan.  Raises KvaError(NEEDS_EVICTION, deficit=...)."""
+    if append_workspace is None:
+        append_workspace = _workspace(kv_append_workspace_size(batch), k_new.device, stream)
+    if attn_workspace is None:
+        attn_workspace = _workspace(hybrid_attention_workspace_size(batch), k_new.device, stream)
+    deficit = ctypes.c_int32(0)
+    h = ctypes.c_void_p()
+    st = load().kv_append_plan(pool.handle, ctypes.byref(batch.desc()), _ptr(k_new), _ptr(v_new), k_new.stride(0),
+                               ctypes.byref(deficit), _ptr(append_workspace), append_workspace.numel(),
+                               _ptr(attn_workspace), attn_workspace.numel(), _stream(stream), ctypes.byref(h))
+    _check(st, deficit=deficit.value)
+    plan = Plan(pool, batch, attn_workspace, _handle=h)
+    plan.append_workspace = append_workspace
+    return plan
+
+
 def hybrid_attention_workspace_size(batch: Batch) -> int:
     n = ctypes.c_size_t()
     _check(load().hybrid_attention_workspace_size(ctypes.byref(batch.desc()), ctypes.byref(n)))
@@ -319,17 +340,19 @@ class Plan:
     """hybrid_attention_plan: work lists uploaded into `workspace`; reusable by run()."""
 
     def __init__(self, pool: Pool, batch: Batch, workspace: torch.Tensor | None = None, stream=None,
-                 device=None):
-        L = load()
+                 device=None, _handle=None):
         device = device or pool.k_pool.device
         if workspace is None:
             workspace = _workspace(hybrid_attention_workspace_size(batch), device, stream)
         self.workspace = workspace
         self.pool = pool  # the C plan uses the pool's side stream / events: keep it alive
-        self.handle = ctypes.c_void_p()
-        _check(L.hybrid_attention_plan(pool.handle, ctypes.byref(batch.desc()), _ptr(workspace),
-                                       workspace.numel(), _stream(stream), ctypes.byref(self.handle)))
         self.batch = batch
+        if _handle is not None:  # made by kv_append_plan
+            self.handle = _handle
+            return
+        self.handle = ctypes.c_void_p()
+        _check(load().hybrid_attention_plan(pool.handle, ctypes.byref(batch.desc()), _ptr(workspace),
+                                            workspace.numel(), _stream(stream), ctypes.byref(self.handle)))
 
     def stats(self) -> dict:
         s = PlanStats()

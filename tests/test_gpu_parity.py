@@ -416,3 +416,49 @@ def test_nested_group_errors():
         b["group_parent"] = np.array(parent, np.int32)
         batch = K.Batch(b, "cuda")
         assert K.validate_batch(batch, b["num_blocks"], 1) == expect, parent
+
+
+def _casc_small():
+    reqs = [W.ReqSpec(W.OFFLINE_DECODE, 40 * 16 + 5 + i, 1, 0) for i in range(40)]
+    reqs += [W.ReqSpec(W.ONLINE_DECODE, 300, 1), W.ReqSpec(W.OFFLINE_PREFILL, 40 * 16 + 100, 90, 0)]
+    return W.custom_config("casc", 20, 4, 128, 19, reqs, [40])
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "casc"])
+def test_append_plan_fused_matches_oracle(cfg):
+    """kv_append_plan (one call: append then plan the same descriptor, one validation) gives the
+    oracle's pool bytes, tables and attention; on NEEDS_EVICTION it makes no plan and changes
+    nothing (S:137)."""
+    import paper_2504_03651_b200 as K
+    wl = W.make_workload(cfg if cfg == "tiny" else _casc_small())
+    dev = "cuda"
+    kp, vp = wl.k_pool.to(dev).contiguous(), wl.v_pool.to(dev).contiguous()
+    fb = K.free_bits_tensor(wl.free_bits, dev)
+    pool = K.Pool(kp, vp, fb)
+    batch = K.Batch(wl.batch, dev)
+    plan = K.kv_append_plan(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+    q = wl.q.to(dev)
+    out = torch.full(q.shape, float("nan"), dtype=torch.float32, device=dev)
+    lse = torch.full(q.shape[:2], float("nan"), dtype=torch.float32, device=dev)
+    plan.run(q, out, lse)
+    torch.cuda.synchronize()
+    ref = oracle_step(wl)
+    assert np.array_equal(batch.table_dev.cpu().numpy(), ref["block_table"])
+    assert np.array_equal(bits16(kp), ref["k_pool"].view(np.uint16))
+    assert np.array_equal(fb.cpu().numpy().view(np.uint32), ref["free_bits"])
+    assert_attention_close(out, lse, ref["out"], ref["lse"])
+    plan.close()
+    # a pool with too few free blocks: NEEDS_EVICTION, nothing enqueued, no plan
+    bits = wl.free_bits.copy()
+    free = [b for b in range(wl.batch["num_blocks"]) if (int(bits[b // 32]) >> (b % 32)) & 1]
+    for blk in free[1:]:
+        bits[blk // 32] &= ~np.uint32(1 << (blk % 32))
+    kp2 = wl.k_pool.to(dev)
+    pool2 = K.Pool(kp2, wl.v_pool.to(dev), K.free_bits_tensor(bits, dev))
+    batch2 = K.Batch(wl.batch, dev)
+    with pytest.raises(K.KvaError) as ei:
+        K.kv_append_plan(pool2, batch2, wl.k_new.to(dev), wl.v_new.to(dev))
+    assert ei.value.status == K.NEEDS_EVICTION and ei.value.deficit > 0
+    torch.cuda.synchronize()
+    assert torch.equal(kp2.cpu().view(torch.int16), wl.k_pool.view(torch.int16))
+    assert np.array_equal(batch2.table_dev.cpu().numpy(), wl.batch["block_table"])
