@@ -284,7 +284,7 @@ def run_ours(args, rank, world, local):
     ev_fork, ev_join, ev_keys = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
     # the attention pair is launched after the manager's key pass, so the cooperative eviction
     # selection (next on its stream) is placed on the SMs before the decode kernel fills them
-    gate_attn = os.environ.get("KVA_BENCH_GATE", "1") == "1"
+    gate_attn = os.environ.get("KVA_BENCH_GATE", "0" if os.environ.get("KVA_BENCH_FUSED_MGR", "1") == "1" else "1") == "1"
     # The manager pass + selection of step i depend only on the block metadata (updated in order
     # on their own stream), not on step i-1's attention: by default they are not forked from the
     # main stream each step, so step i's metadata pass runs as soon as step i-1's selection
@@ -303,13 +303,22 @@ def run_ours(args, rank, world, local):
     import queue
     jobs, done = queue.SimpleQueue(), queue.SimpleQueue()
 
+    # the manager step and the selection as ONE cooperative kernel (kv_manager_step_select: the
+    # key pass feeds the selection directly); KVA_BENCH_FUSED_MGR=0: two launches
+    fused_mgr = os.environ.get("KVA_BENCH_FUSED_MGR", "1") == "1"
+
     def evict_enqueue(ev, fork):
         if fork:
             ev_stream.wait_event(ev_fork)
-        keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
-                         stream=ev_stream)
-        ev_keys.record(ev_stream)
-        K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream, sync=False)
+        if fused_mgr:
+            ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
+                      stream=ev_stream, select=(ev["k"], ev["ids"], ev["ws"]))
+            ev_keys.record(ev_stream)
+        else:
+            keys = ev["mgr"](1 << 20, ev["chains"], ev["pool_ids"], del_ids=ev["del_ids"], recount=False,
+                             stream=ev_stream)
+            ev_keys.record(ev_stream)
+            K.evict_select(keys, ev["k"], out_ids=ev["ids"], workspace=ev["ws"], stream=ev_stream, sync=False)
         ev_join.record(ev_stream)
 
     def evict_worker():
@@ -346,7 +355,7 @@ def run_ours(args, rank, world, local):
                 jobs.put((ev, fork))
             else:
                 evict_enqueue(ev, fork)
-            n += 2
+            n += 1 if fused_mgr else 2
         if ev is not None and gate_attn and not threaded:  # the attention pair follows the key pass
             stream.wait_event(ev_keys)
         # kv_append + plan of the same descriptor in one library call (one validation)
@@ -438,7 +447,7 @@ def run_ours(args, rank, world, local):
                 jobs.put((ev, fork))
             else:
                 evict_enqueue(ev, fork)
-            n += 2
+            n += 1 if fused_mgr else 2
         stream.wait_event(ev_in[i % 2])
         if i >= 2:
             stream.wait_event(ev_out[i % 2])   # the host copy of this buffer's last result is done

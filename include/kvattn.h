@@ -345,6 +345,19 @@ kva_status kv_manager_step_workspace_size(const kva_block_meta *meta, const kva_
 kva_status kv_manager_step(const kva_block_meta *meta, const kva_manager_update *u,
                            uint64_t *keys_out, int64_t *n_active, void *workspace,
                            size_t workspace_bytes, kva_stream_t stream);
+/* kv_manager_step followed by evict_select(keys_out, num_blocks, k, out_ids, n_selected = NULL,
+ * apply = 0) — the KV manager's per-iteration pass and its victim order —
+ * as ONE cooperative kernel: the manager's key pass writes keys_out and feeds the selection's
+ * first pass directly (one launch and one pass over the keys fewer).  Results are identical to
+ * the two calls in sequence (keys_out, *n_active, the metadata updates, out_ids[0, min(k, E)));
+ * the selected count is left on the device in the first 8 bytes of sel_workspace (int64), as
+ * with evict_select's asynchronous mode.  workspace: kv_manager_step_workspace_size();
+ * sel_workspace: evict_select_workspace_size(num_blocks, k).  k == 0: the manager step alone.
+ * Errors: those of the two calls (validation before anything is enqueued). */
+kva_status kv_manager_step_select(const kva_block_meta *meta, const kva_manager_update *u,
+                                  uint64_t *keys_out, int64_t *n_active, void *workspace,
+                                  size_t workspace_bytes, int64_t k, int32_t *out_ids,
+                                  void *sel_workspace, size_t sel_workspace_bytes, kva_stream_t stream);
 /* Burst-reserve threshold for kv_append.  threshold_blocks
  * < 0 disables it (default); 0 <= threshold <= num_blocks else KVA_ERR_INVALID.  With a
  * threshold, kv_append first checks capacity (KVA_NEEDS_EVICTION, deficit = need - free),

@@ -168,12 +168,108 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 int32_t *win, bool recount, const int32_t *pool_ids, int64_t pool_len,
                                 const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
                                 cudaStream_t s);
+
+// KV-manager step arguments (kernels_evict.cu manager_kernel; kernels_select.cu runs the same
+// phases ahead of the selection when fused, kv_manager_step_select)
+struct MgrArgs {
+  uint8_t *state;
+  uint32_t *rc, *lat;
+  const uint16_t *depth;
+  int64_t n;
+  uint32_t now;
+  const int32_t *tr_ids;
+  int64_t n_tr;
+  const int32_t *tr_indptr;
+  const uint8_t *tr_state;
+  int32_t n_chains;
+  int32_t *win;
+  int32_t recount;
+  const int32_t *pool_ids;
+  int64_t pool_len;
+  const int32_t *del_ids;
+  int64_t del_len;
+  uint64_t *keys;
+  unsigned long long *n_active;
+  unsigned long long *span;  // diagnostics (span_ring): {CTA 0 start, latest CTA end}
+};
+inline MgrArgs make_mgr_args(uint8_t *state, uint32_t *rc, uint32_t *lat, const uint16_t *depth, int64_t n,
+                             uint32_t now, const int32_t *tr_ids, int64_t n_tr, const int32_t *tr_indptr,
+                             const uint8_t *tr_state, int32_t n_chains, int32_t *win, bool recount,
+                             const int32_t *pool_ids, int64_t pool_len, const int32_t *del_ids, int64_t del_len,
+                             uint64_t *keys, int64_t *n_active) {
+  return MgrArgs{state, rc, lat, depth, n, now, tr_ids, n_tr, tr_indptr, tr_state, n_chains, win,
+                 recount ? 1 : 0, pool_ids, pool_len, del_ids, del_len, keys,
+                 reinterpret_cast<unsigned long long *>(n_active), nullptr};
+}
+#ifdef __CUDACC__
+// the eviction key of one block (evict_keys' encoding, readings #18-#20) + the active count
+__device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t la, uint32_t dp, unsigned &act) {
+  act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
+  if (s == 0 || s == 1 || s == 2 || s > 5) return ~0ull;
+  uint64_t code;
+  if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
+  else code = (s == 4) ? 1ull : 0ull;
+  return (code << 48) | ((uint64_t)la << 16) | (0xFFFFull - (uint64_t)dp);
+}
+// Manager phases 0-2 over thread t0 of nt (grid-stride), sync() = a grid barrier:
+//   phase 0  rc = 0 (recount), win[id] = -1 for listed ids, *n_active = 0
+//   phase 1  win[id] = max element index listing id ("last chain wins", reading R36)
+//   phase 2  winners apply (state, lat = now); rc += pool chains, -= deleted chains
+// Ends with a barrier when phase 2 had work (phase 3, the keys, reads what it wrote).
+template <class Sync>
+__device__ __forceinline__ void manager_phases(const MgrArgs &a, int64_t t0, int64_t nt, Sync &&sync) {
+  if (a.recount) {
+    const int64_t n4 = (reinterpret_cast<uintptr_t>(a.rc) & 15) ? 0 : a.n / 4;
+    for (int64_t q = t0; q < n4; q += nt) reinterpret_cast<uint4 *>(a.rc)[q] = make_uint4(0, 0, 0, 0);
+    for (int64_t b = 4 * n4 + t0; b < a.n; b += nt) a.rc[b] = 0u;
+  }
+  // transition ids outside [0, n) (possible only for device-resident chains, which the host
+  // does not check) are skipped in every phase
+  for (int64_t e = t0; e < a.n_tr; e += nt) {
+    const int32_t id = a.tr_ids[e];
+    if ((uint32_t)id < (uint64_t)a.n) a.win[id] = -1;
+  }
+  if (a.n_active && t0 == 0) *a.n_active = 0ull;
+  sync();  // (also orders the n_active reset before phase 3's adds)
+  if (a.n_tr > 0) {
+    for (int64_t e = t0; e < a.n_tr; e += nt) {
+      const int32_t id = a.tr_ids[e];
+      if ((uint32_t)id < (uint64_t)a.n) atomicMax(&a.win[id], (int32_t)e);
+    }
+    sync();
+  }
+  const int64_t m = a.n_tr + a.pool_len + a.del_len;
+  for (int64_t e = t0; e < m; e += nt) {
+    if (e < a.n_tr) {
+      const int32_t id = a.tr_ids[e];
+      if ((uint32_t)id >= (uint64_t)a.n || a.win[id] != (int32_t)e) continue;  // out of range / a later chain lists it
+      int lo = 0, hi = a.n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.tr_indptr[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      a.state[id] = a.tr_state[lo];
+      a.lat[id] = a.now;
+    } else if (e < a.n_tr + a.pool_len) {
+      const int32_t id = a.pool_ids[e - a.n_tr];
+      if ((uint64_t)id < (uint64_t)a.n) atomicAdd(&a.rc[id], 1u);
+    } else {
+      const int32_t id = a.del_ids[e - a.n_tr - a.pool_len];
+      if ((uint64_t)id < (uint64_t)a.n) atomicSub(&a.rc[id], 1u);
+    }
+  }
+  if (m > 0) sync();
+}
+#endif
 size_t evict_select_ws_bytes(int64_t n, int64_t k);
 // evict_select: one cooperative kernel of `ctas` CTAs (<= 0: #SMs / 2); free_bits != nullptr:
 // the selected blocks are also marked free (apply)
+// mgr != nullptr: the manager step runs first in the same kernel (its keys pass writes
+// mgr->keys == keys and feeds the selection's first pass: kv_manager_step_select)
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
-                                int ctas, cudaStream_t s);
+                                int ctas, cudaStream_t s, const MgrArgs *mgr = nullptr);
 constexpr int kReleaseBatch = 3800;  // ids (+ table entries) per release launch (kernel parameter)
 // free bits of ids_host[0, n) set; tbl_host != nullptr: table[tbl_host[i]] = -1 as well
 cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,

@@ -62,86 +62,11 @@ cudaError_t launch_evict_keys(const uint8_t *state, const uint32_t *rc, const ui
 //   phase 1  win[id] = max element index listing id
 //   phase 2  winners apply (state, lat = now); rc += pool chains, -= deleted chains
 //   phase 3  keys (evict_keys' encoding) + active count
-struct MgrArgs {
-  uint8_t *state;
-  uint32_t *rc, *lat;
-  const uint16_t *depth;
-  int64_t n;
-  uint32_t now;
-  const int32_t *tr_ids;
-  int64_t n_tr;
-  const int32_t *tr_indptr;
-  const uint8_t *tr_state;
-  int32_t n_chains;
-  int32_t *win;
-  int32_t recount;
-  const int32_t *pool_ids;
-  int64_t pool_len;
-  const int32_t *del_ids;
-  int64_t del_len;
-  uint64_t *keys;
-  unsigned long long *n_active;
-  unsigned long long *span;  // diagnostics (span_ring): {CTA 0 start, latest CTA end}
-};
-
-__device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t la, uint32_t dp, unsigned &act) {
-  act += (s == 1 || s == 2 || (s >= 3 && s <= 5 && r > 0)) ? 1u : 0u;
-  if (s == 0 || s == 1 || s == 2 || s > 5) return kInf;
-  uint64_t code;
-  if (r > 0) code = r >= 0x7FFFu ? 0xFFFEull : 2ull * r;
-  else code = (s == 4) ? 1ull : 0ull;
-  return (code << 48) | ((uint64_t)la << 16) | (0xFFFFull - (uint64_t)dp);
-}
-
 __global__ void __launch_bounds__(256) manager_kernel(const __grid_constant__ MgrArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
   if (a.span && t0 == 0) a.span[0] = gtime();
-  // phase 0
-  if (a.recount) {
-    const int64_t n4 = (reinterpret_cast<uintptr_t>(a.rc) & 15) ? 0 : a.n / 4;
-    for (int64_t q = t0; q < n4; q += nt) reinterpret_cast<uint4 *>(a.rc)[q] = make_uint4(0, 0, 0, 0);
-    for (int64_t b = 4 * n4 + t0; b < a.n; b += nt) a.rc[b] = 0u;
-  }
-  // transition ids outside [0, n) (possible only for device-resident chains, which the host
-  // does not check) are skipped in every phase
-  for (int64_t e = t0; e < a.n_tr; e += nt) {
-    const int32_t id = a.tr_ids[e];
-    if ((uint32_t)id < (uint64_t)a.n) a.win[id] = -1;
-  }
-  if (a.n_active && t0 == 0) *a.n_active = 0ull;
-  grid.sync();  // (also orders the n_active reset before phase 3's adds)
-  // phase 1
-  if (a.n_tr > 0) {
-    for (int64_t e = t0; e < a.n_tr; e += nt) {
-      const int32_t id = a.tr_ids[e];
-      if ((uint32_t)id < (uint64_t)a.n) atomicMax(&a.win[id], (int32_t)e);
-    }
-    grid.sync();
-  }
-  // phase 2
-  const int64_t m = a.n_tr + a.pool_len + a.del_len;
-  for (int64_t e = t0; e < m; e += nt) {
-    if (e < a.n_tr) {
-      const int32_t id = a.tr_ids[e];
-      if ((uint32_t)id >= (uint64_t)a.n || a.win[id] != (int32_t)e) continue;  // out of range / a later chain lists it
-      int lo = 0, hi = a.n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (a.tr_indptr[mid] <= e) lo = mid;
-        else hi = mid - 1;
-      }
-      a.state[id] = a.tr_state[lo];
-      a.lat[id] = a.now;
-    } else if (e < a.n_tr + a.pool_len) {
-      const int32_t id = a.pool_ids[e - a.n_tr];
-      if ((uint64_t)id < (uint64_t)a.n) atomicAdd(&a.rc[id], 1u);
-    } else {
-      const int32_t id = a.del_ids[e - a.n_tr - a.pool_len];
-      if ((uint64_t)id < (uint64_t)a.n) atomicSub(&a.rc[id], 1u);
-    }
-  }
-  if (m > 0) grid.sync();
+  manager_phases(a, t0, nt, [&] { grid.sync(); });
   // phase 3: 4 blocks per thread with vector loads/stores when the arrays allow it (torch
   // allocations are 256-B aligned), scalar tail
   unsigned act = 0;
@@ -190,9 +115,9 @@ cudaError_t launch_manager_step(uint8_t *state, uint32_t *rc, uint32_t *lat, con
                                 int32_t *win, bool recount, const int32_t *pool_ids, int64_t pool_len,
                                 const int32_t *del_ids, int64_t del_len, uint64_t *keys, int64_t *n_active,
                                 cudaStream_t s) {
-  MgrArgs a{state, rc, lat, depth, n, now, tr_ids, n_tr, tr_indptr, tr_state, n_chains, win,
-            recount ? 1 : 0, pool_ids, pool_len, del_ids, del_len, keys,
-            reinterpret_cast<unsigned long long *>(n_active), span_ring_slot(0)};
+  MgrArgs a = make_mgr_args(state, rc, lat, depth, n, now, tr_ids, n_tr, tr_indptr, tr_state, n_chains, win,
+                            recount, pool_ids, pool_len, del_ids, del_len, keys, n_active);
+  a.span = span_ring_slot(0);
   if (n <= 0 && n_active == nullptr) return cudaSuccess;
   // two 256-thread CTAs per SM (co-resident on an idle GPU: cooperative launch); every phase is
   // a grid-stride pass over <= 2^20 elements (a few per thread)

@@ -107,6 +107,8 @@ struct SelArgs {
   int32_t *si[2];
   uint4 *rs[2], *rl[2];  // bucket records (off, size, take, dig | src << 8): <= 256 / larger
   unsigned long long *span;  // diagnostics (span_ring): {CTA 0 start, latest CTA end}
+  int fused;                 // the manager step runs first (mgr; its keys pass is phase 0's input)
+  MgrArgs mgr;
 };
 
 __device__ __forceinline__ bool pair_gt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
@@ -685,7 +687,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     }
   };
   const int64_t n = a.n;
-  const int64_t per = (((n + C - 1) / C) + 1) & ~1ll;  // even: 16-B aligned slices
+  const int64_t per = (((n + C - 1) / C) + 3) & ~3ll;  // multiple of 4: 16-B aligned key / metadata slices
   const int64_t lo = std::min<int64_t>(n, c * per), hi = std::min<int64_t>(n, lo + per);
   const bool vec = (reinterpret_cast<uintptr_t>(a.keys) & 15) == 0;
 
@@ -737,6 +739,10 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     }
   };
 
+  if (a.fused) {  // the KV-manager step's phases 0-2 (internal.h), then its keys pass in phase 0
+    manager_phases(a.mgr, (int64_t)c * kT + tid, (int64_t)C * kT, [&] { grid.sync(); });
+    stamp();
+  }
   // ---------------- phase 0: which bits vary among the evictable keys, how many ----------------
   // The pass also counts digit 0 speculatively, with the layout of the varying-bit mask the
   // previous call on this workspace found (ctl->v_prev; any value is safe: the counts are used
@@ -752,7 +758,7 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
     const bool raw0 = d0r.n0 >= 0;
     unsigned long long o = 0, an = 0, cn = 0;
     stamp();
-    for_slice([&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
+    auto acc = [&](const uint64_t (&k4)[4], const int32_t (&i4)[4]) {
       int d4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -764,7 +770,55 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
         d4[u] = k4[u] == kInf ? -1 : raw0 ? digit0_raw(d0r, k4[u]) : digit(ds0, compress(cr0, k4[u]), i4[u]);
       }
       hist_batch<4>(s_cnt, d4);
-    });
+    };
+    if (a.fused) {  // the manager's keys pass over this CTA's slice, feeding the statistics
+      const MgrArgs &m = a.mgr;
+      uint64_t *keys_out = m.keys;
+      unsigned act = 0;
+      const bool mvec = (lo & 3) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(m.state) | reinterpret_cast<uintptr_t>(m.rc) |
+                          reinterpret_cast<uintptr_t>(m.lat) | reinterpret_cast<uintptr_t>(keys_out) |
+                          (m.depth ? reinterpret_cast<uintptr_t>(m.depth) : 0)) & 15) == 0;
+      const int64_t q0 = lo >> 2, q1 = mvec ? (hi >> 2) : q0;
+      for (int64_t base = q0; base < q1; base += kT) {  // 4 blocks per lane, vector loads / stores
+        const int64_t q = base + tid;
+        uint64_t k4[4] = {kInf, kInf, kInf, kInf};
+        int32_t i4[4];
+        if (q < q1) {
+          const uint32_t s4 = __ldcg(reinterpret_cast<const uint32_t *>(m.state) + q);
+          const uint4 r4 = __ldcg(reinterpret_cast<const uint4 *>(m.rc) + q);
+          const uint4 l4 = __ldcg(reinterpret_cast<const uint4 *>(m.lat) + q);
+          uint2 dd = make_uint2(0u, 0u);
+          if (m.depth) dd = __ldcg(reinterpret_cast<const uint2 *>(m.depth) + q);
+          k4[0] = manager_key(s4 & 0xFF, r4.x, l4.x, dd.x & 0xFFFF, act);
+          k4[1] = manager_key((s4 >> 8) & 0xFF, r4.y, l4.y, dd.x >> 16, act);
+          k4[2] = manager_key((s4 >> 16) & 0xFF, r4.z, l4.z, dd.y & 0xFFFF, act);
+          k4[3] = manager_key(s4 >> 24, r4.w, l4.w, dd.y >> 16, act);
+          reinterpret_cast<ulonglong2 *>(keys_out)[2 * q] = make_ulonglong2(k4[0], k4[1]);
+          reinterpret_cast<ulonglong2 *>(keys_out)[2 * q + 1] = make_ulonglong2(k4[2], k4[3]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) i4[u] = (int32_t)(4 * q + u);
+        acc(k4, i4);
+      }
+      for (int64_t b0 = std::max<int64_t>(lo, 4 * q1); b0 < hi; b0 += kT) {  // scalar rest of the slice
+        const int64_t i = b0 + tid;
+        uint64_t k4[4] = {kInf, kInf, kInf, kInf};
+        const int32_t i4[4] = {(int32_t)i, (int32_t)i, (int32_t)i, (int32_t)i};
+        if (i < hi) {
+          k4[0] = manager_key(__ldcg(m.state + i), __ldcg(m.rc + i), __ldcg(m.lat + i), m.depth ? m.depth[i] : 0u, act);
+          keys_out[i] = k4[0];
+        }
+        acc(k4, i4);
+      }
+      if (m.n_active) {  // one atomic per warp
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) act += __shfl_xor_sync(0xffffffffu, act, s);
+        if (lane == 0 && act) atomicAdd(m.n_active, (unsigned long long)act);
+      }
+    } else {
+      for_slice(acc);
+    }
     stamp();
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
@@ -1169,7 +1223,8 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
 size_t evict_select_ws_bytes(int64_t n, int64_t k) { return layout(n, k).total; }
 
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids, int64_t *d_count,
-                                uint32_t *free_bits, void *ws, size_t ws_bytes, int ctas, cudaStream_t s) {
+                                uint32_t *free_bits, void *ws, size_t ws_bytes, int ctas, cudaStream_t s,
+                                const MgrArgs *mgr) {
   const Layout L = layout(n, k);
   if (ws_bytes < L.total) return cudaErrorInvalidValue;
   uint8_t *p = static_cast<uint8_t *>(ws);
@@ -1181,6 +1236,8 @@ cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int3
   a.d_count = d_count;
   a.free_bits = free_bits;
   a.span = span_ring_slot(1);
+  a.fused = mgr != nullptr;
+  if (mgr) a.mgr = *mgr;
   a.ctl = reinterpret_cast<Ctl *>(p + L.ctl);
   a.part = reinterpret_cast<Part *>(p + L.part);
   a.hist = reinterpret_cast<unsigned int *>(p + L.hist);

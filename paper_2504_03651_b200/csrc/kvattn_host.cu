@@ -1454,8 +1454,17 @@ extern "C" kva_status kv_manager_step_workspace_size(const kva_block_meta *m, co
   return KVA_OK;
 }
 
-extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys,
-                                      int64_t *n_active, void *ws, size_t ws_bytes, kva_stream_t stream) {
+namespace {
+struct MgrPrep {
+  const int32_t *d_ids = nullptr, *d_ind = nullptr;
+  const uint8_t *d_st = nullptr;
+  int32_t *win = nullptr;
+  int64_t tot = 0;
+  int32_t nc = 0;
+};
+// validation + (host chains) the upload of the raw chains into the workspace
+kva_status manager_prepare(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys, void *ws,
+                           size_t ws_bytes, cudaStream_t s, MgrPrep &o) {
   int64_t tot = 0;
   HSection hs;
   kva_status st = manager_validate(m, u, &tot);
@@ -1467,16 +1476,19 @@ extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager
   if (tot > 0 && (!ws || ws_bytes < need))
     return fail(KVA_ERR_INVALID, "kv_manager_step workspace too small (%zu < %zu)", ws_bytes, need);
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(KVA_ERR_INVALID, "workspace must be 256-B aligned");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t *w = static_cast<uint8_t *>(ws);
   const size_t o_ind = align256((size_t)tot * 4), o_st = o_ind + align256((size_t)(nc + 1) * 4);
   const size_t o_win = o_st + align256((size_t)nc + 1);
-  const int32_t *d_ids = reinterpret_cast<const int32_t *>(w), *d_ind = reinterpret_cast<const int32_t *>(w + o_ind);
-  const uint8_t *d_st = w + o_st;
+  o.d_ids = reinterpret_cast<const int32_t *>(w);
+  o.d_ind = reinterpret_cast<const int32_t *>(w + o_ind);
+  o.d_st = w + o_st;
+  o.win = reinterpret_cast<int32_t *>(w + o_win);
+  o.tot = tot;
+  o.nc = nc;
   if (u->chains_on_device) {
-    d_ids = u->chain_ids;
-    d_ind = u->chain_indptr;
-    d_st = u->chain_state;
+    o.d_ids = u->chain_ids;
+    o.d_ind = u->chain_indptr;
+    o.d_st = u->chain_state;
   } else if (tot > 0) {  // upload the raw chains (no per-element host work beyond validation)
     std::lock_guard<std::mutex> lk(g_mgr_mu);
     Staging::Slot *slot = nullptr;
@@ -1488,9 +1500,47 @@ extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager
     CUDA_TRY(g_mgr_staging.upload(slot, ws, o_st + nc, s));
   }
   hs.lap("manager.upload");
-  CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now, d_ids, tot, d_ind, d_st, nc,
-                               reinterpret_cast<int32_t *>(w + o_win), u->recount != 0, u->pool_ids,
-                               u->pool_len, u->del_ids, u->del_len, keys, n_active, s));
+  return KVA_OK;
+}
+}  // namespace
+
+extern "C" kva_status kv_manager_step(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys,
+                                      int64_t *n_active, void *ws, size_t ws_bytes, kva_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  MgrPrep o;
+  if (kva_status st = manager_prepare(m, u, keys, ws, ws_bytes, s, o); st != KVA_OK) return st;
+  HSection hs;
+  CUDA_TRY(launch_manager_step(m->state, m->rc, m->lat, m->depth, m->num_blocks, u->now, o.d_ids, o.tot, o.d_ind,
+                               o.d_st, o.nc, o.win, u->recount != 0, u->pool_ids, u->pool_len, u->del_ids,
+                               u->del_len, keys, n_active, s));
+  hs.lap("manager.launch");
+  return KVA_OK;
+}
+
+extern "C" kva_status kv_manager_step_select(const kva_block_meta *m, const kva_manager_update *u, uint64_t *keys,
+                                             int64_t *n_active, void *ws, size_t ws_bytes, int64_t k,
+                                             int32_t *out_ids, void *sel_ws, size_t sel_ws_bytes,
+                                             kva_stream_t stream) {
+  if (!m) return fail(KVA_ERR_INVALID, "null argument");
+  const int64_t n = m->num_blocks;
+  if (k < 0) return fail(KVA_ERR_INVALID, "k must be >= 0");
+  if (n >= (1ll << 31)) return fail(KVA_ERR_UNSUPPORTED, "n >= 2^31");
+  if (k > 0 && n > 0 && !out_ids) return fail(KVA_ERR_INVALID, "out_ids required");
+  const size_t need = evict_select_ws_bytes(n, k) + 256;
+  if (!sel_ws || sel_ws_bytes < need)
+    return fail(KVA_ERR_INVALID, "selection workspace too small (%zu < %zu)", sel_ws_bytes, need);
+  if (k == 0 || n == 0)  // nothing to select: the manager step alone
+    return kv_manager_step(m, u, keys, n_active, ws, ws_bytes, stream);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  MgrPrep o;
+  if (kva_status st = manager_prepare(m, u, keys, ws, ws_bytes, s, o); st != KVA_OK) return st;
+  HSection hs;
+  MgrArgs ma = make_mgr_args(m->state, m->rc, m->lat, m->depth, n, u->now, o.d_ids, o.tot, o.d_ind, o.d_st, o.nc,
+                             o.win, u->recount != 0, u->pool_ids, u->pool_len, u->del_ids, u->del_len, keys,
+                             n_active);
+  uint8_t *w = static_cast<uint8_t *>(sel_ws);
+  CUDA_TRY(launch_evict_select(keys, n, k, out_ids, reinterpret_cast<int64_t *>(w), nullptr, w + 256,
+                               sel_ws_bytes - 256, (int)opt(kOptEvictCtas), s, &ma));
   hs.lap("manager.launch");
   return KVA_OK;
 }

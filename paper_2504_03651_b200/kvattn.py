@@ -75,7 +75,7 @@ EXPORTS = ["kva_last_error", "kva_version", "kva_validate_batch", "kv_pool_creat
            "kva_plan_destroy",
            "kva_plan_get_stats", "hybrid_attention", "kv_release_blocks", "kv_truncate", "evict_keys",
            "evict_select_workspace_size", "evict_select", "kva_diag_occupy", "kv_pool_set_threshold",
-           "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step",
+           "kv_pool_set_active_blocks", "kv_manager_step_workspace_size", "kv_manager_step", "kv_manager_step_select",
            "kva_prefix_index_create", "kva_prefix_index_destroy", "kva_prefix_insert", "kva_prefix_lookup",
            "kva_prefix_remove", "kva_prefix_size", "kva_group_batch", "kva_group_batch_nested",
            "kva_set_option", "kva_get_option"]
@@ -132,6 +132,7 @@ def load(build_if_missing: bool = True):
         "kv_pool_set_active_blocks": ([P, i64], ctypes.c_int),
         "kv_manager_step_workspace_size": ([P, P, P], ctypes.c_int),
         "kv_manager_step": ([P, P, P, P, P, sz, P], ctypes.c_int),
+        "kv_manager_step_select": ([P, P, P, P, P, sz, i64, P, P, sz, P], ctypes.c_int),
         "kva_prefix_index_create": ([P], ctypes.c_int),
         "kva_prefix_index_destroy": ([P], ctypes.c_int),
         "kva_prefix_insert": ([P, P, i64, P, ctypes.c_uint32], ctypes.c_int),
@@ -482,10 +483,12 @@ class ManagerStep:
         return ci, cids, cst
 
     def __call__(self, now: int, chains, pool_ids: torch.Tensor | None, del_ids: torch.Tensor | None = None,
-                 recount: bool = True, stream=None):
+                 recount: bool = True, stream=None, select=None):
         """chains: [(state, ids-array), ...] or a chains_csr() tuple (host); pool_ids: device
         int32 (recount: every pool chain; incremental: the chains that joined), del_ids: device
-        int32 (incremental: the chains that left)."""
+        int32 (incremental: the chains that left).  select = (k, out_ids, sel_workspace): the
+        eviction order of the new keys in the same kernel (kv_manager_step_select; the count
+        stays on the device in sel_workspace[:8])."""
         ci, cids, cst = chains if isinstance(chains, tuple) else self.chains_csr(chains)
         plen = pool_ids.numel() if pool_ids is not None else 0
         dlen = del_ids.numel() if del_ids is not None else 0
@@ -511,8 +514,14 @@ class ManagerStep:
         u.recount = 1 if recount else 0
         if self.ws.numel() < need_b:
             self.ws = torch.empty(need_b, dtype=torch.uint8, device=self.state.device)
-        _check(L.kv_manager_step(ctypes.byref(self.meta), ctypes.byref(u), _ptr(self.keys), _ptr(self.n_active),
-                                 _ptr(self.ws), self.ws.numel(), _stream(stream)))
+        if select is None:
+            _check(L.kv_manager_step(ctypes.byref(self.meta), ctypes.byref(u), _ptr(self.keys), _ptr(self.n_active),
+                                     _ptr(self.ws), self.ws.numel(), _stream(stream)))
+            return self.keys
+        k, out_ids, sel_ws = select
+        _check(L.kv_manager_step_select(ctypes.byref(self.meta), ctypes.byref(u), _ptr(self.keys),
+                                        _ptr(self.n_active), _ptr(self.ws), self.ws.numel(), int(k), _ptr(out_ids),
+                                        _ptr(sel_ws), sel_ws.numel(), _stream(stream)))
         return self.keys
 
 

@@ -182,3 +182,68 @@ def test_manager_device_resident_chains(seed):
     assert np.array_equal(_u32(d_rc), rc) and np.array_equal(_u32(d_lat), lat)
     assert np.array_equal(keys.cpu().numpy().view(np.uint64), rkeys)
     assert int(mgr.n_active.item()) == nact
+
+
+def _fused_select(mgr, now, chains, pool_ids, k, n, **kw):
+    ids = torch.full((max(k, 1),), -7, dtype=torch.int32, device="cuda")
+    ws = torch.empty(K.evict_select_workspace_size(n, k), dtype=torch.uint8, device="cuda")
+    keys = mgr(now, chains, pool_ids, select=(k, ids, ws), **kw)
+    torch.cuda.synchronize()
+    return keys, ids, int(ws[:8].view(torch.int64).item())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_manager_step_select_fused_random(seed):
+    """kv_manager_step_select (the manager step and the selection in one kernel) == the oracle's
+    manager step then its eviction order, over a sequence of iterations on one workspace (the
+    selection's cached layout is exercised across calls); sizes include odd n (scalar slice
+    tails) and k above the evictable count."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(50, 40000)) | 1
+    state = rng.integers(0, 6, n).astype(np.uint8)
+    lat = rng.integers(0, 1 << 20, n).astype(np.uint32)
+    depth = rng.integers(0, 64, n).astype(np.uint16)
+    rc = np.zeros(n, np.uint32)
+    d_state, d_lat, d_rc = _dev(state, np.uint8), _dev(lat, np.int32), _dev(rc, np.int32)
+    mgr = K.ManagerStep(d_state, d_rc, d_lat, _dev(depth, np.int16))
+    for it in range(3):
+        now = (1 << 20) + it
+        chains = [(int(rng.integers(0, 6)), rng.choice(n, int(rng.integers(1, 400)), replace=False))
+                  for _ in range(int(rng.integers(0, 12)))]
+        pool = [rng.choice(n, int(rng.integers(1, 60)), replace=False) for _ in range(int(rng.integers(0, 30)))]
+        pool_ids = torch.from_numpy(np.concatenate(pool).astype(np.int32)).cuda() if pool else None
+        k = int(rng.integers(1, n + 50))
+        keys, ids, cnt = _fused_select(mgr, now, chains, pool_ids, k, n)
+        st, state, rc, lat, rkeys, nact = oracle.manager_step(state, rc, lat, depth, now, chains, pool)
+        assert st == oracle.OK
+        assert np.array_equal(d_state.cpu().numpy(), state)
+        assert np.array_equal(_u32(d_rc), rc)
+        assert np.array_equal(_u32(d_lat), lat)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), rkeys)
+        assert int(mgr.n_active.item()) == nact
+        _, rids = oracle.evict_select(rkeys, k)
+        assert cnt == len(rids)
+        assert np.array_equal(ids[:cnt].cpu().numpy(), rids)
+
+
+@pytest.mark.parametrize("ctas", [0, 148, 37])
+def test_manager_step_select_fused_full_size(ctas):
+    """The `evict` config at full size (2^20 blocks, top-64k), fused, at several grid sizes:
+    bit-exact against the oracle."""
+    ev = W.make_evict()
+    chains, pool = W.make_manager_update(ev, now=1 << 20, seed=1)
+    rc0 = np.zeros(len(ev.state), np.uint32)
+    d_state, d_lat = _dev(ev.state, np.uint8), _dev(ev.lat, np.int32)
+    d_rc, d_depth = _dev(rc0, np.int32), _dev(ev.depth, np.int16)
+    mgr = K.ManagerStep(d_state, d_rc, d_lat, d_depth)
+    pool_ids = torch.from_numpy(np.concatenate(pool).astype(np.int32)).cuda()
+    with K.options(evict_ctas=ctas):
+        keys, ids, cnt = _fused_select(mgr, 1 << 20, chains, pool_ids, ev.k, len(ev.state))
+    st, state, rc, lat, rkeys, nact = oracle.manager_step(ev.state, rc0, ev.lat, ev.depth, 1 << 20, chains, pool)
+    assert st == oracle.OK
+    assert np.array_equal(_u32(d_rc), rc)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), rkeys)
+    assert int(mgr.n_active.item()) == nact
+    _, rids = oracle.evict_select(rkeys, ev.k)
+    assert cnt == len(rids)
+    assert np.array_equal(ids.cpu().numpy(), rids)
