@@ -306,6 +306,8 @@ def run_ours(args, rank, world, local):
     # the manager step and the selection as ONE cooperative kernel (kv_manager_step_select: the
     # key pass feeds the selection directly); KVA_BENCH_FUSED_MGR=0: two launches
     fused_mgr = os.environ.get("KVA_BENCH_FUSED_MGR", "1") == "1"
+    if os.environ.get("KVA_BENCH_EVICT_CTAS"):  # diagnostics: the selection's grid size
+        K.set_option("evict_ctas", int(os.environ["KVA_BENCH_EVICT_CTAS"]))
 
     def evict_enqueue(ev, fork):
         if fork:

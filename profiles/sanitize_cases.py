@@ -44,4 +44,21 @@ chains = [(4, rng.choice(len(ev.state), 40, replace=False)), (2, rng.choice(len(
 csr = K.ManagerStep.chains_to_device(K.ManagerStep.chains_csr(chains), dev)
 mgr(5, csr, torch.from_numpy(rng.integers(0, len(ev.state), 300).astype(np.int32)).to(dev))
 torch.cuda.synchronize()
+# kv_manager_step_select (manager + selection in one kernel), twice on one workspace (the
+# selection's cached layout), odd n (scalar slice tails)
+n2 = len(ev.state) - 3
+mgr2 = K.ManagerStep(t(ev.state[:n2], np.uint8), t(ev.rc[:n2], np.int32), t(ev.lat[:n2], np.int32),
+                     t(ev.depth[:n2], np.int16))
+sws = torch.empty(K.evict_select_workspace_size(n2, 1000), dtype=torch.uint8, device=dev)
+sids = torch.empty(1000, dtype=torch.int32, device=dev)
+for now in (6, 7):
+    mgr2(now, chains, torch.from_numpy(rng.integers(0, n2, 300).astype(np.int32)).to(dev), select=(1000, sids, sws))
+torch.cuda.synchronize()
+# kv_append_plan (one call) on a fresh tiny workload
+wl2 = W.make_workload("tiny")
+pool2 = K.Pool(wl2.k_pool.to(dev), wl2.v_pool.to(dev), K.free_bits_tensor(wl2.free_bits, dev))
+batch2 = K.Batch(wl2.batch, dev)
+plan2 = K.kv_append_plan(pool2, batch2, wl2.k_new.to(dev), wl2.v_new.to(dev))
+plan2.run(wl2.q.to(dev), torch.empty(wl2.q.shape, dtype=torch.bfloat16, device=dev))
+torch.cuda.synchronize()
 print("sanitize cases ok")
