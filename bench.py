@@ -306,6 +306,8 @@ def run_ours(args, rank, world, local):
     # the manager step and the selection as ONE cooperative kernel (kv_manager_step_select: the
     # key pass feeds the selection directly); KVA_BENCH_FUSED_MGR=0: two launches
     fused_mgr = os.environ.get("KVA_BENCH_FUSED_MGR", "1") == "1"
+    if os.environ.get("KVA_BENCH_TILE_CTAS"):  # diagnostics: the tile kernel's SM share (0 = plan's split)
+        K.set_option("tile_ctas", int(os.environ["KVA_BENCH_TILE_CTAS"]))
     if os.environ.get("KVA_BENCH_EVICT_CTAS"):  # diagnostics: the selection's grid size
         K.set_option("evict_ctas", int(os.environ["KVA_BENCH_EVICT_CTAS"]))
 
@@ -549,6 +551,11 @@ def run_ours(args, rank, world, local):
     if ring is not None:
         K.set_option("span_ring", 0)
         _dump_timeline(ring, spans, span_used)
+        for j, rp in enumerate(reps):  # the selection's phase stamps (CTA 0) of each replica's last call
+            if rp["ev"] is not None:
+                ts = rp["ev"]["ws"][256:512].view(torch.int64).cpu().numpy()
+                ts = ts[ts > 0]
+                sys.stderr.write(f"[timeline] sel phases (replica {j}, us): {[round(float(x) / 1e3, 1) for x in np.diff(ts)]}\n")
     gpu_launches = launches["n"]
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
     ms_same = None

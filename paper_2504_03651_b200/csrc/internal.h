@@ -216,8 +216,17 @@ __device__ __forceinline__ uint64_t manager_key(uint32_t s, uint32_t r, uint32_t
 //   phase 1  win[id] = max element index listing id ("last chain wins", reading R36)
 //   phase 2  winners apply (state, lat = now); rc += pool chains, -= deleted chains
 // Ends with a barrier when phase 2 had work (phase 3, the keys, reads what it wrote).
+// s_ind: shared memory for the chain index (the binary search of phase 2: ~10 dependent loads
+// per transition, L2 round trips when read from global memory), cap entries; the copy is
+// ordered before phase 2 by phase 0's barrier
 template <class Sync>
-__device__ __forceinline__ void manager_phases(const MgrArgs &a, int64_t t0, int64_t nt, Sync &&sync) {
+__device__ __forceinline__ void manager_phases(const MgrArgs &a, int64_t t0, int64_t nt, Sync &&sync,
+                                               int32_t *s_ind = nullptr, int cap = 0) {
+  const int32_t *ind = a.tr_indptr;
+  if (s_ind && a.n_tr > 0 && a.n_chains + 1 <= cap) {
+    for (int i = threadIdx.x; i <= a.n_chains; i += blockDim.x) s_ind[i] = __ldg(a.tr_indptr + i);
+    ind = s_ind;
+  }
   if (a.recount) {
     const int64_t n4 = (reinterpret_cast<uintptr_t>(a.rc) & 15) ? 0 : a.n / 4;
     for (int64_t q = t0; q < n4; q += nt) reinterpret_cast<uint4 *>(a.rc)[q] = make_uint4(0, 0, 0, 0);
@@ -246,7 +255,7 @@ __device__ __forceinline__ void manager_phases(const MgrArgs &a, int64_t t0, int
       int lo = 0, hi = a.n_chains - 1;       // chain j: indptr[j] <= e < indptr[j + 1]
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (a.tr_indptr[mid] <= e) lo = mid;
+        if (ind[mid] <= e) lo = mid;
         else hi = mid - 1;
       }
       a.state[id] = a.tr_state[lo];

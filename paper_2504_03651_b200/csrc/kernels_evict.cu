@@ -21,6 +21,7 @@ namespace cg = cooperative_groups;
 namespace kva {
 
 constexpr uint64_t kInf = ~0ull;
+constexpr int kMgrIndCap = 2048;  // chain-index entries kept in shared memory (8 KB: leaves room for 2 decode CTAs)
 
 __global__ void evict_keys_kernel(const uint8_t *__restrict__ state, const uint32_t *__restrict__ rc,
                                   const uint32_t *__restrict__ lat, const uint16_t *__restrict__ depth,
@@ -66,7 +67,8 @@ __global__ void __launch_bounds__(256) manager_kernel(const __grid_constant__ Mg
   cg::grid_group grid = cg::this_grid();
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
   if (a.span && t0 == 0) a.span[0] = gtime();
-  manager_phases(a, t0, nt, [&] { grid.sync(); });
+  __shared__ int32_t s_ind[kMgrIndCap];
+  manager_phases(a, t0, nt, [&] { grid.sync(); }, s_ind, kMgrIndCap);
   // phase 3: 4 blocks per thread with vector loads/stores when the arrays allow it (torch
   // allocations are 256-B aligned), scalar tail
   unsigned act = 0;

@@ -740,7 +740,8 @@ __global__ void __maxnreg__(KVA_SEL_MAXREG) evict_select_kernel(const __grid_con
   };
 
   if (a.fused) {  // the KV-manager step's phases 0-2 (internal.h), then its keys pass in phase 0
-    manager_phases(a.mgr, (int64_t)c * kT + tid, (int64_t)C * kT, [&] { grid.sync(); });
+    manager_phases(a.mgr, (int64_t)c * kT + tid, (int64_t)C * kT, [&] { stamp(); grid.sync(); stamp(); },
+                   reinterpret_cast<int32_t *>(s_buf), kBufBytes / 4);
     stamp();
   }
   // ---------------- phase 0: which bits vary among the evictable keys, how many ----------------
