@@ -527,6 +527,18 @@ def run_ours(args, rank, world, local):
             ms = t.item()
         return ms
 
+    # The selection's build (option evict_threads): it runs beside the attention on its own
+    # stream.  When the step's decode stream alone takes several selection times (llama7b:
+    # ~330 us of decode vs ~50-65 us of selection) its cost is the decode CTAs it displaces, so
+    # the 256-thread build (~30 KB of shared memory, shares an SM with two decode CTAs) is
+    # used; otherwise (qwen14b: ~66 us of decode) its latency matters and the 512-thread build
+    # is used.  Measured (profiles/r02s3): llama7b 392.5 -> 385.3 us/step, qwen14b 130.3 vs
+    # 169.6 us with the 256 build.  KVA_BENCH_EVICT_THREADS overrides.
+    planA = K.Plan(pool, _post_append_batch(K, wl, dev), stream=stream)
+    dec_est_us = planA.stats()["decode_kv_bytes"] / 6.5e6
+    planA.close()
+    evict_threads = int(os.environ.get("KVA_BENCH_EVICT_THREADS", "256" if dec_est_us > 4 * 50.0 else "512"))
+    K.set_option("evict_threads", evict_threads)
     for _ in range(max(args.warmup, R)):  # every replica warmed
         step()
     barrier()
@@ -693,6 +705,7 @@ def run_ours(args, rank, world, local):
                           % (stats["kv_bytes_algorithmic"] / 1e9)) if R > 1 else
                          "no rotation (--l2-rotate 1): KV working set %.2f GB/rank" % (stats["kv_bytes_algorithmic"] / 1e9),
                    "ms_per_step_without_l2_rotation": ms_same,
+                   "evict_threads": evict_threads,
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,

@@ -421,6 +421,12 @@ kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t num_reqs, const 
  *   "pdl"         1 = decode launched as a programmatic dependent of the tile kernel on one
  *                 stream (default), 0 = the two kernels on two streams (events)
  *   "evict_ctas"  CTAs of the cooperative evict_select kernel (0 = #SMs / 2, default)
+ *   "evict_threads" 512 (default): the selection's fastest build alone; 256: a build whose CTA
+ *                 (~30 KB of shared memory, 256 x 80 registers) shares its SM with two decode
+ *                 CTAs — for selections that run beside a long decode-bound attention step
+ *                 (same results; other values -> KVA_ERR_INVALID)
+ *   "span_ring"   device address of a u64 [2][256][2] ring: manager (0) / evict_select (1)
+ *                 launch i writes {CTA 0 start, latest CTA end} (%globaltimer ns) at [i % 256]
  *   "host_prof"   1 = accumulate host section times (printed at process exit)
  *   "debug_flags" tile-kernel diagnostics, WRONG RESULTS: 1 = softmax skipped, 2 = PV MMAs not
  *                 issued, 4 = QK MMAs not issued (pipeline studies)

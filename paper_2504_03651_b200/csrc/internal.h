@@ -21,7 +21,7 @@ int sm_count();
 
 // Tuning / diagnostics options (kva_set_option; process-wide, read at each call)
 enum Opt : int { kOptTileCtas = 0, kOptOverlap, kOptPdl, kOptEvictCtas, kOptHostProf, kOptDebugFlags, kOptDebugTs,
-                 kOptSpanRing, kOptCount };
+                 kOptSpanRing, kOptEvictThreads, kOptCount };
 // span_ring (diagnostics): device u64 [2][256][2] — manager (0) / evict_select (1) launch i writes
 // [kind][i % 256] = {CTA 0 start, latest CTA end} (%globaltimer ns)
 unsigned long long *span_ring_slot(int kind);
@@ -275,10 +275,19 @@ size_t evict_select_ws_bytes(int64_t n, int64_t k);
 // evict_select: one cooperative kernel of `ctas` CTAs (<= 0: #SMs / 2); free_bits != nullptr:
 // the selected blocks are also marked free (apply)
 // mgr != nullptr: the manager step runs first in the same kernel (its keys pass writes
-// mgr->keys == keys and feeds the selection's first pass: kv_manager_step_select)
+// mgr->keys == keys and feeds the selection's first pass: kv_manager_step_select).  Dispatches
+// to the 512- or 256-thread build (option evict_threads); the workspace size covers both.
 cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                 int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
                                 int ctas, cudaStream_t s, const MgrArgs *mgr = nullptr);
+size_t evict_select_ws_bytes_512(int64_t n, int64_t k);
+size_t evict_select_ws_bytes_256(int64_t n, int64_t k);
+cudaError_t launch_evict_select_512(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
+                                    int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
+                                    int ctas, cudaStream_t s, const MgrArgs *mgr);
+cudaError_t launch_evict_select_256(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
+                                    int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
+                                    int ctas, cudaStream_t s, const MgrArgs *mgr);
 constexpr int kReleaseBatch = 3800;  // ids (+ table entries) per release launch (kernel parameter)
 // free bits of ids_host[0, n) set; tbl_host != nullptr: table[tbl_host[i]] = -1 as well
 cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,

@@ -126,8 +126,8 @@ struct OptDef {
 // defaults = the measured best
 constexpr OptDef kOptDefs[kOptCount] = {{"tile_ctas", 0}, {"overlap", 1}, {"pdl", 1},   {"evict_ctas", 0},
                                         {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0},
-                                        {"span_ring", 0}};
-std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}};
+                                        {"span_ring", 0}, {"evict_threads", 512}};
+std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}, {512}};
 std::atomic<unsigned> g_span_seq[2] = {{0}, {0}};
 int opt_index(const char *name) {
   if (!name) return -1;
@@ -137,6 +137,16 @@ int opt_index(const char *name) {
 }
 }  // namespace
 int64_t opt(Opt o) { return g_opt[o].load(std::memory_order_relaxed); }
+size_t evict_select_ws_bytes(int64_t n, int64_t k) {
+  return std::max(evict_select_ws_bytes_512(n, k), evict_select_ws_bytes_256(n, k));
+}
+cudaError_t launch_evict_select(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids, int64_t *d_count,
+                                uint32_t *free_bits, void *ws, size_t ws_bytes, int ctas, cudaStream_t s,
+                                const MgrArgs *mgr) {
+  return opt(kOptEvictThreads) == 256
+             ? launch_evict_select_256(keys, n, k, out_ids, d_count, free_bits, ws, ws_bytes, ctas, s, mgr)
+             : launch_evict_select_512(keys, n, k, out_ids, d_count, free_bits, ws, ws_bytes, ctas, s, mgr);
+}
 unsigned long long *span_ring_slot(int kind) {
   const int64_t r = opt(kOptSpanRing);
   if (!r) return nullptr;
@@ -147,6 +157,8 @@ unsigned long long *span_ring_slot(int kind) {
 extern "C" kva_status kva_set_option(const char *name, int64_t value) {
   const int i = kva::opt_index(name);
   if (i < 0) return fail(KVA_ERR_INVALID, "unknown option '%s'", name ? name : "(null)");
+  if (i == kva::kOptEvictThreads && value != 256 && value != 512)
+    return fail(KVA_ERR_INVALID, "evict_threads must be 256 or 512");
   kva::g_opt[i].store(value, std::memory_order_relaxed);
   return KVA_OK;
 }

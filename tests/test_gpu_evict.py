@@ -246,3 +246,28 @@ def test_truncate_rollback_matches_oracle(cfg):
     assert np.array_equal(batch.table_host, after)
     with pytest.raises(K.KvaError):  # keep > ctx
         K.kv_truncate(pool, batch, wl.batch["ctx_len"] + 1)
+
+
+@pytest.mark.parametrize("case", _ADV + ["evict", "straddle"])
+def test_select_256_thread_build(case):
+    """The 256-thread build (option evict_threads = 256: 1,024-pair CTA buckets, 7-bit warp
+    digits, the warp areas inside the round buffer) gives the oracle's order bit-exactly on the
+    adversarial cases and the full-size `evict` config (+ straddle)."""
+    import paper_2504_03651_b200 as K
+    if case in ("evict", "straddle"):
+        ev = W.make_evict(straddle=case == "straddle")
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).cuda()  # noqa: E731
+        d = K.evict_keys(t(ev.state, np.uint8), t(ev.rc, np.int32), t(ev.lat, np.int32), t(ev.depth, np.int16))
+        keys = d.cpu().numpy().view(np.uint64)
+        k = ev.k
+    else:
+        keys, k = _adversarial(case, 1 << 17)
+        d = torch.from_numpy(keys.view(np.int64)).cuda()
+    s, ref = oracle.evict_select(keys, k)
+    for ctas in (0, 37):
+        with K.options(evict_threads=256, evict_ctas=ctas):
+            ids, nsel = K.evict_select(d, k)
+        assert nsel == len(ref)
+        assert np.array_equal(ids.cpu().numpy(), ref), ctas
+    with pytest.raises(K.KvaError):
+        K.set_option("evict_threads", 300)

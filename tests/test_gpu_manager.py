@@ -226,8 +226,8 @@ def test_manager_step_select_fused_random(seed):
         assert np.array_equal(ids[:cnt].cpu().numpy(), rids)
 
 
-@pytest.mark.parametrize("ctas", [0, 148, 37])
-def test_manager_step_select_fused_full_size(ctas):
+@pytest.mark.parametrize("ctas,threads", [(0, 512), (148, 512), (37, 512), (0, 256), (148, 256)])
+def test_manager_step_select_fused_full_size(ctas, threads):
     """The `evict` config at full size (2^20 blocks, top-64k), fused, at several grid sizes:
     bit-exact against the oracle."""
     ev = W.make_evict()
@@ -237,7 +237,7 @@ def test_manager_step_select_fused_full_size(ctas):
     d_rc, d_depth = _dev(rc0, np.int32), _dev(ev.depth, np.int16)
     mgr = K.ManagerStep(d_state, d_rc, d_lat, d_depth)
     pool_ids = torch.from_numpy(np.concatenate(pool).astype(np.int32)).cuda()
-    with K.options(evict_ctas=ctas):
+    with K.options(evict_ctas=ctas, evict_threads=threads):
         keys, ids, cnt = _fused_select(mgr, 1 << 20, chains, pool_ids, ev.k, len(ev.state))
     st, state, rc, lat, rkeys, nact = oracle.manager_step(ev.state, rc0, ev.lat, ev.depth, 1 << 20, chains, pool)
     assert st == oracle.OK
