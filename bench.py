@@ -294,6 +294,11 @@ def run_ours(args, rank, world, local):
     # KVA_BENCH_EVICT_PIPELINE=0: fork every step (serialises it behind the previous step).
     evict_pipeline = os.environ.get("KVA_BENCH_EVICT_PIPELINE", "1") == "1"
     fork_next = {"v": True}
+    # The eviction stream is joined into the main stream once, at the end of the timed region
+    # (every step's manager pass + selection is still inside it): a per-step event wait would
+    # sit between the merge and the next kv_truncate / kv_append launches and break their
+    # programmatic-dependent-launch chain.  KVA_BENCH_JOIN_EACH_STEP=1: join every step.
+    join_each_step = os.environ.get("KVA_BENCH_JOIN_EACH_STEP", "0") == "1"
     gather_on = {"v": True}
 
     # The KV manager's per-step enqueue on its own host thread (a serving engine's scheduler /
@@ -383,7 +388,8 @@ def run_ours(args, rank, world, local):
                 exc = done.get()
                 if exc is not None:
                     raise exc
-            stream.wait_event(ev_join)
+            if join_each_step:
+                stream.wait_event(ev_join)
         K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
         launches["n"] += n
@@ -407,6 +413,7 @@ def run_ours(args, rank, world, local):
             t_h = time.perf_counter()
             step(time_idx=i if time_kernels else None)
             host_t.append(time.perf_counter() - t_h)
+        stream.wait_event(ev_join)  # the last step's eviction work (ev_join: recorded after every step's)
         e.record(stream)
         if os.environ.get("KVA_BENCH_HOST_TIMING") == "1":  # diagnostics: host enqueue time per step
             sys.stderr.write(f"[bench host] step enqueue median {1e6 * sorted(host_t)[len(host_t) // 2]:.1f} us\n")
@@ -476,7 +483,8 @@ def run_ours(args, rank, world, local):
                 exc = done.get()
                 if exc is not None:
                     raise exc
-            stream.wait_event(ev_join)
+            if join_each_step:
+                stream.wait_event(ev_join)
         K.kv_truncate(pool, batch, keep_len, stream=stream)
         n += 1
         launches["n"] += n
@@ -517,6 +525,7 @@ def run_ours(args, rank, world, local):
         for i in range(nsteps):
             step_e2e(i)
         stream.wait_stream(cs_out)   # the last result is on the host
+        stream.wait_event(ev_join)   # the last step's eviction work
         e.record(stream)
         barrier()
         ms = s.elapsed_time(e) / nsteps
@@ -557,7 +566,7 @@ def run_ours(args, rank, world, local):
     rot["i"] = 0
     ring = None
     if os.environ.get("KVA_BENCH_SPAN_RING") == "1":  # diagnostics: manager / selection spans
-        ring = torch.zeros(2 * 256 * 2, dtype=torch.int64, device=dev)
+        ring = torch.zeros(5 * 256 * 2, dtype=torch.int64, device=dev)
         K.set_option("span_ring", ring.data_ptr())
     ms = timed(args.steps, time_kernels=True)
     if ring is not None:
@@ -765,9 +774,10 @@ def run_ours(args, rank, world, local):
 def _dump_timeline(ring, spans, used):
     """stderr: one line per timed step — attention kernel spans and the manager / selection
     launches (span_ring) that overlap it, us relative to the first step's first start."""
-    r = ring.cpu().numpy().view(np.uint64).reshape(2, 256, 2)
+    r = ring.cpu().numpy().view(np.uint64).reshape(5, 256, 2)
     sp = spans.cpu().numpy().view(np.uint64)
-    ev = [("mgr", int(a), int(b)) for a, b in r[0] if a and b] + [("sel", int(a), int(b)) for a, b in r[1] if a and b]
+    ev = [(nm, int(a), int(b)) for kind, nm in enumerate(("mgr", "sel", "app_dec", "app_pre", "release"))
+          for a, b in r[kind] if a and b]
     att = []
     for i in used:
         for nm, j in (("dec", 0), ("tile", 2), ("merge", 4)):

@@ -425,8 +425,9 @@ kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t num_reqs, const 
  *                 (~30 KB of shared memory, 256 x 80 registers) shares its SM with two decode
  *                 CTAs — for selections that run beside a long decode-bound attention step
  *                 (same results; other values -> KVA_ERR_INVALID)
- *   "span_ring"   device address of a u64 [2][256][2] ring: manager (0) / evict_select (1)
- *                 launch i writes {CTA 0 start, latest CTA end} (%globaltimer ns) at [i % 256]
+ *   "span_ring"   device address of a u64 [5][256][2] ring: manager (0) / evict_select (1) /
+ *                 append + allocation (2) / prefill-row append (3) / release (4): launch i
+ *                 writes {CTA 0 start, latest CTA end} (%globaltimer ns) at [kind][i % 256]
  *   "host_prof"   1 = accumulate host section times (printed at process exit)
  *   "debug_flags" tile-kernel diagnostics, WRONG RESULTS: 1 = softmax skipped, 2 = PV MMAs not
  *                 issued, 4 = QK MMAs not issued (pipeline studies)

@@ -22,8 +22,9 @@ int sm_count();
 // Tuning / diagnostics options (kva_set_option; process-wide, read at each call)
 enum Opt : int { kOptTileCtas = 0, kOptOverlap, kOptPdl, kOptEvictCtas, kOptHostProf, kOptDebugFlags, kOptDebugTs,
                  kOptSpanRing, kOptEvictThreads, kOptCount };
-// span_ring (diagnostics): device u64 [2][256][2] — manager (0) / evict_select (1) launch i writes
-// [kind][i % 256] = {CTA 0 start, latest CTA end} (%globaltimer ns)
+// span_ring (diagnostics): device u64 [5][256][2] — manager (0) / evict_select (1) / append of
+// the decode-class rows + allocation (2) / append of the prefill rows (3) / release (4): launch i
+// writes [kind][i % 256] = {CTA 0 start, latest CTA end} (%globaltimer ns)
 unsigned long long *span_ring_slot(int kind);
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned long long gtime() {
@@ -288,6 +289,9 @@ cudaError_t launch_evict_select_512(const uint64_t *keys, int64_t n, int64_t k, 
 cudaError_t launch_evict_select_256(const uint64_t *keys, int64_t n, int64_t k, int32_t *out_ids,
                                     int64_t *d_count, uint32_t *free_bits, void *ws, size_t ws_bytes,
                                     int ctas, cudaStream_t s, const MgrArgs *mgr);
+// an empty kernel launched normally: it completes only after everything before it on the
+// stream (ends a run whose last kernel is a programmatic dependent that does not wait)
+cudaError_t launch_join(cudaStream_t s);
 constexpr int kReleaseBatch = 3800;  // ids (+ table entries) per release launch (kernel parameter)
 // free bits of ids_host[0, n) set; tbl_host != nullptr: table[tbl_host[i]] = -1 as well
 cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,

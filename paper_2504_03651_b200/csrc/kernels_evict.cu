@@ -139,10 +139,19 @@ struct ReleaseList {
   int32_t tbl[CAP];
 };
 template <int CAP>
-__global__ void release_ids_kernel(uint32_t *free_bits, const __grid_constant__ ReleaseList<CAP> r) {
+__global__ void release_ids_kernel(uint32_t *free_bits, const __grid_constant__ ReleaseList<CAP> r,
+                                   unsigned long long *span) {
+  // a programmatic dependent of the preceding kernel (option pdl): waits for it first
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (span && blockIdx.x == 0 && threadIdx.x == 0) span[0] = gtime();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < r.n; i += gridDim.x * blockDim.x) {
     atomicOr(free_bits + (r.ids[i] >> 5), 1u << (r.ids[i] & 31));
     if (r.table) r.table[r.tbl[i]] = -1;
+  }
+  if (span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(span + 1, gtime());
   }
 }
 template <int CAP>
@@ -153,8 +162,16 @@ static cudaError_t release_launch(uint32_t *free_bits, const int32_t *ids, const
   r.table = tbl ? table : nullptr;
   std::memcpy(r.ids, ids, sizeof(int32_t) * n);
   if (tbl) std::memcpy(r.tbl, tbl, sizeof(int32_t) * n);
-  release_ids_kernel<CAP><<<(n + 255) / 256, 256, 0, s>>>(free_bits, r);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = opt(kOptPdl) != 0 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, release_ids_kernel<CAP>, free_bits, r, span_ring_slot(4));
 }
 
 cudaError_t launch_release_ids(uint32_t *free_bits, const int32_t *ids_host, int n, cudaStream_t s,

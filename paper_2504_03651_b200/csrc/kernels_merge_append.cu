@@ -26,6 +26,9 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(const AttnParams p,
   const int lane = threadIdx.x & 31, hl = lane & 15;  // lane within the half-warp
   const unsigned hmask = (lane < 16) ? 0x0000FFFFu : 0xFFFF0000u;
   const int w = blockIdx.x * kUnitsPerCta + (threadIdx.x >> 4);  // this half-warp's unit
+  // the next launch on the stream (kv_truncate's release, the next kv_append: programmatic
+  // dependents that wait for this grid before touching memory) may be set up now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (p.span && threadIdx.x == 0) {  // instrumentation: CTA start
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -136,6 +139,12 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(const AttnParams p,
   }
 }
 
+__global__ void join_kernel() {}
+cudaError_t launch_join(cudaStream_t s) {
+  join_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(const AttnParams &p, const ReqList<MergeReq> &RL, int n_units, cudaStream_t s) {
   if (n_units <= 0) return cudaSuccess;
   const int grid = (n_units + 15) / 16;  // 16 units (half-warps) per 256-thread CTA
@@ -165,6 +174,7 @@ struct AppendArgs {
   int32_t *block_table;
   int32_t max_blocks, total_new_tok, early_trigger, n_app_ctas;
   uint32_t *free_bits;
+  unsigned long long *span;  // diagnostics (span_ring)
 };
 template <bool ALLOC>
 struct AllocParam {
@@ -177,14 +187,18 @@ template <bool ALLOC>
 __global__ void __launch_bounds__(256) append_kernel(const __grid_constant__ AppendArgs a,
                                                      const __grid_constant__ ReqList<AppendReq> L,
                                                      const __grid_constant__ AllocParam<ALLOC> ap) {
-  // early_trigger (the append of the tile-path rows only): the tile kernel launched right
-  // after it (programmatic dependent launch) may become resident now; it waits
+  // early_trigger, after the wait: the append of the tile-path rows — the tile kernel launched
+  // right after it (programmatic dependent launch) may become resident now; it waits
   // (griddepcontrol.wait) before reading the pool.  The decode kernel, a dependent of the tile
-  // kernel that does NOT wait, reads only decode-class rows, which an earlier append on the
-  // stream wrote.  The decode-class append never triggers early: a tile kernel launched right
-  // after it (no tile-path rows) starts only once those rows are complete, and so does the
-  // decode kernel behind it.
+  // kernel that does NOT wait, reads only decode-class rows, which the preceding append wrote
+  // (complete: this kernel waited for it).  The decode-class append triggers early only when
+  // the tile-path append follows it (that one waits); with no tile-path rows the tile kernel
+  // follows it directly and starts only once it is complete, and so does the decode kernel.
+  // launched as a programmatic dependent of the preceding kernel (option pdl): its setup
+  // overlaps that kernel, and nothing is read or written before it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.span && blockIdx.x == 0 && threadIdx.x == 0) a.span[0] = gtime();
   if constexpr (ALLOC) {
     if ((int)blockIdx.x >= a.n_app_ctas) {  // allocation publishing
       const AllocList &al = ap.al;
@@ -249,6 +263,10 @@ __global__ void __launch_bounds__(256) append_kernel(const __grid_constant__ App
 #pragma unroll
   for (int k = 0; k < kMaxIt; ++k)
     if (dsto[k] >= 0) *reinterpret_cast<uint4 *>((isv[k] ? a.v_pool : a.k_pool) + dsto[k]) = v[k];
+  if (a.span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(a.span + 1, gtime());
+  }
 }
 
 cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t stride_tok,
@@ -261,22 +279,32 @@ cudaError_t launch_append(const uint16_t *k_new, const uint16_t *v_new, int64_t 
   const int n_alloc = al ? (al->n + 255) / 256 : 0;
   if (n_app + n_alloc <= 0) return cudaSuccess;
   AppendArgs a{k_new, v_new, stride_tok, k_pool, v_pool, Hkv, d, block_table, max_blocks,
-               total_new_tok, early_trigger ? 1 : 0, n_app, free_bits};
+               total_new_tok, early_trigger ? 1 : 0, n_app, free_bits, span_ring_slot(al ? 2 : 3)};
+  // programmatic dependent launch (option pdl): the kernel waits for its predecessor at its
+  // first instruction, so only the launch latency overlaps
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = opt(kOptPdl) != 0 ? 1 : 0;
   if (al && al->n > 0) {
     static bool carve = (cudaFuncSetAttribute(append_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                               cudaSharedmemCarveoutMaxShared), true);
     (void)carve;
     AllocParam<true> ap;
     ap.al = *al;
-    append_kernel<true><<<(unsigned)(n_app + n_alloc), 256, 0, s>>>(a, L, ap);
-  } else {
-    if (n_app <= 0) return cudaSuccess;
-    static bool carve = (cudaFuncSetAttribute(append_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                              cudaSharedmemCarveoutMaxShared), true);
-    (void)carve;
-    append_kernel<false><<<(unsigned)n_app, 256, 0, s>>>(a, L, AllocParam<false>{});
+    cfg.gridDim = dim3((unsigned)(n_app + n_alloc));
+    return cudaLaunchKernelEx(&cfg, append_kernel<true>, a, L, ap);
   }
-  return cudaGetLastError();
+  if (n_app <= 0) return cudaSuccess;
+  static bool carve = (cudaFuncSetAttribute(append_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared), true);
+  (void)carve;
+  cfg.gridDim = dim3((unsigned)n_app);
+  return cudaLaunchKernelEx(&cfg, append_kernel<false>, a, L, AllocParam<false>{});
 }
 
 }  // namespace kva

@@ -128,7 +128,7 @@ constexpr OptDef kOptDefs[kOptCount] = {{"tile_ctas", 0}, {"overlap", 1}, {"pdl"
                                         {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0},
                                         {"span_ring", 0}, {"evict_threads", 512}};
 std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}, {512}};
-std::atomic<unsigned> g_span_seq[2] = {{0}, {0}};
+std::atomic<unsigned> g_span_seq[5] = {{0}, {0}, {0}, {0}, {0}};
 int opt_index(const char *name) {
   if (!name) return -1;
   for (int i = 0; i < kOptCount; ++i)
@@ -695,8 +695,10 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
   hs.lap("append.lists");
   uint16_t *kp = static_cast<uint16_t *>(p->desc.k_pool), *vp = static_cast<uint16_t *>(p->desc.v_pool);
   const uint16_t *kn = static_cast<const uint16_t *>(k_new), *vn = static_cast<const uint16_t *>(v_new);
+  // the decode-class append lets the prefill-row append (which waits for it) be set up early;
+  // with no prefill rows the attention follows it directly and it must complete first
   CUDA_TRY(launch_append(kn, vn, stride_tok, kp, vp, Hkv, d, b->block_table, b->max_blocks, la, pa.back(), s,
-                         false, &al, p->desc.free_bits));
+                         /*early_trigger=*/!rb.empty(), &al, p->desc.free_bits));
   if (!rb.empty())  // the tile kernel (PDL) may start while these rows are written
     CUDA_TRY(launch_append(kn, vn, stride_tok, kp, vp, Hkv, d, b->block_table, b->max_blocks, lb, pbv.back(), s,
                            /*early_trigger=*/true));
@@ -1230,6 +1232,11 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
     if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
+    // the decode kernel does not wait for the tile kernel: when it is the last kernel of the
+    // run, a join kernel ends it, so the completion of the run's last kernel implies the tile
+    // kernel's (the next kv_truncate / kv_append are programmatic dependents that wait only
+    // for their immediate predecessor)
+    else if (do_dec) CUDA_TRY(launch_join(s));
     hs.lap("run.launch_merge");
     return KVA_OK;
   }
