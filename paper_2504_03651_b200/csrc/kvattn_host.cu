@@ -1299,8 +1299,11 @@ extern "C" kva_status kva_plan_set_timing_events(kva_plan *pl, void *tile_begin,
 
 extern "C" kva_status kva_plan_launch_count(const kva_plan *pl, int32_t phases, int32_t *n) {
   if (!pl || !n) return fail(KVA_ERR_INVALID, "null argument");
-  *n = ((phases & KVA_PHASE_TILE) && pl->n_tile > 0) + ((phases & KVA_PHASE_DECODE) && pl->n_dec > 0) +
-       ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0);
+  const bool tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0, dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
+  const bool merge = (phases & KVA_PHASE_MERGE) && pl->n_mrows > 0;
+  // + the join kernel that ends an overlapped PDL run without a merge (hybrid_attention_run)
+  const bool join = tile && dec && pl->overlap && opt(kOptPdl) != 0 && !merge;
+  *n = tile + dec + merge + join;
   return KVA_OK;
 }
 

@@ -91,3 +91,33 @@ def test_evict_select_grid_sizes(ctas):
         ids, n = K.evict_select(torch.from_numpy(keys.view(np.int64)).cuda(), 40000)
         _, rids = oracle.evict_select(keys, 40000)
         assert np.array_equal(ids.cpu().numpy(), rids)
+
+
+def test_truncate_after_a_run_without_merge_waits_for_the_tile_kernel():
+    """A run whose last kernel is the decode kernel (every decode direct: no split, no group, so
+    no merge) with the tile kernel as the long pole (1 persistent CTA): kv_truncate right after
+    it resets the chunk's new table entries, and its release kernel is a programmatic dependent
+    that waits only for its predecessor — the join kernel that ends such a run must make that
+    the tile kernel as well, else the tile kernel reads -1 entries (zero-filled K/V)."""
+    import paper_2504_03651_b200 as K
+    reqs = [W.ReqSpec(W.OFFLINE_PREFILL, 2400, 2000, -1), W.ReqSpec(W.ONLINE_DECODE, 300, 1),
+            W.ReqSpec(W.ONLINE_DECODE, 500, 1)]
+    wl = W.make_workload(W.custom_config("join", 16, 2, 128, 67, reqs, []))
+    dev = "cuda"
+    r = oracle_step(wl)
+    for _ in range(3):
+        with K.options(tile_ctas=1, overlap=1, pdl=1):
+            pool = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), K.free_bits_tensor(wl.free_bits, dev))
+            batch = K.Batch(wl.batch, dev)
+            plan = K.kv_append_plan(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+            st = plan.stats()
+            assert st["n_merge_rows"] == 0 and st["n_tile_items"] > 0 and st["n_decode_items"] > 0
+            assert plan.launch_count() == 3  # tile, decode, join
+            q = wl.q.to(dev)
+            out = torch.empty(q.shape, dtype=torch.float32, device=dev)
+            lse = torch.empty(q.shape[:2], dtype=torch.float32, device=dev)
+            plan.run(q, out, lse)
+            keep = (wl.batch["ctx_len"] - np.diff(wl.batch["q_indptr"])).astype(np.int32)
+            K.kv_truncate(pool, batch, keep)
+            torch.cuda.synchronize()
+        assert_attention_close(out, lse, r["out"], r["lse"])
