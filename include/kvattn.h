@@ -183,10 +183,13 @@ kva_status hybrid_attention_plan(kva_pool *pool, const kva_batch_desc *desc, voi
                                  size_t workspace_bytes, kva_stream_t stream, kva_plan **plan);
 /* kv_append followed by hybrid_attention_plan of the same descriptor, in one call (the serving
  * iteration's order: append the step's K/V, then attend).  Same arguments, errors
- * and effects as the two calls in sequence (on KVA_NEEDS_EVICTION nothing is enqueued and no
- * plan is made); the descriptor is validated once: kv_append checks the resident part and
- * writes every new position's table entry itself, which is what the plan's own check would
- * re-verify.  *plan is owned by the caller (kva_plan_destroy). */
+ * and effects as the two calls in sequence; the descriptor is validated once: kv_append checks
+ * the resident part and writes every new position's table entry itself, which is what the
+ * plan's own check would re-verify.  The plan is made first (it reads no block id), then the
+ * append: on ANY error (KVA_NEEDS_EVICTION with *deficit_blocks, a workspace too small, ...)
+ * the pool, the tables and the free bitmap are unchanged and no plan is returned (the plan's
+ * work lists may already have been uploaded into attn_workspace).  *plan is owned by the
+ * caller (kva_plan_destroy). */
 kva_status kv_append_plan(kva_pool *pool, kva_batch_desc *desc, const void *k_new, const void *v_new,
                           int64_t new_stride_tok, int32_t *deficit_blocks, void *append_workspace,
                           size_t append_workspace_bytes, void *attn_workspace, size_t attn_workspace_bytes,

@@ -554,12 +554,13 @@ extern "C" kva_status kv_append_workspace_size(const kva_batch_desc *b, size_t *
   return KVA_OK;
 }
 
-extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_new,
-                                const void *v_new, int64_t stride_tok, int32_t *deficit,
-                                void *workspace, size_t ws_bytes, kva_stream_t stream) {
+// validated: the caller has just run validate_desc(p, b, 1) (kv_append_plan)
+static kva_status append_impl(kva_pool *p, kva_batch_desc *b, const void *k_new, const void *v_new,
+                              int64_t stride_tok, int32_t *deficit, void *workspace, size_t ws_bytes,
+                              kva_stream_t stream, bool validated) {
   if (deficit) *deficit = 0;
   HSection hs;
-  kva_status st = validate_desc(p, b, 1);
+  kva_status st = validated ? KVA_OK : validate_desc(p, b, 1);
   hs.lap("append.validate");
   if (st != KVA_OK) return st;
   if (b->num_reqs == 0) return KVA_OK;
@@ -710,6 +711,12 @@ extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_ne
   for (size_t j = 0; j < ap.ids.size(); ++j) b->block_table_host[ap.tbl_idx[j]] = ap.ids[j];
   hs.lap("append.commit");
   return KVA_OK;
+}
+
+extern "C" kva_status kv_append(kva_pool *p, kva_batch_desc *b, const void *k_new,
+                                const void *v_new, int64_t stride_tok, int32_t *deficit,
+                                void *workspace, size_t ws_bytes, kva_stream_t stream) {
+  return append_impl(p, b, k_new, v_new, stride_tok, deficit, workspace, ws_bytes, stream, false);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1124,9 +1131,23 @@ extern "C" kva_status kv_append_plan(kva_pool *p, kva_batch_desc *b, const void 
                                      void *ws_attn, size_t ws_attn_bytes, kva_stream_t stream, kva_plan **out) {
   if (!out) return fail(KVA_ERR_INVALID, "null plan pointer");
   *out = nullptr;
-  kva_status st = kv_append(p, b, k_new, v_new, stride_tok, deficit, ws_append, ws_append_bytes, stream);
+  if (deficit) *deficit = 0;
+  // one validation (the append's: the resident part; the plan reads no block id, and the
+  // append itself writes every new position's entry), then the plan — so a plan error leaves
+  // the pool untouched — then the append (its own errors: the plan is destroyed)
+  kva_status st = validate_desc(p, b, 1);
   if (st != KVA_OK) return st;
-  return plan_impl(p, b, ws_attn, ws_attn_bytes, stream, out, true);
+  kva_plan *pl = nullptr;
+  if ((st = plan_impl(p, b, ws_attn, ws_attn_bytes, stream, &pl, true)) != KVA_OK) return st;
+  st = append_impl(p, b, k_new, v_new, stride_tok, deficit, ws_append, ws_append_bytes, stream, true);
+  if (st != KVA_OK) {
+    const std::string msg = g_err;  // kva_plan_destroy does not touch it; keep the append's message
+    delete pl;
+    g_err = msg;
+    return st;
+  }
+  *out = pl;
+  return KVA_OK;
 }
 
 extern "C" kva_status kva_plan_destroy(kva_plan *pl) {

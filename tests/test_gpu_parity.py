@@ -462,3 +462,16 @@ def test_append_plan_fused_matches_oracle(cfg):
     torch.cuda.synchronize()
     assert torch.equal(kp2.cpu().view(torch.int16), wl.k_pool.view(torch.int16))
     assert np.array_equal(batch2.table_dev.cpu().numpy(), wl.batch["block_table"])
+    assert np.array_equal(batch2.table_host, wl.batch["block_table"])
+    # an attention workspace too small: an error before the append, nothing changes
+    pool3 = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), K.free_bits_tensor(wl.free_bits, dev))
+    batch3 = K.Batch(wl.batch, dev)
+    free0 = pool3.free_count()
+    tiny_ws = torch.empty(256, dtype=torch.uint8, device=dev)
+    with pytest.raises(K.KvaError) as ei:
+        K.kv_append_plan(pool3, batch3, wl.k_new.to(dev), wl.v_new.to(dev), attn_workspace=tiny_ws)
+    assert ei.value.status == K.ERR_INVALID
+    torch.cuda.synchronize()
+    assert pool3.free_count() == free0
+    assert np.array_equal(batch3.table_host, wl.batch["block_table"])
+    assert np.array_equal(batch3.table_dev.cpu().numpy(), wl.batch["block_table"])
