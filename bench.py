@@ -311,6 +311,8 @@ def run_ours(args, rank, world, local):
     # the manager step and the selection as ONE cooperative kernel (kv_manager_step_select: the
     # key pass feeds the selection directly); KVA_BENCH_FUSED_MGR=0: two launches
     fused_mgr = os.environ.get("KVA_BENCH_FUSED_MGR", "1") == "1"
+    if os.environ.get("KVA_BENCH_FOLD"):  # diagnostics: 0 = cascade members merged by the merge kernel
+        K.set_option("fold", int(os.environ["KVA_BENCH_FOLD"]))
     if os.environ.get("KVA_BENCH_TILE_CTAS"):  # diagnostics: the tile kernel's SM share (0 = plan's split)
         K.set_option("tile_ctas", int(os.environ["KVA_BENCH_TILE_CTAS"]))
     if os.environ.get("KVA_BENCH_EVICT_CTAS"):  # diagnostics: the selection's grid size

@@ -428,6 +428,12 @@ kva_status kva_group_batch_nested(kva_prefix_index *ix, int32_t num_reqs, const 
  *                 (~30 KB of shared memory, 256 x 80 registers) shares its SM with two decode
  *                 CTAs — for selections that run beside a long decode-bound attention step
  *                 (same results; other values -> KVA_ERR_INVALID)
+ *   "fold"        1: in the one-stream overlapped mode, decode-class members of a one-level
+ *                 group whose suffix is one split merge their partial with the group's cascade
+ *                 partial in the decode kernel's epilogue (waiting on the tile kernel's
+ *                 per-item completion counters) instead of in the merge kernel — bit-identical
+ *                 results; 0 (default): the decode kernel then waits for the cascade tiles,
+ *                 which measured slower on qwen14b (step period 122 vs 117 us)
  *   "span_ring"   device address of a u64 [5][256][2] ring: manager (0) / evict_select (1) /
  *                 append + allocation (2) / prefill-row append (3) / release (4): launch i
  *                 writes {CTA 0 start, latest CTA end} (%globaltimer ns) at [kind][i % 256]

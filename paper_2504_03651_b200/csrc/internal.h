@@ -21,7 +21,7 @@ int sm_count();
 
 // Tuning / diagnostics options (kva_set_option; process-wide, read at each call)
 enum Opt : int { kOptTileCtas = 0, kOptOverlap, kOptPdl, kOptEvictCtas, kOptHostProf, kOptDebugFlags, kOptDebugTs,
-                 kOptSpanRing, kOptEvictThreads, kOptCount };
+                 kOptSpanRing, kOptEvictThreads, kOptFold, kOptCount };
 // span_ring (diagnostics): device u64 [5][256][2] — manager (0) / evict_select (1) / append of
 // the decode-class rows + allocation (2) / append of the prefill rows (3) / release (4): launch i
 // writes [kind][i % 256] = {CTA 0 start, latest CTA end} (%globaltimer ns)
@@ -47,8 +47,17 @@ constexpr int kMaxOutExtra = 7;   // extra output destinations (peers of an 8-GP
 // kSplitKeys; the decode kernel runs every (split, kv head) as one warp.  Partial slot of
 // (head h, split s, row r) = slot + (h * nsplit + s) * rows + r, rows = n_tok * g; slot < 0:
 // single split, the output is written directly.
+// fold: index into the plan's FoldReq list (-1: none) — a decode-class member of a one-level
+// group whose suffix is one split: in fold mode the decode kernel merges its own partial with
+// the group's cascade partial in its epilogue (no merge-kernel entry)
 struct DecodeReq {
-  int32_t q_row0, n_tok, table_row, kb, ctx, slot, nsplit, pad;
+  int32_t q_row0, n_tok, table_row, kb, ctx, slot, nsplit, fold;
+};
+// casc_slot / casc_hstride as in MergeReq (head 0); member_row0: the member's first row in the
+// group's stacked row space; flag_base: the group's first cascade-item index (kv head 0), mtiles
+// items per kv head (item of row x, head h = flag_base + h * mtiles + x / 256; Q tile (x % 256) / 128)
+struct FoldReq {
+  int32_t casc_slot, casc_hstride, member_row0, flag_base, mtiles, pad[3];
 };
 
 // One tile CTA: <= kTileM rows of one row space (r = tok*g + hh) over keys [k0, k1).
@@ -62,7 +71,7 @@ struct TileItem {
   int32_t k0, k1;
   int32_t pos0;      // causal: position of tok 0
   int32_t slot;      // partial slot of row r0; -1 = direct output
-  int32_t flags;
+  int32_t flags;     // kTile* bits; bits 8+: cascade item index + 1 (fold completion flags)
 };
 
 // One request whose partials are merged (a6): each of its rows r < rows is merged for every
@@ -125,6 +134,13 @@ struct AttnParams {
   // (kva_plan_set_span_buffer), nullable
   unsigned long long *span;
   int32_t debug_flags;      // diagnostics only (KVA_DEBUG_FLAGS): 1 = tile softmax skipped
+  // fold (decode-epilogue merge of cascade members): FoldReq list, per (cascade item, Q tile)
+  // completion counters (+1 per softmax warp, zeroed by the plan upload), this run's epoch
+  // (runs that launched the tile kernel, counting this one), fold_on = this run folds
+  const FoldReq *fold;
+  unsigned *fold_flags;
+  uint32_t epoch;
+  int32_t fold_on;
 };
 
 // launchers (kernels_*.cu)

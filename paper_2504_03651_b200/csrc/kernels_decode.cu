@@ -306,6 +306,10 @@ __global__ void __launch_bounds__(128, MINB)
     }
   }
   constexpr float kLn2 = 0.6931471805599453f;
+  // fold: this member's suffix partial is merged here with its group's cascade partial (the
+  // tile kernel, resident before this kernel started, counts each stored Q tile of a cascade
+  // item: 4 softmax warps per run) — the merge kernel's arithmetic, in its partial order
+  const bool folded = p.fold_on && rq.fold >= 0;
   if (lane < 4) {
 #pragma unroll
     for (int nt = 0; nt < NR; ++nt)
@@ -314,16 +318,79 @@ __global__ void __launch_bounds__(128, MINB)
         const int r = nt * 8 + cq + c;
         if (r >= n_rows) continue;
         const float lse = l[nt][c] > 0.f ? (m[nt][c] + __log2f(l[nt][c])) * kLn2 : -CUDART_INF_F;
-        if (slot < 0) {
+        if (folded) {
+          stg[r * SROW + D] = lse;  // the padding column
+        } else if (slot < 0) {
           if (p.lse) p.lse[(int64_t)(q_row0 + r / g) * p.Hq + kv_head * g + r % g] = lse;
         } else {
           p.part_lse[slot + r] = lse;
         }
       }
   }
+  FoldReq fr{};
+  if (folded) {
+    fr = p.fold[rq.fold];
+    if (lane == 0) {
+      const uint32_t target = 4u * p.epoch;
+      const int x0 = fr.member_row0, x1 = x0 + n_rows - 1;
+      const int f0 = 2 * (fr.flag_base + kv_head * fr.mtiles + x0 / 256) + (x0 % 256) / 128;
+      const int f1 = 2 * (fr.flag_base + kv_head * fr.mtiles + x1 / 256) + (x1 % 256) / 128;
+      for (int f : {f0, f1}) {
+        unsigned spins = 0;
+        while (ld_acquire_u32(p.fold_flags + f) < target) {
+          __nanosleep(128);
+          if (++spins > (1u << 26)) __trap();  // a counter that never arrives: fail, not hang
+        }
+      }
+    }
+  }
   __syncwarp();
   constexpr int V = D / 32;  // values per lane per row
-  for (int r = 0; r < n_rows; ++r) {
+  if (folded) {
+    for (int r = 0; r < n_rows; ++r) {
+      const int cs = fr.casc_slot + kv_head * fr.casc_hstride + r;
+      const float lc = __ldcg(p.part_lse + cs), lo = stg[r * SROW + D];
+      const float *src = stg + r * SROW + lane * V;
+      const float *csrc = p.part_o + (int64_t)cs * D + lane * V;
+      const float L = fmaxf(lc, lo);
+      const float w0 = lc == -CUDART_INF_F ? 0.f : __expf(lc - L);
+      const float w1 = lo == -CUDART_INF_F ? 0.f : __expf(lo - L);
+      float sum = 0.f;
+      sum += w0;
+      sum += w1;
+      const float inv = 1.f / sum;
+      float v[V];
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const float2 xc = __ldcg(reinterpret_cast<const float2 *>(csrc + i));
+        const float2 xo = *reinterpret_cast<const float2 *>(src + i);
+        float a0 = 0.f, a1 = 0.f;
+        a0 += w0 * xc.x;
+        a1 += w0 * xc.y;
+        a0 += w1 * xo.x;
+        a1 += w1 * xo.y;
+        v[i] = a0 * inv;
+        v[i + 1] = a1 * inv;
+      }
+      const int64_t qrow = q_row0 + r / g;
+      const int hq = kv_head * g + r % g;
+      const int64_t off = qrow * p.o_stride_tok + hq * p.o_stride_head + lane * V;
+      for (int o = 0; o <= p.n_out_extra; ++o) {
+        void *base = o == 0 ? p.out : p.out_extra[o - 1];
+        if (p.out_f32) {
+          float *dst = reinterpret_cast<float *>(base) + off;
+#pragma unroll
+          for (int i = 0; i < V; i += 2) *reinterpret_cast<float2 *>(dst + i) = make_float2(v[i], v[i + 1]);
+        } else {
+          uint16_t *dst = reinterpret_cast<uint16_t *>(base) + off;
+#pragma unroll
+          for (int i = 0; i < V; i += 2) *reinterpret_cast<uint32_t *>(dst + i) = pack_bf16(v[i], v[i + 1]);
+        }
+      }
+      if (p.lse && lane == 0) p.lse[qrow * p.Hq + hq] = L + __logf(sum);
+    }
+  }
+  for (int r = 0; r < (folded ? 0 : n_rows); ++r) {
     const float *src = stg + r * SROW + lane * V;
     float v[V];
 #pragma unroll

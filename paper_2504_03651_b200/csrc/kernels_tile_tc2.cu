@@ -583,6 +583,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (it.slot >= 0) p.part_lse[it.slot + (r - it.r0)] = lse;
         else if (p.lse) p.lse[(int64_t)qrow * p.Hq + hq] = lse;
       }
+      if (p.fold_flags && (it.flags >> 8)) {  // a cascade item: this warp's partial rows are stored
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(p.fold_flags + 2 * ((it.flags >> 8) - 1) + t, 1u);
+        }
+      }
       fence_before();  // O reads done before this group's next item overwrites O
       item = nxt;
     }

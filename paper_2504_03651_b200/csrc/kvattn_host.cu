@@ -126,8 +126,8 @@ struct OptDef {
 // defaults = the measured best
 constexpr OptDef kOptDefs[kOptCount] = {{"tile_ctas", 0}, {"overlap", 1}, {"pdl", 1},   {"evict_ctas", 0},
                                         {"host_prof", 0}, {"debug_flags", 0}, {"debug_ts", 0},
-                                        {"span_ring", 0}, {"evict_threads", 512}};
-std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}, {512}};
+                                        {"span_ring", 0}, {"evict_threads", 512}, {"fold", 0}};
+std::atomic<int64_t> g_opt[kOptCount] = {{0}, {1}, {1}, {0}, {0}, {0}, {0}, {0}, {512}, {0}};
 std::atomic<unsigned> g_span_seq[5] = {{0}, {0}, {0}, {0}, {0}};
 int opt_index(const char *name) {
   if (!name) return -1;
@@ -729,6 +729,10 @@ struct kva_plan {
   bool has3d = false;
   ReqList<DecodeReq> dec;                  // decode requests (inline kernel parameter or uploaded)
   ReqList<MergeReq> mrg;                   // merged requests (idem)
+  ReqList<MergeReq> mrg_red;               // the same without the folded requests (fold mode)
+  int n_mrows_red = 0;
+  bool has_fold = false;                   // FoldReq list + counters in the workspace
+  mutable uint32_t runs = 0;               // runs that launched the tile kernel (fold epoch)
   TileList tiles;                          // tcgen05 tile items (inline kernel parameter or uploaded)
   int n_dec = 0, n_tile = 0, n_mrows = 0;  // work units: decode (split, head), tiles, merge (row, head)
   // the plan arrays are uploaded on the pool's side stream (ordered after `stream`'s prior work
@@ -756,6 +760,10 @@ struct PlanBuild {
   std::vector<MergeReq> mrg;
   std::vector<int32_t> mrg_pre{0};   // exclusive prefix of rows per merged request
   std::vector<int32_t> row_list;
+  std::vector<FoldReq> fold;          // folded decode-class members (DecodeReq::fold)
+  std::vector<MergeReq> mrg_red;      // the merge list without them (fold mode)
+  std::vector<int32_t> mrg_red_pre{0};
+  int32_t n_casc_items = 0;           // cascade tile items (fold counters: 2 per item)
   int64_t n_slots = 0;
   int64_t tile_flops = 0;
   kva_plan_stats stats{};
@@ -780,7 +788,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
   std::vector<std::vector<int>> members(G);  // decode-class requests at or below the group
   std::vector<std::vector<int>> member_off(G);  // their token offsets in the group's row list
   std::vector<int64_t> casc_base(G, -1);
-  std::vector<int> group_rows(G, 0), list_off(G, 0);
+  std::vector<int> group_rows(G, 0), list_off(G, 0), flag_base(G, -1), mtiles(G, 0);
   for (int i = 0; i < R; ++i)
     for (int l = grp(i); l >= 0; l = parent(l))
       if (first_member[l] < 0) first_member[l] = i;
@@ -798,6 +806,11 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     const int np = b->group_prefix_blocks[gi];
     const int kstart = parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] * kBlock : 0;
     casc_base[gi] = pb.n_slots;
+    if (np * kBlock > kstart) {  // cascade item (gi, h, m0) = flag_base + h * mtiles + m0 / kTileM
+      flag_base[gi] = pb.n_casc_items;
+      mtiles[gi] = cdiv(group_rows[gi], kTileM);
+      pb.n_casc_items += Hkv * mtiles[gi];
+    }
     for (int h = 0; h < Hkv; ++h) {
       for (int m0 = 0; m0 < group_rows[gi]; m0 += kTileM) {
         if (np * kBlock <= kstart) break;  // a level with no blocks of its own: no tile
@@ -811,7 +824,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
         t.k1 = np * kBlock;
         t.pos0 = 0;
         t.slot = (int32_t)(pb.n_slots + m0);
-        t.flags = kTileList;
+        t.flags = kTileList | ((flag_base[gi] + h * mtiles[gi] + m0 / kTileM + 1) << 8);
         pb.tile.push_back(t);
         pb.stats.n_cascade_items++;
       }
@@ -864,6 +877,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
       dq.ctx = ctx;
       dq.slot = direct ? -1 : (int32_t)base;
       dq.nsplit = nsplit;
+      dq.fold = -1;
       pb.dec.push_back(dq);
       pb.dec_pre.push_back(pb.dec_pre.back() + nsplit);
       dec_keys += (int64_t)(ctx - kb) * Hkv;
@@ -885,6 +899,23 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
         mq.nsplit = nsplit;
         pb.mrg.push_back(mq);
         pb.mrg_pre.push_back(pb.mrg_pre.back() + rows);
+        // fold: a member of a one-level group whose suffix is one split (the decode warp owns
+        // the whole suffix partial and merges it with the cascade partial itself)
+        if (cascaded && parent(gi) < 0 && level_has_tile(gi) && nsplit == 1 && mq.n_casc == 1) {
+          const auto &mv = members[gi];
+          const size_t pos = std::lower_bound(mv.begin(), mv.end(), i) - mv.begin();
+          FoldReq fr{};
+          fr.casc_slot = mq.casc_slot[0];
+          fr.casc_hstride = mq.casc_hstride[0];
+          fr.member_row0 = member_off[gi][pos] * g;
+          fr.flag_base = flag_base[gi];
+          fr.mtiles = mtiles[gi];
+          pb.dec.back().fold = (int32_t)pb.fold.size();  // (dq was pushed above)
+          pb.fold.push_back(fr);
+        } else {
+          pb.mrg_red.push_back(mq);
+          pb.mrg_red_pre.push_back(pb.mrg_red_pre.back() + rows);
+        }
       }
     } else {
       const int rows = ql * g;
@@ -954,7 +985,9 @@ static size_t plan_bytes(const PlanBuild &pb, int d, size_t *arrays_bytes) {
   // upper bound: the request lists count even when they travel as kernel parameters
   size_t a = align256(sizeof(DecodeReq) * pb.dec.size()) + align256(4 * pb.dec_pre.size()) +
              align256(sizeof(MergeReq) * pb.mrg.size()) + align256(4 * pb.mrg_pre.size()) +
-             align256(sizeof(TileItem) * pb.tile.size()) + align256(4 * pb.row_list.size()) + 6 * 256;
+             align256(sizeof(TileItem) * pb.tile.size()) + align256(4 * pb.row_list.size()) +
+             align256(sizeof(MergeReq) * pb.mrg_red.size()) + align256(4 * pb.mrg_red_pre.size()) +
+             align256(sizeof(FoldReq) * pb.fold.size()) + align256(8 * (size_t)pb.n_casc_items) + 10 * 256;
   if (arrays_bytes) *arrays_bytes = a;
   return a + align256((size_t)pb.n_slots * d * 4) + align256((size_t)pb.n_slots * 4);
 }
@@ -1018,11 +1051,19 @@ static kva_status plan_impl(kva_pool *p, const kva_batch_desc *b, void *ws, size
     std::copy(pb.mrg.begin(), pb.mrg.end(), pl->mrg.req);
     std::copy(pb.mrg_pre.begin(), pb.mrg_pre.end(), pl->mrg.pre);
   }
+  const bool has_fold = !pb.fold.empty();
+  const bool mrg_red_inline = pb.mrg_red.size() <= (size_t)kInlineReqs;
+  pl->mrg_red.n = (int32_t)pb.mrg_red.size();
+  if (has_fold && mrg_red_inline) {
+    std::copy(pb.mrg_red.begin(), pb.mrg_red.end(), pl->mrg_red.req);
+    std::copy(pb.mrg_red_pre.begin(), pb.mrg_red_pre.end(), pl->mrg_red.pre);
+  }
   const bool tile_inline = pb.tile.size() <= (size_t)kInlineTiles;
   pl->tiles.n = (int32_t)pb.tile.size();
   pl->tiles.ptr = nullptr;
   if (tile_inline) std::copy(pb.tile.begin(), pb.tile.end(), pl->tiles.item);
-  const bool need_upload = (!pb.tile.empty() && !tile_inline) || !pb.row_list.empty() || !dec_inline || !mrg_inline;
+  const bool need_upload = (!pb.tile.empty() && !tile_inline) || !pb.row_list.empty() || !dec_inline || !mrg_inline ||
+                           has_fold;
   hs.lap("plan.inline_copy");
   if (need_upload) {
     std::lock_guard<std::mutex> lk(p->up_mu);
@@ -1050,6 +1091,16 @@ static kva_status plan_impl(kva_pool *p, const kva_batch_desc *b, void *ws, size
     if (!mrg_inline) {
       pl->mrg.ptr = reinterpret_cast<const MergeReq *>(put(pb.mrg.data(), sizeof(MergeReq) * pb.mrg.size()));
       pl->mrg.pre_ptr = reinterpret_cast<const int32_t *>(put(pb.mrg_pre.data(), 4 * pb.mrg_pre.size()));
+    }
+    if (has_fold) {  // the fold list, zeroed completion counters, the reduced merge list if large
+      pl->p.fold = reinterpret_cast<const FoldReq *>(put(pb.fold.data(), sizeof(FoldReq) * pb.fold.size()));
+      const std::vector<uint32_t> zeros(2 * (size_t)pb.n_casc_items, 0u);
+      pl->p.fold_flags = reinterpret_cast<unsigned *>(put(zeros.data(), 4 * zeros.size()));
+      if (!mrg_red_inline) {
+        pl->mrg_red.ptr = reinterpret_cast<const MergeReq *>(put(pb.mrg_red.data(), sizeof(MergeReq) * pb.mrg_red.size()));
+        pl->mrg_red.pre_ptr = reinterpret_cast<const int32_t *>(put(pb.mrg_red_pre.data(), 4 * pb.mrg_red_pre.size()));
+      }
+      pl->has_fold = true;
     }
     // upload on the side stream, ordered after everything already enqueued on `stream`
     // (WAR on the workspace), so the decode launch on `stream` does not queue behind a
@@ -1103,6 +1154,7 @@ static kva_status plan_impl(kva_pool *p, const kva_batch_desc *b, void *ws, size
   pl->n_dec = pb.dec_pre.back() * b->num_kv_heads;
   pl->n_tile = (int)pb.tile.size();
   pl->n_mrows = pb.mrg_pre.back() * b->num_kv_heads;
+  pl->n_mrows_red = pb.mrg_red_pre.back() * b->num_kv_heads;
   AttnParams &ap = pl->p;
   ap.k_pool = static_cast<const uint16_t *>(p->desc.k_pool);
   ap.v_pool = static_cast<const uint16_t *>(p->desc.v_pool);
@@ -1196,8 +1248,16 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   const bool do_tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0;
   const bool do_dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
   const bool fork = do_tile && do_dec && pl->overlap;
+  const bool pdl_mode = opt(kOptPdl) != 0;
+  // the plan's fold (decode-epilogue merge of cascade members) needs the tile kernel resident
+  // before the decode kernel: only in the one-stream PDL mode with both kernels in this run
+  // (and the merge in the same run: it then uses the list without the folded requests)
+  const bool fold = fork && pdl_mode && pl->has_fold && (phases & KVA_PHASE_MERGE) && opt(kOptFold) != 0;
+  if (do_tile) ++pl->runs;  // the epoch the tile kernel's fold counters reach in this run
+  p.epoch = pl->runs;
+  p.fold_on = fold ? 1 : 0;
   cudaStream_t ts = s;
-  if (fork) {  // tile kernel first on the high-priority side stream, then decode on `s`
+  if (fork && !pdl_mode) {  // tile kernel first on the high-priority side stream, then decode on `s`
     CUDA_TRY(cudaEventRecord(pl->ev_fork, s));
     CUDA_TRY(cudaStreamWaitEvent(pl->aux, pl->ev_fork, 0));
     ts = pl->aux;
@@ -1238,7 +1298,6 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
   // the decode kernel (programmatic dependent launch) start on the remaining SMs.  This fixes
   // the SM split: with two streams the decode kernel's 2-CTA/SM grid could be dispatched first
   // and hold every SM until its first wave retired.  Timing events bracket the pair.
-  const bool pdl_mode = opt(kOptPdl) != 0;
   if (fork && pdl_mode) {
     if (wait_upload(true) != KVA_OK || wait_append() != KVA_OK) return KVA_ERR_CUDA;
     if (pl->t_ev[0]) CUDA_TRY(cudaEventRecord(pl->t_ev[0], s));
@@ -1252,7 +1311,9 @@ extern "C" kva_status hybrid_attention_run_phases(const kva_plan *pl, const void
     hs.lap("run.launch_decode");
     if (pl->t_ev[1]) CUDA_TRY(cudaEventRecord(pl->t_ev[1], s));
     if (pl->t_ev[3]) CUDA_TRY(cudaEventRecord(pl->t_ev[3], s));
-    if ((phases & KVA_PHASE_MERGE) && pl->n_mrows > 0) CUDA_TRY(launch_merge(p, pl->mrg, pl->n_mrows, s));
+    const ReqList<MergeReq> &mrg = fold ? pl->mrg_red : pl->mrg;
+    const int n_mrows = fold ? pl->n_mrows_red : pl->n_mrows;
+    if ((phases & KVA_PHASE_MERGE) && n_mrows > 0) CUDA_TRY(launch_merge(p, mrg, n_mrows, s));
     // the decode kernel does not wait for the tile kernel: when it is the last kernel of the
     // run, a join kernel ends it, so the completion of the run's last kernel implies the tile
     // kernel's (the next kv_truncate / kv_append are programmatic dependents that wait only
@@ -1321,9 +1382,11 @@ extern "C" kva_status kva_plan_set_timing_events(kva_plan *pl, void *tile_begin,
 extern "C" kva_status kva_plan_launch_count(const kva_plan *pl, int32_t phases, int32_t *n) {
   if (!pl || !n) return fail(KVA_ERR_INVALID, "null argument");
   const bool tile = (phases & KVA_PHASE_TILE) && pl->n_tile > 0, dec = (phases & KVA_PHASE_DECODE) && pl->n_dec > 0;
-  const bool merge = (phases & KVA_PHASE_MERGE) && pl->n_mrows > 0;
+  const bool pdl_fork = tile && dec && pl->overlap && opt(kOptPdl) != 0;
+  const bool fold = pdl_fork && pl->has_fold && (phases & KVA_PHASE_MERGE) && opt(kOptFold) != 0;
+  const bool merge = (phases & KVA_PHASE_MERGE) && (fold ? pl->n_mrows_red : pl->n_mrows) > 0;
   // + the join kernel that ends an overlapped PDL run without a merge (hybrid_attention_run)
-  const bool join = tile && dec && pl->overlap && opt(kOptPdl) != 0 && !merge;
+  const bool join = pdl_fork && !merge;
   *n = tile + dec + merge + join;
   return KVA_OK;
 }

@@ -21,7 +21,7 @@ def _mixed(d, Hq, Hkv):
     return W.make_workload(W.custom_config("v", Hq, Hkv, d, 7, reqs, [600 // 16]))
 
 
-MODES = {"pdl": dict(overlap=1, pdl=1), "two_streams": dict(overlap=1, pdl=0),
+MODES = {"pdl": dict(overlap=1, pdl=1), "pdl_fold": dict(overlap=1, pdl=1, fold=1), "two_streams": dict(overlap=1, pdl=0),
          "sequential": dict(overlap=0), "tile40": dict(overlap=1, tile_ctas=40),
          "tile1": dict(overlap=1, tile_ctas=1)}
 
@@ -121,3 +121,32 @@ def test_truncate_after_a_run_without_merge_waits_for_the_tile_kernel():
             K.kv_truncate(pool, batch, keep)
             torch.cuda.synchronize()
         assert_attention_close(out, lse, r["out"], r["lse"])
+
+
+def test_fold_merges_members_in_the_decode_epilogue():
+    """Option fold: the decode-class members of a one-level group whose suffix is one split
+    merge their suffix partial with the cascade partial in the decode kernel's epilogue (waiting
+    on the tile kernel's per-item completion counters); the merge kernel gets the remaining
+    requests.  Results equal the merge-kernel path bit-exactly and the oracle within
+    tolerance, across repeated runs of one plan (the counters' epochs) and a tile kernel on one
+    CTA (the decode warps wait for it)."""
+    import paper_2504_03651_b200 as K
+    wl = _mixed(128, 16, 2)
+    r = oracle_step(wl)
+    dev = "cuda"
+    outs = []
+    for opts in (dict(fold=0), dict(fold=1), dict(fold=1, tile_ctas=1)):
+        with K.options(overlap=1, pdl=1, **opts):
+            pool = K.Pool(wl.k_pool.to(dev), wl.v_pool.to(dev), K.free_bits_tensor(wl.free_bits, dev))
+            batch = K.Batch(wl.batch, dev)
+            plan = K.kv_append_plan(pool, batch, wl.k_new.to(dev), wl.v_new.to(dev))
+            q = wl.q.to(dev)
+            for _ in range(3):
+                out = torch.full(q.shape, float("nan"), dtype=torch.float32, device=dev)
+                lse = torch.full(q.shape[:2], float("nan"), dtype=torch.float32, device=dev)
+                plan.run(q, out, lse)
+                torch.cuda.synchronize()
+                assert_attention_close(out, lse, r["out"], r["lse"])
+                outs.append((out.cpu().numpy(), lse.cpu().numpy()))
+    for o, l in outs[1:]:
+        assert np.array_equal(o, outs[0][0]) and np.array_equal(l, outs[0][1])
