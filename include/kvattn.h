@@ -26,9 +26,10 @@
  *     owns only its opaque handles, host planning scratch and pinned staging buffers.
  *   - bf16 = IEEE bfloat16 bit pattern (uint16).  Block size is fixed at 16 tokens
  *     (reading #5).  head_dim must be 64 or 128 (else KVA_ERR_UNSUPPORTED).
- *   - Single writer per pool: calls on one pool (kv_append, hybrid_attention_plan /
- *     _run, kv_release_blocks, evict_select with apply, kv_pool_*) must be serialised by the
- *     caller; the library does not lock them (it only guards its upload staging ring).
+ *   - Single writer per pool: calls on one pool (kv_append, kv_append_plan,
+ *     hybrid_attention_plan / _run, kv_release_blocks, kv_truncate, evict_select with apply,
+ *     kv_pool_*) must be serialised by the caller, and so must the runs of one plan; the library
+ *     does not lock them (it only guards its upload staging ring).
  *   - *_workspace_size calls validate the descriptor exactly as the call they size does (minus
  *     the block-id range, which needs the pool) and return that status on error.
  */
