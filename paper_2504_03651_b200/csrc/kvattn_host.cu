@@ -456,6 +456,14 @@ static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
     return fail(KVA_ERR_INVALID, "q_indptr, ctx_len, block_table and block_table_host are required");
   if (b->max_blocks <= 0) return fail(KVA_ERR_INVALID, "max_blocks <= 0");
   if (b->q_indptr[0] != 0) return fail(KVA_ERR_INVALID, "q_indptr[0] != 0");
+  // a group member's prefix entries equal its group's first member's (checked below, entry by
+  // entry), so only the first member of each group range-checks them
+  const int Gv = b->group_of ? std::max(b->num_groups, 0) : 0;
+  std::vector<int> first_of(Gv, -1);
+  for (int i = 0; i < b->num_reqs && Gv > 0; ++i) {
+    const int gi = b->group_of[i];
+    if (gi >= 0 && gi < Gv && first_of[gi] < 0) first_of[gi] = i;
+  }
   for (int i = 0; i < b->num_reqs; ++i) {
     const int ql = qlen(b, i), ctx = b->ctx_len[i];
     if (ql < 1 || ql > ctx) return fail(KVA_ERR_INVALID, "request %d: q_len %d not in [1, ctx=%d]", i, ql, ctx);
@@ -463,8 +471,11 @@ static kva_status validate_batch(const kva_batch_desc *b, int nb, int mode) {
       return fail(KVA_ERR_INVALID, "request %d: ctx %d > max_blocks*16", i, ctx);
     const int need_blocks = mode == 0 ? cdiv(ctx, kBlock) : cdiv(ctx - ql, kBlock);
     const int32_t *row = b->block_table_host + (int64_t)i * b->max_blocks;
+    const int gi = Gv > 0 ? b->group_of[i] : -1;
+    const int k0 = (gi >= 0 && gi < Gv && first_of[gi] != i && b->group_prefix_blocks)
+                       ? std::max(0, std::min(b->group_prefix_blocks[gi], need_blocks)) : 0;
     uint32_t bad = 0;  // branch-free (vectorised) range check; the slow path names the entry
-    for (int k = 0; k < need_blocks; ++k) bad |= (uint32_t)row[k] >= (uint32_t)nb;
+    for (int k = k0; k < need_blocks; ++k) bad |= (uint32_t)row[k] >= (uint32_t)nb;
     if (bad)
       for (int k = 0; k < need_blocks; ++k)
         if (row[k] < 0 || row[k] >= nb)
@@ -770,6 +781,7 @@ struct PlanBuild {
 };
 
 static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
+  HSection hb;
   const int kTileM = 2 * kTileMTc;  // rows per tile item: the tcgen05 kernel's two Q tiles
   const int R = b->num_reqs, Hkv = b->num_kv_heads, Hq = b->num_q_heads, g = Hq / Hkv;
   const int d = b->head_dim;
@@ -831,6 +843,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
       pb.n_slots += group_rows[gi];
     }
   }
+  hb.lap("build.cascade");
   // the merge lists a level only if it has a tile (blocks of its own)
   auto level_has_tile = [&](int gi) {
     const int kstart = parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] * kBlock : 0;
@@ -848,7 +861,13 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     pb.dec_pre.reserve(nd + 1);
     pb.mrg.reserve(nm);
     pb.mrg_pre.reserve(nm + 1);
+    pb.mrg_red.reserve(nm);
+    pb.mrg_red_pre.reserve(nm + 1);
+    pb.fold.reserve(nm);
   }
+  // a member's position in its level's member list: the members are listed in request order,
+  // so a running cursor per level replaces the binary search
+  std::vector<int> cursor(G, 0);
   int64_t kv_tokens = 0, dec_keys = 0, dec_rows = 0;
   for (int gi = 0; gi < G; ++gi)  // each level's own blocks once
     kv_tokens += (int64_t)(b->group_prefix_blocks[gi] - (parent(gi) >= 0 ? b->group_prefix_blocks[parent(gi)] : 0)) * kBlock;
@@ -887,10 +906,14 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
         mq.rows = rows;
         mq.n_casc = 0;
         // level l's partial of (head h, row r): casc_base[l] + h * group_rows[l] + off * g + r
+        int pos0 = 0;  // position in the deepest level's member list
         for (int l = cascaded ? gi : -1; l >= 0; l = parent(l)) {
-          if (!level_has_tile(l)) continue;
           const auto &mv = members[l];
-          const size_t pos = std::lower_bound(mv.begin(), mv.end(), i) - mv.begin();
+          int &cur = cursor[l];
+          while (cur < (int)mv.size() && mv[cur] < i) ++cur;  // members[l] is ascending
+          const int pos = cur;
+          if (l == gi) pos0 = pos;
+          if (!level_has_tile(l)) continue;
           mq.casc_slot[mq.n_casc] = (int32_t)(casc_base[l] + (int64_t)member_off[l][pos] * g);
           mq.casc_hstride[mq.n_casc] = group_rows[l];
           ++mq.n_casc;
@@ -902,12 +925,10 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
         // fold: a member of a one-level group whose suffix is one split (the decode warp owns
         // the whole suffix partial and merges it with the cascade partial itself)
         if (cascaded && parent(gi) < 0 && level_has_tile(gi) && nsplit == 1 && mq.n_casc == 1) {
-          const auto &mv = members[gi];
-          const size_t pos = std::lower_bound(mv.begin(), mv.end(), i) - mv.begin();
           FoldReq fr{};
           fr.casc_slot = mq.casc_slot[0];
           fr.casc_hstride = mq.casc_hstride[0];
-          fr.member_row0 = member_off[gi][pos] * g;
+          fr.member_row0 = member_off[gi][pos0] * g;
           fr.flag_base = flag_base[gi];
           fr.mtiles = mtiles[gi];
           pb.dec.back().fold = (int32_t)pb.fold.size();  // (dq was pushed above)
@@ -937,6 +958,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
       }
     }
   }
+  hb.lap("build.requests");
   // longest tiles first (LPT); ties keep (kv_head, m-tile, member) order so concurrently
   // running CTAs of a group share its prefix blocks in L2
   // F(x) = sum_{r<x} floor(r/g) (closed form), so a causal tile's visible keys are exact
@@ -970,6 +992,7 @@ static void build_plan(const kva_batch_desc *b, PlanBuild &pb) {
     pb.dec.swap(dec);
     pb.dec_pre.swap(pre);
   }
+  hb.lap("build.sort");
   pb.stats.n_decode_items = (int64_t)pb.dec_pre.back() * Hkv;  // (split, head) units
   pb.stats.n_tile_items = (int64_t)pb.tile.size();
   pb.stats.n_merge_rows = (int64_t)pb.mrg_pre.back() * Hkv;
@@ -1187,7 +1210,9 @@ extern "C" kva_status kv_append_plan(kva_pool *p, kva_batch_desc *b, const void 
   // one validation (the append's: the resident part; the plan reads no block id, and the
   // append itself writes every new position's entry), then the plan — so a plan error leaves
   // the pool untouched — then the append (its own errors: the plan is destroyed)
+  HSection hs;
   kva_status st = validate_desc(p, b, 1);
+  hs.lap("append_plan.validate");
   if (st != KVA_OK) return st;
   kva_plan *pl = nullptr;
   if ((st = plan_impl(p, b, ws_attn, ws_attn_bytes, stream, &pl, true)) != KVA_OK) return st;
