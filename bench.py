@@ -550,6 +550,12 @@ def run_ours(args, rank, world, local):
     planA.close()
     evict_threads = int(os.environ.get("KVA_BENCH_EVICT_THREADS", "256" if dec_est_us > 4 * 50.0 else "512"))
     K.set_option("evict_threads", evict_threads)
+    # the same rule for the eviction stream's schedule: beside a long decode-bound step its cost
+    # is a throughput tax, spread best as one pass per step (forked at the step's start: llama7b
+    # 20 steps 387 -> 382, 50 steps 380 -> 378.5 us/step); where its latency is on the loop
+    # (qwen14b) the passes run back to back (pipelined: 135.7 vs 144.9 with a fork per step)
+    if "KVA_BENCH_EVICT_PIPELINE" not in os.environ:
+        evict_pipeline = evict_threads != 256
     for _ in range(max(args.warmup, R)):  # every replica warmed
         step()
     barrier()
@@ -709,7 +715,7 @@ def run_ours(args, rank, world, local):
                    "flops_per_rank": stats["flops"],
                    "step": "kv_append+hybrid_attention(plan,tile,decode,merge)" +
                            ("+allgather" if world > 1 else "") + ("" if args.no_evict else "+kv_manager_step(1M blocks: 49k transitions, rc +-91k refs, keys)+evict_select(k=64k)" +
-                            (" [eviction pass pipelined: issued after the previous step's selection]" if (ev is not None and evict_pipeline) else "")) +
+                            ((" [eviction pass pipelined: issued after the previous step's selection]" if evict_pipeline else " [eviction pass forked at each step's start]") if ev is not None else "")) +
                            "+kv_truncate(rollback of the step's allocations)",
                    "l2": (f"{R} replicas of every per-step input (pool, tables, Q/K/V, workspaces, manager "
                           f"metadata, keys) cycled step by step (KV working set %.2f GB/rank per replica)"
