@@ -586,6 +586,20 @@ def run_ours(args, rank, world, local):
                 ts = ts[ts > 0]
                 sys.stderr.write(f"[timeline] sel phases (replica {j}, us): {[round(float(x) / 1e3, 1) for x in np.diff(ts)]}\n")
     gpu_launches = launches["n"]
+    # the block metadata is replicated, so every rank's eviction order must be
+    # bit-identical — an order-sensitive checksum of replica 0's last selection, min == max
+    # over ranks
+    evict_identical = None
+    if world > 1 and reps[0]["ev"] is not None:
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        ids = reps[0]["ev"]["ids"].to(torch.int64)
+        h = (ids * torch.arange(1, ids.numel() + 1, device=dev, dtype=torch.int64)).sum().reshape(1)
+        lo_h, hi_h = h.clone(), h.clone()
+        dist.all_reduce(lo_h, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi_h, op=dist.ReduceOp.MAX)
+        evict_identical = bool(lo_h.item() == hi_h.item())
+        assert evict_identical, "eviction orders differ across ranks"
     ck = clocks.stop() if not args.profile else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
     ms_same = None
     if R > 1 and not args.profile:  # the same steps on replica 0 only (the delta L2 reuse buys)
@@ -723,6 +737,7 @@ def run_ours(args, rank, world, local):
                          "no rotation (--l2-rotate 1): KV working set %.2f GB/rank" % (stats["kv_bytes_algorithmic"] / 1e9),
                    "ms_per_step_without_l2_rotation": ms_same,
                    "evict_threads": evict_threads,
+                   "eviction_identical_across_ranks": evict_identical,
                    "decode_kernel_ms": dec_avg, "out_dtype": args.out_dtype,
                    "tile_kernel_ms": statistics.mean(tile_ms) if tile_ms else None,
                    "tile_kernel_tflops": (stats["tile_flops"] / (statistics.mean(tile_ms) * 1e-3) / 1e12) if tile_ms else None,
