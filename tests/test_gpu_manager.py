@@ -247,3 +247,31 @@ def test_manager_step_select_fused_full_size(ctas, threads):
     _, rids = oracle.evict_select(rkeys, ev.k)
     assert cnt == len(rids)
     assert np.array_equal(ids.cpu().numpy(), rids)
+
+
+def test_manager_step_select_fused_unaligned_metadata():
+    """The fused kernel's key pass on metadata views that are not 16-B aligned (every block by
+    the scalar path) and an odd block count: bit-exact against the oracle."""
+    rng = np.random.default_rng(77)
+    n = 20001
+    state = rng.integers(0, 6, n + 1).astype(np.uint8)
+    lat = rng.integers(0, 1 << 20, n + 1).astype(np.uint32)
+    depth = rng.integers(0, 64, n + 1).astype(np.uint16)
+    rc = np.zeros(n + 1, np.uint32)
+    d_state, d_lat, d_rc = _dev(state, np.uint8)[1:], _dev(lat, np.int32)[1:], _dev(rc, np.int32)[1:]
+    d_depth = _dev(depth, np.int16)[1:]
+    mgr = K.ManagerStep(d_state, d_rc, d_lat, d_depth)
+    st_h, lat_h, dep_h, rc_h = state[1:].copy(), lat[1:].copy(), depth[1:].copy(), rc[1:].copy()
+    for it in range(2):
+        now = (1 << 20) + it
+        chains = [(int(rng.integers(0, 6)), rng.choice(n, int(rng.integers(1, 300)), replace=False)) for _ in range(5)]
+        pool = [rng.choice(n, int(rng.integers(1, 60)), replace=False) for _ in range(10)]
+        pool_ids = torch.from_numpy(np.concatenate(pool).astype(np.int32)).cuda()
+        k = 3000
+        keys, ids, cnt = _fused_select(mgr, now, chains, pool_ids, k, n)
+        st, st_h, rc_h, lat_h, rkeys, nact = oracle.manager_step(st_h, rc_h, lat_h, dep_h, now, chains, pool)
+        assert st == oracle.OK
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), rkeys)
+        assert int(mgr.n_active.item()) == nact
+        _, rids = oracle.evict_select(rkeys, k)
+        assert cnt == len(rids) and np.array_equal(ids[:cnt].cpu().numpy(), rids)
