@@ -160,3 +160,36 @@ def test_workspace_size_validates_groups(K):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stderr
     assert r.stdout.split() == [str(K.ERR_GROUP)] * (2 * len(cases)), r.stdout
+
+
+def test_member_prefix_entries_checked_through_the_first_member(K):
+    """Only a group's first member range-checks its prefix entries; another member's prefix
+    entries are checked equal to them, so an out-of-range entry there is still rejected."""
+    reqs = [W.ReqSpec(W.OFFLINE_DECODE, 90, 1, 0), W.ReqSpec(W.OFFLINE_DECODE, 95, 1, 0),
+            W.ReqSpec(W.ONLINE_DECODE, 40, 1)]
+    wl = W.make_workload(W.custom_config("m", 4, 2, 64, 15, reqs, [3]), preappended=True)
+    nb = wl.batch["num_blocks"]
+    assert K.validate_batch(_batch(K, wl), nb, 0) == K.OK
+    for row, want in ((1, K.ERR_GROUP), (0, K.ERR_INVALID)):
+        bt = wl.batch["block_table"].copy()
+        bt[row, 1] = nb + 7
+        assert K.validate_batch(_batch(K, wl, block_table=bt), nb, 0) == want, row
+
+
+def test_options_evict_threads_fold_span_ring(K):
+    """kva_set_option: evict_threads accepts 256 / 512 only; fold and span_ring round-trip."""
+    try:
+        for v in (256, 512):
+            K.set_option("evict_threads", v)
+            assert K.get_option("evict_threads") == v
+        with pytest.raises(K.KvaError):
+            K.set_option("evict_threads", 300)
+        assert K.get_option("evict_threads") == 512
+        for name, v in (("fold", 1), ("fold", 0), ("span_ring", 0)):
+            K.set_option(name, v)
+            assert K.get_option(name) == v
+        with pytest.raises(K.KvaError):
+            K.set_option("no_such_option", 1)
+    finally:
+        K.set_option("evict_threads", 512)
+        K.set_option("fold", 0)
